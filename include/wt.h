@@ -1,0 +1,184 @@
+/*
+ * wt.h -- C ABI of the B200-native levelwise wavelet-tree builder
+ * (libwt.so, package paper_1610_05994_b200).
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, "P:n" = line n):
+ *   the one-pointer-per-level wavelet tree (Fig. 1b) of a sequence
+ *   S[0..n) over the contiguous alphabet [0, sigma), i.e. for each
+ *   of the L = ceil(lg sigma) levels (L = 0 when sigma == 1):
+ *     - the level bitmap B_l: bit (L-1-l) of every symbol, taken in the order
+ *       of S stably sorted by the symbol's top l bits (Prop. 1, P:485-490;
+ *       node of s at level l is s >> (L-l); Alg. 1 lines 8-13);
+ *     - the rank directory of B_l (createRankSelect, Alg. 1 line 14):
+ *       one 64-bit cumulative popcount per 512-bit block;
+ *   and the node offsets C (the prefix-summed counters of Alg. 1 lines 5-7,
+ *   P:539-543, at the leaf granularity): C[c] = #{j : S[j] < c}, c in [0, 2^L].
+ *
+ * Output layout (the parity contract; the oracle emits the identical bytes):
+ *   bitmaps      uint32[L * words_per_level], level-major.  Bit q of level l is
+ *                (bitmaps[l*words_per_level + q/32] >> (q%32)) & 1 (LSB-first).
+ *                words_per_level = 16*ceil(n/512); bits >= n are zero.
+ *   superblocks  uint64[L * sb_per_level], sb_per_level = ceil(n/512) + 1.
+ *                superblocks[l*sb_per_level + t] = popcount of level-l bits in
+ *                [0, min(512 t, n)); the last entry is the level's total ones.
+ *   node_offsets uint64[2^L + 1].  Level-l node v spans positions
+ *                [node_offsets[v << (L-l)], node_offsets[(v+1) << (L-l)]).
+ *
+ * Conventions: 0-based positions; bit 0 = left child, 1 = right child
+ * (P:293-296); access/rank are the paper's traversals with
+ * INCLUSIVE rank ("i = rank1(B,24) - 1 = 7").
+ *
+ * Ownership: every d_ pointer is DEVICE memory owned by the caller (e.g. torch
+ * tensors); every h_ pointer is host memory owned by the caller.  The library
+ * allocates nothing, keeps no global state (only a thread-local last-error
+ * string and thread-local profiling events), never retains a pointer after a
+ * call's work has completed on the stream, and is stream-ordered: all device
+ * work is enqueued on `stream`.  Concurrent builds on different streams need
+ * different workspaces.  A finished tree is immutable; queries on it may run
+ * concurrently.
+ *
+ * Errors: status codes only -- no exceptions, aborts or printing.
+ */
+#ifndef WT_H_
+#define WT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Layout-compatible with cudaStream_t (a CUstream_st*); NULL = legacy default stream. */
+typedef struct CUstream_st* wt_stream_t;
+/* Layout-compatible with cudaEvent_t. */
+typedef struct CUevent_st* wt_event_t;
+
+typedef enum {
+  WT_OK = 0,
+  WT_ERR_ARG = 1,           /* bad width / sigma / n / pointer / alignment */
+  WT_ERR_SYMBOL_RANGE = 2,  /* some S[j] >= sigma; outputs unspecified */
+  WT_ERR_INDEX = 3,         /* query position >= n, or symbol >= sigma, or ordinal out of range */
+  WT_ERR_CUDA = 4,          /* a CUDA runtime call or launch failed (see wt_last_error) */
+  WT_ERR_WORKSPACE = 5      /* workspace NULL or smaller than wt_sizes().workspace_bytes */
+} wt_status;
+
+typedef struct {
+  uint32_t levels;           /* L = ceil(lg sigma); 0 when sigma == 1 */
+  uint32_t width;            /* bytes per input symbol (1, 2 or 4) */
+  uint64_t words_per_level;  /* uint32 words per level bitmap = 16*ceil(n/512) */
+  uint64_t sb_per_level;     /* uint64 superblock entries per level = ceil(n/512) + 1 */
+  uint64_t c_len;            /* uint64 node offsets = 2^L + 1 */
+  uint64_t bitmap_bytes;     /* 4 * L * words_per_level */
+  uint64_t superblock_bytes; /* 8 * L * sb_per_level */
+  uint64_t node_offset_bytes;/* 8 * c_len */
+  size_t workspace_bytes;    /* device scratch wt_build needs (ping-pong permuted
+                                sequences T_l, node tables, scan state, flag) */
+  size_t host_workspace_bytes; /* device scratch wt_build_from_host needs: the
+                                workspace plus a device copy of S and of the tree */
+} wt_sizes_t;
+
+/* A tree in memory the caller owns (device pointers for the device API, host
+ * pointers for the *_from_host output). */
+typedef struct {
+  uint32_t* bitmaps;
+  uint64_t* superblocks;
+  uint64_t* node_offsets;
+} wt_tree_t;
+
+/*
+ * wt_sizes: sizes of every output and of the workspace for a build of n
+ * symbols of `width` bytes over [0, sigma).  Pure host arithmetic.
+ * Errors: WT_ERR_ARG if width not in {1,2,4}, sigma == 0,
+ * sigma > 2^(8*width), L > 30, or out == NULL.
+ */
+wt_status wt_sizes(uint64_t n, uint64_t sigma, uint32_t width, wt_sizes_t* out);
+
+/*
+ * wt_build_async: enqueue the whole construction on `stream`:
+ *   a1 histogram + symbol-range check, a2 exclusive scan -> node_offsets and
+ *   the per-level node tables, a3 one stable bit-partition pass per level
+ *   l < L-1 (bitmap words, superblocks, T_{l+1}), a4 the last level
+ *   (bitmap + superblocks).  No host synchronisation; CUDA-graph capturable.
+ * d_seq       n symbols, little-endian, `width` bytes each; 16-byte aligned
+ *             (any torch/cudaMalloc allocation is).  Read only.
+ * out         device pointers sized per wt_sizes (bitmaps, superblocks,
+ *             node_offsets); fully overwritten.
+ * d_workspace >= wt_sizes().workspace_bytes of device memory, 256-byte aligned;
+ *             contents on entry are irrelevant.
+ * d_status    optional (may be NULL): receives WT_OK or WT_ERR_SYMBOL_RANGE
+ *             (int32) when the stream reaches the end of the build.
+ * Returns WT_ERR_ARG / WT_ERR_WORKSPACE on bad arguments (nothing enqueued),
+ * WT_ERR_CUDA if a launch failed, else WT_OK.
+ */
+wt_status wt_build_async(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t width,
+                         const wt_tree_t* out, void* d_workspace, size_t workspace_bytes,
+                         int32_t* d_status, wt_stream_t stream);
+
+/*
+ * wt_build: wt_build_async, then one stream synchronisation to read the
+ * range-check flag.  Returns WT_ERR_SYMBOL_RANGE if any S[j] >= sigma.
+ */
+wt_status wt_build(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t width,
+                   const wt_tree_t* out, void* d_workspace, size_t workspace_bytes,
+                   wt_stream_t stream);
+
+/*
+ * wt_build_from_host: end-to-end build from HOST memory.  Copies h_seq
+ * (n*width bytes, ideally pinned) to the device, builds, and copies the tree
+ * back into the host buffers of h_out (sizes per wt_sizes), all on `stream`,
+ * then synchronises.  d_workspace >= wt_sizes().host_workspace_bytes.
+ * Errors as wt_build.
+ */
+wt_status wt_build_from_host(const void* h_seq, uint64_t n, uint64_t sigma, uint32_t width,
+                             const wt_tree_t* h_out, void* d_workspace, size_t workspace_bytes,
+                             wt_stream_t stream);
+
+/*
+ * wt_access: d_sym[k] = S[d_pos[k]] for k < m, by the top-down traversal of
+ * P:353-380 simulated with rank on the level bitmaps.
+ * tree: device pointers of a finished build of (n, sigma).
+ * Positions >= n get d_sym[k] = UINT32_MAX and set *d_status = WT_ERR_INDEX
+ * (d_status optional; initialise it to WT_OK yourself).  Asynchronous.
+ */
+wt_status wt_access(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint64_t* d_pos,
+                    uint64_t m, uint32_t* d_sym, int32_t* d_status, wt_stream_t stream);
+
+/*
+ * wt_rank: d_cnt[k] = #{ j <= d_pos[k] : S[j] == d_c[k] } (inclusive rank,
+ * P:279-281).  Pairs with pos >= n or c >= sigma get UINT64_MAX and set
+ * *d_status = WT_ERR_INDEX.  Asynchronous.
+ */
+wt_status wt_rank(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint32_t* d_c,
+                  const uint64_t* d_pos, uint64_t m, uint64_t* d_cnt, int32_t* d_status,
+                  wt_stream_t stream);
+
+/*
+ * wt_select: d_out[k] = position of the d_j[k]-th (1-based) occurrence of
+ * d_c[k] in S, by the bottom-up traversal.  Invalid pairs
+ * (c >= sigma, j == 0, j > occurrences of c) get UINT64_MAX and set
+ * *d_status = WT_ERR_INDEX.  Asynchronous.
+ */
+wt_status wt_select(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint32_t* d_c,
+                    const uint64_t* d_j, uint64_t m, uint64_t* d_out, int32_t* d_status,
+                    wt_stream_t stream);
+
+/* Kernel launches one wt_build_async(n, sigma, width) enqueues, and their kinds
+ * (kinds may be NULL): 1 histogram, 2 scan, 3 node tables, 4 level pass with
+ * scatter (a3), 5 last level (a4), 6 memset. */
+uint32_t wt_launch_plan(uint64_t n, uint64_t sigma, uint32_t width, uint32_t* kinds, uint32_t cap);
+
+/* Profiling hook (thread-local): when events != NULL, the next wt_build_async
+ * calls on this thread record events[2k] before and events[2k+1] after launch
+ * k (k < count/2) on the build stream.  Pass NULL to disable. */
+void wt_set_profile_events(wt_event_t* events, uint32_t count);
+
+const char* wt_status_string(wt_status status);
+/* Detail of the last error on this thread ("" if none). */
+const char* wt_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WT_H_ */

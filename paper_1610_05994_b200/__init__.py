@@ -1,0 +1,301 @@
+"""paper_1610_05994_b200 -- B200-native levelwise wavelet-tree construction
+(arXiv 1610.05994, "Parallel Construction of Wavelet Trees on Multicore
+Architectures"), as hand-written sm_100a CUDA behind the C ABI of
+``include/wt.h`` (``libwt.so``).
+
+This module is argument marshalling only: it allocates device memory with
+torch, passes raw pointers and the current CUDA stream to the C ABI, and wraps
+the results.  Every step of the build runs in the library's kernels; there is
+no CPU fallback -- importing fails loudly if ``libwt.so`` is missing.
+
+Names follow the C ABI: ``sizes``, ``build`` / ``build_async``,
+``build_from_host``, ``access``, ``rank``, ``select``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwt.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is deliberately no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+WT_OK, WT_ERR_ARG, WT_ERR_SYMBOL_RANGE, WT_ERR_INDEX, WT_ERR_CUDA, WT_ERR_WORKSPACE = range(6)
+KIND_NAMES = {1: "hist", 2: "scan", 3: "tables", 4: "level", 5: "last_level"}
+
+
+class WtSizes(ctypes.Structure):
+    _fields_ = [
+        ("levels", ctypes.c_uint32),
+        ("width", ctypes.c_uint32),
+        ("words_per_level", ctypes.c_uint64),
+        ("sb_per_level", ctypes.c_uint64),
+        ("c_len", ctypes.c_uint64),
+        ("bitmap_bytes", ctypes.c_uint64),
+        ("superblock_bytes", ctypes.c_uint64),
+        ("node_offset_bytes", ctypes.c_uint64),
+        ("workspace_bytes", ctypes.c_size_t),
+        ("host_workspace_bytes", ctypes.c_size_t),
+    ]
+
+
+class WtTree(ctypes.Structure):
+    _fields_ = [("bitmaps", ctypes.c_void_p), ("superblocks", ctypes.c_void_p),
+                ("node_offsets", ctypes.c_void_p)]
+
+
+_u64, _u32, _vp, _sz = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_size_t
+_lib.wt_sizes.argtypes = [_u64, _u64, _u32, ctypes.POINTER(WtSizes)]
+_lib.wt_build_async.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(WtTree), _vp, _sz, _vp, _vp]
+_lib.wt_build.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(WtTree), _vp, _sz, _vp]
+_lib.wt_build_from_host.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(WtTree), _vp, _sz, _vp]
+_lib.wt_access.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _u64, _vp, _vp, _vp]
+_lib.wt_rank.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
+_lib.wt_select.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
+_lib.wt_launch_plan.argtypes = [_u64, _u64, _u32, _vp, _u32]
+_lib.wt_launch_plan.restype = _u32
+_lib.wt_set_profile_events.argtypes = [_vp, _u32]
+_lib.wt_set_profile_events.restype = None
+_lib.wt_status_string.argtypes = [ctypes.c_int]
+_lib.wt_status_string.restype = ctypes.c_char_p
+_lib.wt_last_error.argtypes = []
+_lib.wt_last_error.restype = ctypes.c_char_p
+for _f in (_lib.wt_sizes, _lib.wt_build_async, _lib.wt_build, _lib.wt_build_from_host, _lib.wt_access,
+           _lib.wt_rank, _lib.wt_select):
+    _f.restype = ctypes.c_int
+
+EXPORTS = ["wt_sizes", "wt_build_async", "wt_build", "wt_build_from_host", "wt_access", "wt_rank",
+           "wt_select", "wt_launch_plan", "wt_set_profile_events", "wt_status_string", "wt_last_error"]
+
+
+class WtError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        detail = _lib.wt_last_error().decode()
+        super().__init__(f"{what}: {_lib.wt_status_string(status).decode()} {detail}".strip())
+        self.status = status
+
+
+def _check(st: int, what: str):
+    if st != WT_OK:
+        raise WtError(st, what)
+
+
+_WIDTH = {torch.uint8: 1, torch.int8: 1, torch.uint16: 2, torch.int16: 2, torch.int32: 4, torch.uint32: 4}
+
+
+def width_of(t: torch.Tensor) -> int:
+    if t.dtype not in _WIDTH:
+        raise TypeError(f"sequence dtype must be 1/2/4-byte integer, got {t.dtype}")
+    return _WIDTH[t.dtype]
+
+
+def _stream_ptr(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def sizes(n: int, sigma: int, width: int) -> WtSizes:
+    out = WtSizes()
+    _check(_lib.wt_sizes(n, sigma, width, ctypes.byref(out)), "wt_sizes")
+    return out
+
+
+def launch_plan(n: int, sigma: int, width: int) -> list[str]:
+    cnt = _lib.wt_launch_plan(n, sigma, width, None, 0)
+    buf = (ctypes.c_uint32 * max(cnt, 1))()
+    _lib.wt_launch_plan(n, sigma, width, ctypes.cast(buf, _vp), cnt)
+    return [KIND_NAMES.get(buf[i], str(buf[i])) for i in range(cnt)]
+
+
+def set_profile_events(events: list | None):
+    """events: list of torch.cuda.Event (enable_timing=True) or None."""
+    global _prof_keep
+    if not events:
+        _lib.wt_set_profile_events(None, 0)
+        _prof_keep = None
+        return
+    arr = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
+    _prof_keep = arr
+    _lib.wt_set_profile_events(ctypes.cast(arr, _vp), len(events))
+
+
+_prof_keep = None
+
+
+@dataclass
+class WaveletTree:
+    """Device-resident tree (all torch tensors on the build's device)."""
+    n: int
+    sigma: int
+    levels: int
+    bitmaps: torch.Tensor       # (L, words_per_level) int32 storage of uint32 words
+    superblocks: torch.Tensor   # (L, sb_per_level) int64 storage of uint64 counts
+    node_offsets: torch.Tensor  # (2^L + 1,) int64 storage of uint64 offsets
+
+    def _ctree(self) -> WtTree:
+        return WtTree(self.bitmaps.data_ptr() if self.bitmaps.numel() else None,
+                      self.superblocks.data_ptr() if self.superblocks.numel() else None,
+                      self.node_offsets.data_ptr())
+
+    def access(self, pos: torch.Tensor, stream=None) -> torch.Tensor:
+        return access(self, pos, stream)
+
+    def rank(self, c: torch.Tensor, pos: torch.Tensor, stream=None) -> torch.Tensor:
+        return rank(self, c, pos, stream)
+
+    def select(self, c: torch.Tensor, j: torch.Tensor, stream=None) -> torch.Tensor:
+        return select(self, c, j, stream)
+
+
+def alloc_tree(n: int, sigma: int, width: int, device) -> WaveletTree:
+    sz = sizes(n, sigma, width)
+    L = sz.levels
+    return WaveletTree(
+        n=n, sigma=sigma, levels=L,
+        bitmaps=torch.empty((L, sz.words_per_level), dtype=torch.int32, device=device),
+        superblocks=torch.empty((L, sz.sb_per_level), dtype=torch.int64, device=device),
+        node_offsets=torch.empty((sz.c_len,), dtype=torch.int64, device=device))
+
+
+def alloc_workspace(n: int, sigma: int, width: int, device, host: bool = False) -> torch.Tensor:
+    sz = sizes(n, sigma, width)
+    nbytes = sz.host_workspace_bytes if host else sz.workspace_bytes
+    return torch.empty((max(nbytes, 256),), dtype=torch.uint8, device=device)
+
+
+def build_async(seq: torch.Tensor, sigma: int, tree: WaveletTree | None = None,
+                workspace: torch.Tensor | None = None, status: torch.Tensor | None = None,
+                stream=None) -> WaveletTree:
+    """Enqueue wt_build_async on `stream` (default: torch's current stream).
+    `status` (int32 device tensor, optional) receives WT_OK / WT_ERR_SYMBOL_RANGE."""
+    if not seq.is_cuda:
+        raise ValueError("seq must be a CUDA tensor (use build_from_host for host data)")
+    seq = seq.contiguous()
+    w = width_of(seq)
+    n = seq.numel()
+    if tree is None:
+        tree = alloc_tree(n, sigma, w, seq.device)
+    if workspace is None:
+        workspace = alloc_workspace(n, sigma, w, seq.device)
+    ct = tree._ctree()
+    st = _lib.wt_build_async(seq.data_ptr() if n else None, n, sigma, w, ctypes.byref(ct),
+                             workspace.data_ptr(), workspace.numel(),
+                             status.data_ptr() if status is not None else None, _stream_ptr(stream))
+    _check(st, "wt_build_async")
+    return tree
+
+
+def build(seq: torch.Tensor, sigma: int, tree: WaveletTree | None = None,
+          workspace: torch.Tensor | None = None, stream=None) -> WaveletTree:
+    """wt_build: enqueue the build and synchronise once to read the range flag."""
+    if not seq.is_cuda:
+        raise ValueError("seq must be a CUDA tensor (use build_from_host for host data)")
+    seq = seq.contiguous()
+    w = width_of(seq)
+    n = seq.numel()
+    if tree is None:
+        tree = alloc_tree(n, sigma, w, seq.device)
+    if workspace is None:
+        workspace = alloc_workspace(n, sigma, w, seq.device)
+    ct = tree._ctree()
+    st = _lib.wt_build(seq.data_ptr() if n else None, n, sigma, w, ctypes.byref(ct),
+                       workspace.data_ptr(), workspace.numel(), _stream_ptr(stream))
+    _check(st, "wt_build")
+    return tree
+
+
+@dataclass
+class HostTree:
+    n: int
+    sigma: int
+    levels: int
+    bitmaps: torch.Tensor       # host (pinned) tensors
+    superblocks: torch.Tensor
+    node_offsets: torch.Tensor
+
+
+def alloc_host_tree(n: int, sigma: int, width: int, pin: bool = True) -> HostTree:
+    sz = sizes(n, sigma, width)
+    L = sz.levels
+    return HostTree(n=n, sigma=sigma, levels=L,
+                    bitmaps=torch.empty((L, sz.words_per_level), dtype=torch.int32, pin_memory=pin),
+                    superblocks=torch.empty((L, sz.sb_per_level), dtype=torch.int64, pin_memory=pin),
+                    node_offsets=torch.empty((sz.c_len,), dtype=torch.int64, pin_memory=pin))
+
+
+def build_from_host(h_seq: torch.Tensor, sigma: int, h_tree: HostTree | None = None,
+                    workspace: torch.Tensor | None = None, device=None, stream=None) -> HostTree:
+    """wt_build_from_host: H2D of the sequence, build, D2H of the whole tree, one sync."""
+    if h_seq.is_cuda:
+        raise ValueError("h_seq must be a host tensor")
+    h_seq = h_seq.contiguous()
+    w = width_of(h_seq)
+    n = h_seq.numel()
+    device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if h_tree is None:
+        h_tree = alloc_host_tree(n, sigma, w)
+    if workspace is None:
+        workspace = alloc_workspace(n, sigma, w, device, host=True)
+    ct = WtTree(h_tree.bitmaps.data_ptr() if h_tree.bitmaps.numel() else None,
+                h_tree.superblocks.data_ptr() if h_tree.superblocks.numel() else None,
+                h_tree.node_offsets.data_ptr())
+    st = _lib.wt_build_from_host(h_seq.data_ptr() if n else None, n, sigma, w, ctypes.byref(ct),
+                                 workspace.data_ptr(), workspace.numel(), _stream_ptr(stream))
+    _check(st, "wt_build_from_host")
+    return h_tree
+
+
+def _status_tensor(device):
+    return torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def access(tree: WaveletTree, pos: torch.Tensor, stream=None, status: torch.Tensor | None = None) -> torch.Tensor:
+    """S[pos] for a batch of positions (int64 device tensor) -> int64 tensor (uint32 values)."""
+    pos = pos.to(torch.int64).contiguous()
+    m = pos.numel()
+    out = torch.empty(m, dtype=torch.int32, device=pos.device)
+    ct = tree._ctree()
+    st = _lib.wt_access(ctypes.byref(ct), tree.n, tree.sigma, pos.data_ptr() if m else None, m,
+                        out.data_ptr() if m else None, status.data_ptr() if status is not None else None,
+                        _stream_ptr(stream))
+    _check(st, "wt_access")
+    return out.to(torch.int64) & 0xFFFFFFFF
+
+
+def rank(tree: WaveletTree, c: torch.Tensor, pos: torch.Tensor, stream=None,
+         status: torch.Tensor | None = None) -> torch.Tensor:
+    """inclusive rank_c(S, pos) for paired batches (c: int32/uint32, pos: int64)."""
+    c = c.to(torch.int32).contiguous()
+    pos = pos.to(torch.int64).contiguous()
+    m = pos.numel()
+    out = torch.empty(m, dtype=torch.int64, device=pos.device)
+    ct = tree._ctree()
+    st = _lib.wt_rank(ctypes.byref(ct), tree.n, tree.sigma, c.data_ptr() if m else None,
+                      pos.data_ptr() if m else None, m, out.data_ptr() if m else None,
+                      status.data_ptr() if status is not None else None, _stream_ptr(stream))
+    _check(st, "wt_rank")
+    return out
+
+
+def select(tree: WaveletTree, c: torch.Tensor, j: torch.Tensor, stream=None,
+           status: torch.Tensor | None = None) -> torch.Tensor:
+    """position of the j-th (1-based) occurrence of c, for paired batches."""
+    c = c.to(torch.int32).contiguous()
+    j = j.to(torch.int64).contiguous()
+    m = j.numel()
+    out = torch.empty(m, dtype=torch.int64, device=j.device)
+    ct = tree._ctree()
+    st = _lib.wt_select(ctypes.byref(ct), tree.n, tree.sigma, c.data_ptr() if m else None,
+                        j.data_ptr() if m else None, m, out.data_ptr() if m else None,
+                        status.data_ptr() if status is not None else None, _stream_ptr(stream))
+    _check(st, "wt_select")
+    return out

@@ -1,0 +1,446 @@
+// wt_api.cu -- host side of libwt.so: argument checks, workspace carving and
+// the launch sequence of the levelwise build.  The C ABI is declared (and
+// documented, with the paper citations) in include/wt.h.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "wt.h"
+#include "wt_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local wt_event_t* g_events = nullptr;
+thread_local uint32_t g_event_count = 0;
+
+wt_status fail(wt_status st, const char* what) {
+  g_last_error = what;
+  return st;
+}
+wt_status fail_cuda(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return WT_ERR_CUDA;
+}
+
+constexpr size_t ALIGN = 256;
+size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
+
+uint32_t levels_of(uint64_t sigma) {
+  uint32_t L = 0;
+  while (L < 63 && (1ull << L) < sigma) ++L;
+  return L;
+}
+
+uint64_t level_tile(uint32_t width) {
+  switch (width) {
+    case 1: return wt::LevelCfg<uint8_t>::TILE;
+    case 2: return wt::LevelCfg<uint16_t>::TILE;
+    default: return wt::LevelCfg<uint32_t>::TILE;
+  }
+}
+
+constexpr uint32_t SMEM_HIST_MAX_L = 12;  // 4096 bins * 4 B fit several copies in 48 KiB
+constexpr int MAX_LOOKBACK_LAUNCHES = 64;
+
+// Workspace carve (all offsets 256-byte aligned).  The control block
+// [0, ctrl_bytes) is zeroed once per build: range flag, tile counters (one per
+// look-back launch), level bases, look-back status words (shared by every
+// look-back launch of the build, told apart by epoch).
+struct Carve {
+  uint32_t L = 0;
+  uint64_t words = 0, nsb = 0, c_len = 0;
+  uint64_t status_entries = 0, tab_entries = 0;
+  size_t off_flag = 0, off_counters = 0, off_lvlbase = 0, off_status = 0, ctrl_bytes = 0;
+  size_t off_tab = 0, off_bufA = 0, off_bufB = 0, total = 0;
+  // host-API extras (after total)
+  size_t off_seq = 0, off_bits = 0, off_sb = 0, off_c = 0, host_total = 0;
+};
+
+Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
+  Carve c;
+  c.L = levels_of(sigma);
+  c.words = 16 * ((n + 511) / 512);
+  c.nsb = (n + 511) / 512 + 1;
+  c.c_len = (1ull << c.L) + 1;
+  const uint64_t tiles = (n + level_tile(width) - 1) / level_tile(width);
+  const uint64_t scan_tiles = ((1ull << c.L) + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
+  c.tab_entries = c.L >= 2 ? (1ull << (c.L - 1)) - 1 : 0;
+  const uint64_t tab_tiles = (c.tab_entries + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
+  c.status_entries = std::max<uint64_t>(1, std::max(tiles, std::max(scan_tiles, tab_tiles)));
+  size_t o = 0;
+  c.off_flag = o;
+  o += ALIGN;
+  c.off_counters = o;
+  o += align_up(MAX_LOOKBACK_LAUNCHES * sizeof(uint32_t));
+  c.off_lvlbase = o;
+  o += align_up(64 * sizeof(uint64_t));
+  c.off_status = o;
+  o += align_up(c.status_entries * sizeof(uint64_t));
+  c.ctrl_bytes = o;
+  c.off_tab = o;
+  o += align_up(c.tab_entries * sizeof(ulonglong2));
+  const size_t seq_bytes = align_up(n * width);
+  c.off_bufA = o;
+  if (c.L >= 2) o += seq_bytes;  // T_1, T_3, ...
+  c.off_bufB = o;
+  if (c.L >= 3) o += seq_bytes;  // T_2, T_4, ...
+  c.total = o;
+  c.off_seq = o;
+  o += seq_bytes;
+  c.off_bits = o;
+  o += align_up((size_t)c.L * c.words * 4);
+  c.off_sb = o;
+  o += align_up((size_t)c.L * c.nsb * 8);
+  c.off_c = o;
+  o += align_up(c.c_len * 8);
+  c.host_total = o;
+  return c;
+}
+
+wt_status check_args(uint64_t n, uint64_t sigma, uint32_t width) {
+  (void)n;
+  if (width != 1 && width != 2 && width != 4) return fail(WT_ERR_ARG, "width must be 1, 2 or 4");
+  if (sigma == 0) return fail(WT_ERR_ARG, "sigma must be >= 1");
+  if (sigma > (1ull << (8 * width))) return fail(WT_ERR_ARG, "sigma exceeds the symbol width");
+  if (levels_of(sigma) > 30) return fail(WT_ERR_ARG, "more than 30 levels");
+  if (n > (1ull << 50)) return fail(WT_ERR_ARG, "n too large");
+  return WT_OK;
+}
+
+struct Launcher {
+  cudaStream_t s;
+  uint32_t k = 0;
+  void pre() {
+    if (g_events && 2 * k + 1 < g_event_count) cudaEventRecord((cudaEvent_t)g_events[2 * k], s);
+  }
+  void post() {
+    if (g_events && 2 * k + 1 < g_event_count) cudaEventRecord((cudaEvent_t)g_events[2 * k + 1], s);
+    ++k;
+  }
+};
+
+enum Kind : uint32_t { K_HIST = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5 };
+
+// The launch sequence, shared by wt_build_async and wt_launch_plan.
+template <typename T>
+wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out, char* ws, const Carve& c,
+                  cudaStream_t stream, uint32_t* kinds, uint32_t cap, uint32_t* count) {
+  const bool dry = (seq == nullptr && out == nullptr);
+  uint32_t nk = 0;
+  auto note = [&](uint32_t kind) {
+    if (kinds && nk < cap) kinds[nk] = kind;
+    ++nk;
+  };
+  int32_t* flag = reinterpret_cast<int32_t*>(ws + c.off_flag);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(ws + c.off_counters);
+  unsigned long long* lvlbase = reinterpret_cast<unsigned long long*>(ws + c.off_lvlbase);
+  uint64_t* status = reinterpret_cast<uint64_t*>(ws + c.off_status);
+  ulonglong2* tab = reinterpret_cast<ulonglong2*>(ws + c.off_tab);
+  T* buf[2] = {reinterpret_cast<T*>(ws + c.off_bufA), reinterpret_cast<T*>(ws + c.off_bufB)};
+  unsigned long long* C = dry ? nullptr : reinterpret_cast<unsigned long long*>(out->node_offsets);
+  const uint32_t L = c.L;
+  Launcher lk{stream};
+  cudaError_t e;
+
+  if (!dry) {
+    if ((e = cudaMemsetAsync(ws, 0, c.ctrl_bytes, stream)) != cudaSuccess) return fail_cuda(e, "memset ctrl");
+    if ((e = cudaMemsetAsync(C, 0, c.c_len * 8, stream)) != cudaSuccess) return fail_cuda(e, "memset C");
+    if (n == 0) {
+      if (L && (e = cudaMemsetAsync(out->superblocks, 0, (size_t)L * c.nsb * 8, stream)) != cudaSuccess)
+        return fail_cuda(e, "memset sb");
+      if (count) *count = 0;
+      return WT_OK;
+    }
+  } else if (n == 0) {
+    if (count) *count = 0;
+    return WT_OK;
+  }
+
+  // a1: histogram + range check
+  note(K_HIST);
+  if (!dry) {
+    lk.pre();
+    if (L <= SMEM_HIST_MAX_L) {
+      const uint32_t nbins = 1u << L;
+      uint32_t copies = (48u * 1024u) / (nbins * 4u);
+      copies = std::max(1u, std::min(copies, 16u));
+      const uint64_t nvec = n / (16 / sizeof(T));
+      const uint64_t want = (nvec + 511) / 512;
+      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 148 * 4));
+      wt::k_hist_smem<T><<<grid, 512, copies * nbins * 4, stream>>>(seq, n, sigma, nbins, copies, C, flag);
+    } else {
+      const uint64_t nvec = n / (16 / sizeof(T));
+      const uint64_t want = (nvec + 255) / 256;
+      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 148 * 8));
+      wt::k_hist_global<T><<<grid, 256, 0, stream>>>(seq, n, sigma, C, flag);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_hist");
+    lk.post();
+  }
+
+  // a2: C = exclusive_scan(H) in place
+  uint32_t epoch = 1, counter = 0;
+  note(K_SCAN);
+  if (!dry) {
+    lk.pre();
+    const uint64_t cnt = 1ull << L;
+    wt::OpNodeOffsets op{C, cnt};
+    const uint32_t grid = (uint32_t)((cnt + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+    wt::k_scan<wt::OpNodeOffsets><<<grid, wt::SCAN_THREADS, 0, stream>>>(op, cnt, status, counters + counter,
+                                                                         epoch, flag);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(C)");
+    lk.post();
+  }
+  ++epoch;
+  ++counter;
+
+  // a2': node tables {ob, Zn} for levels 0..L-2
+  if (L >= 2) {
+    note(K_TABLES);
+    note(K_TABLES);
+    if (!dry) {
+      lk.pre();
+      wt::OpTables op{C, tab, lvlbase, L};
+      const uint32_t grid = (uint32_t)((c.tab_entries + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+      wt::k_scan<wt::OpTables><<<grid, wt::SCAN_THREADS, 0, stream>>>(op, c.tab_entries, status,
+                                                                      counters + counter, epoch, flag);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(tables)");
+      lk.post();
+      lk.pre();
+      const uint32_t g2 = (uint32_t)std::min<uint64_t>((c.tab_entries + 255) / 256, 148 * 16);
+      wt::k_tables_fix<<<g2, 256, 0, stream>>>(C, tab, lvlbase, L, c.tab_entries, flag);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_tables_fix");
+      lk.post();
+    }
+    ++epoch;
+    ++counter;
+  }
+
+  // a3 / a4: one pass per level
+  constexpr uint64_t TILE = wt::LevelCfg<T>::TILE;
+  const uint32_t grid = (uint32_t)((n + TILE - 1) / TILE);
+  for (uint32_t l = 0; l < L; ++l) {
+    const bool last = (l + 1 == L);
+    note(last ? K_LAST : K_LEVEL);
+    if (!dry) {
+      const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
+      T* o = last ? nullptr : buf[l & 1];
+      const uint32_t sh = L - 1 - l;
+      const ulonglong2* t = last ? nullptr : tab + ((1ull << l) - 1);
+      uint32_t* bits = out->bitmaps + (uint64_t)l * c.words;
+      unsigned long long* sb = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
+      lk.pre();
+      if (last)
+        wt::k_level<T, false><<<grid, wt::LevelCfg<T>::THREADS, 0, stream>>>(
+            in, o, n, sh, t, bits, c.words, sb, c.nsb, status, counters + counter, epoch, flag);
+      else
+        wt::k_level<T, true><<<grid, wt::LevelCfg<T>::THREADS, 0, stream>>>(
+            in, o, n, sh, t, bits, c.words, sb, c.nsb, status, counters + counter, epoch, flag);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_level");
+      lk.post();
+    }
+    ++epoch;
+    ++counter;
+  }
+  if (count) *count = nk;
+  return WT_OK;
+}
+
+wt_status dispatch(const void* seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* out, char* ws,
+                   const Carve& c, cudaStream_t stream, uint32_t* kinds, uint32_t cap, uint32_t* count) {
+  switch (width) {
+    case 1: return enqueue<uint8_t>((const uint8_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count);
+    case 2: return enqueue<uint16_t>((const uint16_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count);
+    default: return enqueue<uint32_t>((const uint32_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count);
+  }
+}
+
+wt::TreeView view_of(const wt_tree_t* t, uint64_t n, uint64_t sigma) {
+  wt::TreeView v;
+  v.bitmaps = t->bitmaps;
+  v.sb = reinterpret_cast<const unsigned long long*>(t->superblocks);
+  v.C = reinterpret_cast<const unsigned long long*>(t->node_offsets);
+  v.n = n;
+  v.W = 16 * ((n + 511) / 512);
+  v.NSB = (n + 511) / 512 + 1;
+  v.L = levels_of(sigma);
+  return v;
+}
+
+}  // namespace
+
+extern "C" {
+
+wt_status wt_sizes(uint64_t n, uint64_t sigma, uint32_t width, wt_sizes_t* out) {
+  if (!out) return fail(WT_ERR_ARG, "out is NULL");
+  wt_status st = check_args(n, sigma, width);
+  if (st != WT_OK) return st;
+  const Carve c = carve(n, sigma, width);
+  out->levels = c.L;
+  out->width = width;
+  out->words_per_level = c.words;
+  out->sb_per_level = c.nsb;
+  out->c_len = c.c_len;
+  out->bitmap_bytes = (uint64_t)c.L * c.words * 4;
+  out->superblock_bytes = (uint64_t)c.L * c.nsb * 8;
+  out->node_offset_bytes = c.c_len * 8;
+  out->workspace_bytes = c.total;
+  out->host_workspace_bytes = c.host_total;
+  return WT_OK;
+}
+
+wt_status wt_build_async(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* out,
+                         void* d_workspace, size_t workspace_bytes, int32_t* d_status, wt_stream_t stream) {
+  g_last_error.clear();
+  wt_status st = check_args(n, sigma, width);
+  if (st != WT_OK) return st;
+  if (!out || !out->node_offsets || (levels_of(sigma) > 0 && (!out->superblocks || (n > 0 && !out->bitmaps))))
+    return fail(WT_ERR_ARG, "output pointers are NULL");
+  if (n > 0 && !d_seq) return fail(WT_ERR_ARG, "d_seq is NULL");
+  if (n > 0 && (reinterpret_cast<uintptr_t>(d_seq) & 15)) return fail(WT_ERR_ARG, "d_seq must be 16-byte aligned");
+  const Carve c = carve(n, sigma, width);
+  if (!d_workspace || workspace_bytes < c.total) return fail(WT_ERR_WORKSPACE, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(d_workspace) & (ALIGN - 1))
+    return fail(WT_ERR_ARG, "workspace must be 256-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(d_workspace);
+  st = dispatch(d_seq, n, sigma, width, out, ws, c, s, nullptr, 0, nullptr);
+  if (st != WT_OK) return st;
+  if (d_status) {
+    cudaError_t e = cudaMemcpyAsync(d_status, ws + c.off_flag, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return fail_cuda(e, "status copy");
+  }
+  return WT_OK;
+}
+
+wt_status wt_build(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* out,
+                   void* d_workspace, size_t workspace_bytes, wt_stream_t stream) {
+  wt_status st = wt_build_async(d_seq, n, sigma, width, out, d_workspace, workspace_bytes, nullptr, stream);
+  if (st != WT_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const Carve c = carve(n, sigma, width);
+  int32_t h_flag = 0;
+  cudaError_t e = cudaMemcpyAsync(&h_flag, static_cast<char*>(d_workspace) + c.off_flag, sizeof(int32_t),
+                                  cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return fail_cuda(e, "flag readback");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail_cuda(e, "stream sync");
+  if (h_flag) return fail(WT_ERR_SYMBOL_RANGE, "a symbol is >= sigma");
+  return WT_OK;
+}
+
+wt_status wt_build_from_host(const void* h_seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* h_out,
+                             void* d_workspace, size_t workspace_bytes, wt_stream_t stream) {
+  g_last_error.clear();
+  wt_status st = check_args(n, sigma, width);
+  if (st != WT_OK) return st;
+  if (!h_out || !h_out->node_offsets || (n > 0 && !h_seq)) return fail(WT_ERR_ARG, "NULL host pointer");
+  const Carve c = carve(n, sigma, width);
+  if (!d_workspace || workspace_bytes < c.host_total) return fail(WT_ERR_WORKSPACE, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(d_workspace) & (ALIGN - 1))
+    return fail(WT_ERR_ARG, "workspace must be 256-byte aligned");
+  char* ws = static_cast<char*>(d_workspace);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  wt_tree_t dtree;
+  dtree.bitmaps = reinterpret_cast<uint32_t*>(ws + c.off_bits);
+  dtree.superblocks = reinterpret_cast<uint64_t*>(ws + c.off_sb);
+  dtree.node_offsets = reinterpret_cast<uint64_t*>(ws + c.off_c);
+  cudaError_t e;
+  if (n && (e = cudaMemcpyAsync(ws + c.off_seq, h_seq, n * width, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return fail_cuda(e, "H2D sequence");
+  st = dispatch(ws + c.off_seq, n, sigma, width, &dtree, ws, c, s, nullptr, 0, nullptr);
+  if (st != WT_OK) return st;
+  const size_t bb = (size_t)c.L * c.words * 4, sbb = (size_t)c.L * c.nsb * 8, cb = c.c_len * 8;
+  if (bb && (e = cudaMemcpyAsync(h_out->bitmaps, dtree.bitmaps, bb, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return fail_cuda(e, "D2H bitmaps");
+  if (sbb && (e = cudaMemcpyAsync(h_out->superblocks, dtree.superblocks, sbb, cudaMemcpyDeviceToHost, s)) !=
+                 cudaSuccess)
+    return fail_cuda(e, "D2H superblocks");
+  if ((e = cudaMemcpyAsync(h_out->node_offsets, dtree.node_offsets, cb, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return fail_cuda(e, "D2H node offsets");
+  int32_t h_flag = 0;
+  if ((e = cudaMemcpyAsync(&h_flag, ws + c.off_flag, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return fail_cuda(e, "flag readback");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail_cuda(e, "stream sync");
+  if (h_flag) return fail(WT_ERR_SYMBOL_RANGE, "a symbol is >= sigma");
+  return WT_OK;
+}
+
+static wt_status query_args(const wt_tree_t* tree, uint64_t n, uint64_t sigma) {
+  if (!tree || !tree->node_offsets) return fail(WT_ERR_ARG, "tree is NULL");
+  if (sigma == 0 || levels_of(sigma) > 30) return fail(WT_ERR_ARG, "bad sigma");
+  if (levels_of(sigma) > 0 && n > 0 && (!tree->bitmaps || !tree->superblocks))
+    return fail(WT_ERR_ARG, "tree pointers are NULL");
+  return WT_OK;
+}
+
+wt_status wt_access(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint64_t* d_pos, uint64_t m,
+                    uint32_t* d_sym, int32_t* d_status, wt_stream_t stream) {
+  g_last_error.clear();
+  wt_status st = query_args(tree, n, sigma);
+  if (st != WT_OK) return st;
+  if (m == 0) return WT_OK;
+  if (!d_pos || !d_sym) return fail(WT_ERR_ARG, "NULL query pointer");
+  const uint32_t grid = (uint32_t)((m + 255) / 256);
+  wt::k_access<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(view_of(tree, n, sigma), d_pos, m, d_sym,
+                                                                         d_status);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_access");
+}
+
+wt_status wt_rank(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint32_t* d_c, const uint64_t* d_pos,
+                  uint64_t m, uint64_t* d_cnt, int32_t* d_status, wt_stream_t stream) {
+  g_last_error.clear();
+  wt_status st = query_args(tree, n, sigma);
+  if (st != WT_OK) return st;
+  if (m == 0) return WT_OK;
+  if (!d_c || !d_pos || !d_cnt) return fail(WT_ERR_ARG, "NULL query pointer");
+  const uint32_t grid = (uint32_t)((m + 255) / 256);
+  wt::k_rank<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      view_of(tree, n, sigma), sigma, d_c, d_pos, m, reinterpret_cast<unsigned long long*>(d_cnt), d_status);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_rank");
+}
+
+wt_status wt_select(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint32_t* d_c, const uint64_t* d_j,
+                    uint64_t m, uint64_t* d_out, int32_t* d_status, wt_stream_t stream) {
+  g_last_error.clear();
+  wt_status st = query_args(tree, n, sigma);
+  if (st != WT_OK) return st;
+  if (m == 0) return WT_OK;
+  if (!d_c || !d_j || !d_out) return fail(WT_ERR_ARG, "NULL query pointer");
+  const uint32_t grid = (uint32_t)((m + 255) / 256);
+  wt::k_select<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      view_of(tree, n, sigma), sigma, d_c, d_j, m, reinterpret_cast<unsigned long long*>(d_out), d_status);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_select");
+}
+
+uint32_t wt_launch_plan(uint64_t n, uint64_t sigma, uint32_t width, uint32_t* kinds, uint32_t cap) {
+  if (check_args(n, sigma, width) != WT_OK) return 0;
+  const Carve c = carve(n, sigma, width);
+  uint32_t count = 0;
+  dispatch(nullptr, n, sigma, width, nullptr, nullptr, c, nullptr, kinds, cap, &count);
+  return count;
+}
+
+void wt_set_profile_events(wt_event_t* events, uint32_t count) {
+  g_events = events;
+  g_event_count = events ? count : 0;
+}
+
+const char* wt_status_string(wt_status status) {
+  switch (status) {
+    case WT_OK: return "WT_OK";
+    case WT_ERR_ARG: return "WT_ERR_ARG";
+    case WT_ERR_SYMBOL_RANGE: return "WT_ERR_SYMBOL_RANGE";
+    case WT_ERR_INDEX: return "WT_ERR_INDEX";
+    case WT_ERR_CUDA: return "WT_ERR_CUDA";
+    case WT_ERR_WORKSPACE: return "WT_ERR_WORKSPACE";
+  }
+  return "WT_ERR_UNKNOWN";
+}
+
+const char* wt_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

@@ -18,3 +18,13 @@ def oracle_lib():
     import oracle
     oracle.build_lib()
     return oracle
+
+
+def build_native():
+    """Compile libwt.so (nvcc, sm_100a) without importing the package first."""
+    import importlib.util
+    path = os.path.join(ROOT, "paper_1610_05994_b200", "buildlib.py")
+    spec = importlib.util.spec_from_file_location("wt_buildlib", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.build()

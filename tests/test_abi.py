@@ -1,0 +1,88 @@
+"""Host-side checks of the C ABI (no GPU): the library loads, exports every
+symbol include/wt.h declares, and its pure-host entry points (sizes, launch
+plan, argument validation) behave as documented."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def wt():
+    from conftest import build_native
+    build_native()
+    import paper_1610_05994_b200 as wt
+    return wt
+
+
+def declared_symbols():
+    with open(os.path.join(ROOT, "include", "wt.h")) as f:
+        src = f.read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\**(wt_\w+)\s*\(", src, re.M)))
+
+
+def test_exports_every_declared_symbol(wt):
+    syms = declared_symbols()
+    assert len(syms) >= 10
+    lib = ctypes.CDLL(wt.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(wt.EXPORTS)
+
+
+def test_library_is_sm100a_only(wt):
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", wt.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert all("sm_100a" in line for line in out.splitlines() if ".cubin" in line)
+
+
+def test_sizes(wt):
+    s = wt.sizes(30, 16, 1)
+    assert (s.levels, s.words_per_level, s.sb_per_level, s.c_len) == (4, 16, 2, 17)
+    s = wt.sizes(0, 16, 1)
+    assert (s.levels, s.words_per_level, s.sb_per_level, s.c_len) == (4, 0, 1, 17)
+    s = wt.sizes(1 << 28, 1 << 24, 4)
+    assert s.levels == 24 and s.words_per_level == (1 << 28) // 32 and s.sb_per_level == (1 << 19) + 1
+    assert s.bitmap_bytes == 24 * (1 << 23) * 4 and s.superblock_bytes == 24 * ((1 << 19) + 1) * 8
+    # two ping-pong permuted copies of the sequence at most
+    assert 2 * (1 << 30) <= s.workspace_bytes < 2 * (1 << 30) + 300 * (1 << 20)
+    assert s.host_workspace_bytes > s.workspace_bytes + (1 << 30)
+    assert wt.sizes(5, 1, 1).levels == 0
+    assert wt.sizes(5, 2, 1).workspace_bytes < 1 << 20   # L=1: no permuted copy
+    for n, sigma, w, L in [(10, 3, 1, 2), (10, 256, 1, 8), (10, 257, 2, 9), (10, 1 << 16, 2, 16)]:
+        assert wt.sizes(n, sigma, w).levels == L
+
+
+@pytest.mark.parametrize("n,sigma,width", [(10, 4, 3), (10, 0, 1), (10, 257, 1), (10, 1 << 17, 2),
+                                           (10, (1 << 31), 4)])
+def test_sizes_rejects_bad_args(wt, n, sigma, width):
+    with pytest.raises(wt.WtError) as e:
+        wt.sizes(n, sigma, width)
+    assert e.value.status == wt.WT_ERR_ARG
+
+
+def test_build_validates_before_touching_the_device(wt):
+    lib = wt._lib
+    tree = wt.WtTree(None, None, None)
+    assert lib.wt_build_async(None, 10, 4, 1, ctypes.byref(tree), None, 0, None, None) == wt.WT_ERR_ARG
+    tree = wt.WtTree(16, 16, 16)
+    assert lib.wt_build_async(None, 10, 4, 1, ctypes.byref(tree), None, 0, None, None) == wt.WT_ERR_ARG
+    assert lib.wt_build_async(32, 10, 4, 1, ctypes.byref(tree), None, 0, None, None) == wt.WT_ERR_WORKSPACE
+    assert lib.wt_build_async(33, 10, 4, 1, ctypes.byref(tree), 256, 1 << 20, None, None) == wt.WT_ERR_ARG
+    assert lib.wt_build_async(32, 10, 4, 1, ctypes.byref(tree), 257, 1 << 20, None, None) == wt.WT_ERR_ARG
+    assert lib.wt_build_async(32, 10, 4, 3, ctypes.byref(tree), 256, 1 << 20, None, None) == wt.WT_ERR_ARG
+    assert lib.wt_access(None, 10, 4, None, 1, None, None, None) == wt.WT_ERR_ARG
+    assert b"workspace" in lib.wt_last_error() or lib.wt_last_error() == b"tree is NULL"
+    assert lib.wt_status_string(2) == b"WT_ERR_SYMBOL_RANGE"
+
+
+def test_launch_plan(wt):
+    assert wt.launch_plan(1 << 20, 256, 1) == ["hist", "scan", "tables", "tables"] + ["level"] * 7 + ["last_level"]
+    assert wt.launch_plan(1 << 20, 4, 1) == ["hist", "scan", "tables", "tables", "level", "last_level"]
+    assert wt.launch_plan(100, 2, 1) == ["hist", "scan", "last_level"]
+    assert wt.launch_plan(100, 1, 1) == ["hist", "scan"]
+    assert wt.launch_plan(0, 16, 1) == []

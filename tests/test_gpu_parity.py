@@ -1,0 +1,237 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
+by element, on seeded inputs.  All wavelet-tree outputs are integers, so the
+bar is bit-exact equality of every bitmap word, superblock and node offset."""
+import numpy as np
+import pytest
+import torch
+
+import brute
+import oracle
+import wt_inputs
+
+pytestmark = pytest.mark.gpu
+
+TILE = {1: 16384, 2: 8192, 4: 4096}   # level-pass tile (positions) per symbol width
+
+
+@pytest.fixture(scope="module")
+def wt():
+    from conftest import build_native
+    build_native()
+    import paper_1610_05994_b200 as wt
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return wt
+
+
+def to_dev(S: np.ndarray) -> torch.Tensor:
+    t = torch.from_numpy(S.view(np.int32) if S.dtype == np.uint32 else S)
+    return t.cuda()
+
+
+def np_tree(tree):
+    return (tree.bitmaps.cpu().numpy().view(np.uint32), tree.superblocks.cpu().numpy().view(np.uint64),
+            tree.node_offsets.cpu().numpy().view(np.uint64))
+
+
+def assert_same(tree, ot, ctx=""):
+    B, SB, C = np_tree(tree)
+    assert tree.levels == ot.L, ctx
+    assert np.array_equal(C, ot.node_offsets), f"node offsets {ctx}"
+    for l in range(ot.L):
+        if not np.array_equal(B[l], ot.bitmaps[l]):
+            bad = np.nonzero(B[l] != ot.bitmaps[l])[0]
+            raise AssertionError(f"level {l} bitmap differs at {bad.size} words, first {bad[:5]} {ctx}")
+        assert np.array_equal(SB[l], ot.superblocks[l]), f"level {l} superblocks {ctx}"
+
+
+def check_case(wt, S, sigma, ctx=""):
+    tree = wt.build(to_dev(S), sigma)
+    assert_same(tree, oracle.build(S, sigma), ctx)
+    return tree
+
+
+# ---------------------------------------------------------------- small cases
+
+
+@pytest.mark.parametrize("sigma", [1, 2, 3, 4, 5, 16, 27, 230, 256, 1000, 1 << 12, 1 << 16, 70000, 1 << 24])
+def test_random_small(wt, sigma):
+    rng = np.random.default_rng(sigma)
+    for k, kind in enumerate(["uniform", "zipf", "runs", "sorted", "reverse", "constant"]):
+        n = int(rng.integers(1, 70000))
+        S = wt_inputs.random_case(100 * sigma + k, n, sigma, kind)
+        check_case(wt, S, sigma, f"sigma={sigma} n={n} kind={kind}")
+
+
+@pytest.mark.parametrize("width", [1, 2, 4])
+def test_edge_sizes(wt, width):
+    t = TILE[width]
+    sigma = {1: 256, 2: 1 << 16, 4: 1 << 20}[width]
+    dtype = {1: np.uint8, 2: np.uint16, 4: np.uint32}[width]
+    for n in [0, 1, 2, 31, 32, 33, 511, 512, 513, 1023, t - 1, t, t + 1, 2 * t - 1, 2 * t, 2 * t + 1,
+              3 * t + 512, 7 * t + 33]:
+        for sg in (sigma, 3):
+            S = wt_inputs.random_case(n, n, sg, "uniform", dtype=dtype)
+            check_case(wt, S, sg, f"n={n} sigma={sg} w={width}")
+
+
+def test_two_hundred_random_cases(wt):
+    rng = np.random.default_rng(99)
+    for k in range(200):
+        sigma = int(rng.choice([1, 2, 3, 4, 16, 27, 230, 1 << 10, 1 << 14, 1 << 18]))
+        n = int(rng.integers(0, 40000))
+        kind = ["uniform", "zipf", "runs", "sorted"][k % 4]
+        dtype = [None, np.uint16, np.uint32][k % 3] if sigma <= 65536 else np.uint32
+        S = wt_inputs.random_case(k, n, sigma, kind, dtype=dtype)
+        check_case(wt, S, sigma, f"k={k}")
+
+
+def test_many_tiles_lookback(wt):
+    # thousands of tiles per level: exercises look-back windows beyond 32 tiles
+    for sigma, dtype in [(4, np.uint8), (256, np.uint8), (1 << 16, np.uint16), (1 << 20, np.uint32)]:
+        S = wt_inputs.random_case(7, 3_000_017, sigma, "zipf", dtype=dtype)
+        check_case(wt, S, sigma, f"sigma={sigma}")
+
+
+def test_symbol_range_error(wt):
+    for S, sigma in [(np.array([0, 1, 4, 2], np.uint8), 4), (np.array([0, 2, 1], np.uint8), 2),
+                     (np.full(100000, 300, np.uint16), 256), (np.array([5], np.uint32), 3)]:
+        with pytest.raises(wt.WtError) as e:
+            wt.build(to_dev(S), sigma)
+        assert e.value.status == wt.WT_ERR_SYMBOL_RANGE
+    # a valid build afterwards on the same device still works
+    check_case(wt, np.array([0, 1, 2, 3], np.uint8), 4)
+
+
+def test_async_status_and_determinism(wt):
+    S = wt_inputs.random_case(5, 500_000, 1 << 14, "zipf", dtype=np.uint16)
+    d = to_dev(S)
+    status = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    t1 = wt.build_async(d, 1 << 14, status=status)
+    t2 = wt.build_async(d, 1 << 14)
+    torch.cuda.synchronize()
+    assert int(status.item()) == wt.WT_OK
+    for a, b in zip(np_tree(t1), np_tree(t2)):
+        assert np.array_equal(a, b)
+    bad = d.clone()
+    bad[1234] = 20000
+    wt.build_async(bad, 1 << 14, status=status)
+    torch.cuda.synchronize()
+    assert int(status.item()) == wt.WT_ERR_SYMBOL_RANGE
+
+
+def test_build_from_host_matches(wt):
+    S = wt_inputs.random_case(11, 1_000_003, 230, "zipf")
+    h = wt.build_from_host(torch.from_numpy(S), 230)
+    ot = oracle.build(S, 230)
+    assert np.array_equal(h.bitmaps.numpy().view(np.uint32), ot.bitmaps)
+    assert np.array_equal(h.superblocks.numpy().view(np.uint64), ot.superblocks)
+    assert np.array_equal(h.node_offsets.numpy().view(np.uint64), ot.node_offsets)
+
+
+# ------------------------------------------------------------------- queries
+
+
+@pytest.mark.parametrize("sigma,n", [(1, 1000), (2, 5000), (16, 70001), (230, 100000), (1 << 16, 200000),
+                                     (1 << 20, 100000)])
+def test_queries(wt, sigma, n):
+    S = wt_inputs.random_case(sigma, n, sigma, "zipf" if sigma > 2 else "uniform",
+                              dtype=np.uint32 if sigma > 65536 else None)
+    tree = check_case(wt, S, sigma)
+    pos = torch.arange(n, device="cuda")
+    got = tree.access(pos).cpu().numpy()
+    assert np.array_equal(got, S.astype(np.int64))
+    rng = np.random.default_rng(3)
+    m = 5000
+    c = rng.integers(0, sigma, m)
+    c[: m // 2] = S[rng.integers(0, n, m // 2)]          # half the queries on present symbols
+    i = rng.integers(0, n, m)
+    cnt = tree.rank(torch.from_numpy(c.astype(np.int32)).cuda(), torch.from_numpy(i).cuda()).cpu().numpy()
+    order = np.argsort(S, kind="stable")
+    ot = oracle.build(S, sigma)
+    for k in range(0, m, 50):
+        assert cnt[k] == ot.rank(int(c[k]), int(i[k]))
+    # brute-force count for all m via sorted occurrence lists
+    Ssorted = S[order]
+    for k in range(m):
+        lo = np.searchsorted(Ssorted, c[k], "left")
+        hi = np.searchsorted(Ssorted, c[k], "right")
+        assert cnt[k] == np.searchsorted(order[lo:hi], i[k], "right")
+    # select: j-th occurrence
+    cs, js, want = [], [], []
+    for sym in np.unique(S)[:200]:
+        occ = np.nonzero(S == sym)[0]
+        for j in (1, occ.size, (occ.size + 1) // 2):
+            cs.append(sym)
+            js.append(j)
+            want.append(occ[j - 1])
+    got = tree.select(torch.tensor(np.array(cs, np.int32)).cuda(), torch.tensor(js).cuda()).cpu().numpy()
+    assert np.array_equal(got, np.array(want))
+
+
+def test_query_index_errors(wt):
+    S = np.array([0, 1, 2, 3, 2, 1], np.uint8)
+    tree = wt.build(to_dev(S), 4)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = wt.access(tree, torch.tensor([0, 6, 5], device="cuda"), status=st)
+    assert out.tolist() == [0, 0xFFFFFFFF, 1] and st.item() == wt.WT_ERR_INDEX
+    st.zero_()
+    out = wt.rank(tree, torch.tensor([1, 4], device="cuda"), torch.tensor([5, 0], device="cuda"), status=st)
+    assert out.tolist()[0] == 2 and out.tolist()[1] == -1 and st.item() == wt.WT_ERR_INDEX
+    st.zero_()
+    out = wt.select(tree, torch.tensor([2, 2, 0], device="cuda"), torch.tensor([2, 3, 0], device="cuda"), status=st)
+    assert out.tolist() == [4, -1, -1] and st.item() == wt.WT_ERR_INDEX
+
+
+def test_fig2_worked_example_on_gpu(wt):
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "fig2_once_upon.json")) as f:
+        g = json.load(f)
+    alpha = g["alphabet_first_appearance"]
+    S = np.array([alpha.index(ch) for ch in g["text"]], np.uint8)
+    tree = check_case(wt, S, 16)
+    assert tree.access(torch.tensor([24], device="cuda")).item() == g["printed"]["access_24_code"]
+    assert tree.rank(torch.tensor([8], device="cuda"), torch.tensor([29], device="cuda")).item() == 3
+
+
+# ------------------------------------------------------- full-size configs
+
+
+def gpu_invariants(tree, S, sigma):
+    """Order-independent properties that hold at any size (checked on the GPU)."""
+    L = tree.levels
+    d = to_dev(S).to(torch.int64) & 0xFFFFFFFF
+    C = tree.node_offsets
+    H = torch.bincount(d, minlength=1 << L)
+    assert torch.equal(C[1:], torch.cumsum(H, 0)) and C[0].item() == 0
+    for l in range(L):
+        ones = int(((d >> (L - 1 - l)) & 1).sum().item())
+        assert int(tree.superblocks[l, -1].item()) == ones, f"level {l} total ones"
+        lut = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.int32, device="cuda")
+        pc = int(lut[tree.bitmaps[l].view(torch.uint8).to(torch.int64)].sum().item())
+        assert pc == ones, f"level {l} bitmap popcount"
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_config_parity(wt, cfg):
+    S, sigma = wt_inputs.generate(cfg)
+    tree = wt.build(to_dev(S), sigma)
+    torch.cuda.synchronize()
+    L = tree.levels
+    B, SB, C = np_tree(tree)
+    assert np.array_equal(C, oracle.node_offsets(S, sigma))
+    if cfg in (1, 2, 3):
+        levels = range(L)                                  # every level, element by element
+    else:
+        levels = sorted({0, 1, L // 2, L - 2, L - 1})      # sampled levels, each one complete
+    for l in levels:
+        ob, osb, onl = oracle.build_level(S, sigma, l)
+        assert np.array_equal(B[l], ob), f"cfg{cfg} level {l} bitmap"
+        assert np.array_equal(SB[l], osb), f"cfg{cfg} level {l} superblocks"
+        assert np.array_equal(C[:: 1 << (L - l)], onl)
+    gpu_invariants(tree, S, sigma)
+    # sampled access(i) == S[i]
+    rng = np.random.default_rng(cfg)
+    idx = rng.integers(0, S.size, 200_000)
+    got = tree.access(torch.from_numpy(idx).cuda()).cpu().numpy()
+    assert np.array_equal(got, S[idx].astype(np.int64))
