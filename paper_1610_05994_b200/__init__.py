@@ -123,6 +123,9 @@ def set_profile_events(events: list | None):
         _lib.wt_set_profile_events(None, 0)
         _prof_keep = None
         return
+    for e in events:            # torch creates the CUDA event lazily, on first record
+        if not e.cuda_event:
+            e.record()
     arr = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
     _prof_keep = arr
     _lib.wt_set_profile_events(ctypes.cast(arr, _vp), len(events))

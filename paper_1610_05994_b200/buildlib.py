@@ -22,6 +22,10 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
+    # share the process's CUDA runtime with torch (streams/events created by
+    # torch are then valid handles here); a static cudart rejects them
+    "-cudart", "shared",
+    "-Xlinker", "-rpath,/usr/local/cuda/lib64",
 ]
 
 

@@ -108,15 +108,20 @@ wt_status check_args(uint64_t n, uint64_t sigma, uint32_t width) {
   return WT_OK;
 }
 
+// Records the thread-local profiling events (if any) around each launch.
+// A failed record (e.g. an uncreated event handle) is reported, not hidden.
 struct Launcher {
   cudaStream_t s;
   uint32_t k = 0;
-  void pre() {
-    if (g_events && 2 * k + 1 < g_event_count) cudaEventRecord((cudaEvent_t)g_events[2 * k], s);
+  cudaError_t pre() {
+    if (g_events && 2 * k + 1 < g_event_count) return cudaEventRecord((cudaEvent_t)g_events[2 * k], s);
+    return cudaSuccess;
   }
-  void post() {
-    if (g_events && 2 * k + 1 < g_event_count) cudaEventRecord((cudaEvent_t)g_events[2 * k + 1], s);
+  cudaError_t post() {
+    cudaError_t e = cudaSuccess;
+    if (g_events && 2 * k + 1 < g_event_count) e = cudaEventRecord((cudaEvent_t)g_events[2 * k + 1], s);
     ++k;
+    return e;
   }
 };
 
@@ -160,7 +165,7 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   // a1: histogram + range check
   note(K_HIST);
   if (!dry) {
-    lk.pre();
+    if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
     if (L <= SMEM_HIST_MAX_L) {
       const uint32_t nbins = 1u << L;
       uint32_t copies = (48u * 1024u) / (nbins * 4u);
@@ -176,21 +181,21 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       wt::k_hist_global<T><<<grid, 256, 0, stream>>>(seq, n, sigma, C, flag);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_hist");
-    lk.post();
+    if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
   }
 
   // a2: C = exclusive_scan(H) in place
   uint32_t epoch = 1, counter = 0;
   note(K_SCAN);
   if (!dry) {
-    lk.pre();
+    if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
     const uint64_t cnt = 1ull << L;
     wt::OpNodeOffsets op{C, cnt};
     const uint32_t grid = (uint32_t)((cnt + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
     wt::k_scan<wt::OpNodeOffsets><<<grid, wt::SCAN_THREADS, 0, stream>>>(op, cnt, status, counters + counter,
                                                                          epoch, flag);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(C)");
-    lk.post();
+    if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
   }
   ++epoch;
   ++counter;
@@ -200,18 +205,18 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     note(K_TABLES);
     note(K_TABLES);
     if (!dry) {
-      lk.pre();
+      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
       wt::OpTables op{C, tab, lvlbase, L};
       const uint32_t grid = (uint32_t)((c.tab_entries + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
       wt::k_scan<wt::OpTables><<<grid, wt::SCAN_THREADS, 0, stream>>>(op, c.tab_entries, status,
                                                                       counters + counter, epoch, flag);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(tables)");
-      lk.post();
-      lk.pre();
+      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
       const uint32_t g2 = (uint32_t)std::min<uint64_t>((c.tab_entries + 255) / 256, 148 * 16);
       wt::k_tables_fix<<<g2, 256, 0, stream>>>(C, tab, lvlbase, L, c.tab_entries, flag);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_tables_fix");
-      lk.post();
+      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
     }
     ++epoch;
     ++counter;
@@ -230,7 +235,7 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       const ulonglong2* t = last ? nullptr : tab + ((1ull << l) - 1);
       uint32_t* bits = out->bitmaps + (uint64_t)l * c.words;
       unsigned long long* sb = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
-      lk.pre();
+      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
       if (last)
         wt::k_level<T, false><<<grid, wt::LevelCfg<T>::THREADS, 0, stream>>>(
             in, o, n, sh, t, bits, c.words, sb, c.nsb, status, counters + counter, epoch, flag);
@@ -238,7 +243,7 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
         wt::k_level<T, true><<<grid, wt::LevelCfg<T>::THREADS, 0, stream>>>(
             in, o, n, sh, t, bits, c.words, sb, c.nsb, status, counters + counter, epoch, flag);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_level");
-      lk.post();
+      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
     }
     ++epoch;
     ++counter;

@@ -119,6 +119,22 @@ def test_async_status_and_determinism(wt):
     assert int(status.item()) == wt.WT_ERR_SYMBOL_RANGE
 
 
+def test_side_stream_and_events(wt):
+    # launches on a torch-created (non-default) stream, profiled with torch events
+    S = wt_inputs.random_case(3, 200_000, 256, "zipf")
+    d = to_dev(S)
+    s = torch.cuda.Stream()
+    plan = wt.launch_plan(S.size, 256, 1)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * len(plan))]
+    wt.set_profile_events(evs)
+    with torch.cuda.stream(s):
+        tree = wt.build_async(d, 256, stream=s)
+    wt.set_profile_events(None)
+    s.synchronize()
+    assert all(evs[2 * i].elapsed_time(evs[2 * i + 1]) >= 0 for i in range(len(plan)))
+    assert_same(tree, oracle.build(S, 256))
+
+
 def test_build_from_host_matches(wt):
     S = wt_inputs.random_case(11, 1_000_003, 230, "zipf")
     h = wt.build_from_host(torch.from_numpy(S), 230)
