@@ -30,7 +30,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 WT_OK, WT_ERR_ARG, WT_ERR_SYMBOL_RANGE, WT_ERR_INDEX, WT_ERR_CUDA, WT_ERR_WORKSPACE = range(6)
-KIND_NAMES = {1: "hist", 2: "scan", 3: "tables", 4: "level", 5: "last_level"}
+KIND_NAMES = {1: "hist", 2: "scan", 3: "tables", 4: "level", 5: "last_level", 6: "tile_scan"}
 
 
 class WtSizes(ctypes.Structure):

@@ -34,10 +34,29 @@ uint32_t levels_of(uint64_t sigma) {
 
 uint64_t level_tile(uint32_t width) {
   switch (width) {
-    case 1: return wt::LevelCfg<uint8_t>::TILE;
-    case 2: return wt::LevelCfg<uint16_t>::TILE;
-    default: return wt::LevelCfg<uint32_t>::TILE;
+    case 1: return wt::LvTile<uint8_t>::TILE;
+    case 2: return wt::LvTile<uint16_t>::TILE;
+    default: return wt::LvTile<uint32_t>::TILE;
   }
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || g_num_sms <= 0)
+      g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// opt in to > 48 KiB dynamic shared memory once per level-kernel instantiation
+template <typename T, bool SC>
+cudaError_t level_kernel_setup() {
+  static cudaError_t once = cudaFuncSetAttribute(wt::k_level<T, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)wt::level_smem_bytes<T>());
+  return once;
 }
 
 constexpr uint32_t SMEM_HIST_MAX_L = 12;  // 4096 bins * 4 B fit several copies in 48 KiB
@@ -45,14 +64,15 @@ constexpr int MAX_LOOKBACK_LAUNCHES = 64;
 
 // Workspace carve (all offsets 256-byte aligned).  The control block
 // [0, ctrl_bytes) is zeroed once per build: range flag, tile counters (one per
-// look-back launch), level bases, look-back status words (shared by every
-// look-back launch of the build, told apart by epoch).
+// look-back scan launch), level bases, look-back status words (shared by every
+// look-back scan of the build, told apart by epoch) and the per-level,
+// per-tile ones counts agg[l][t] (filled by the pass that writes T_l).
 struct Carve {
   uint32_t L = 0;
-  uint64_t words = 0, nsb = 0, c_len = 0;
+  uint64_t words = 0, nsb = 0, c_len = 0, ntiles = 0;
   uint64_t status_entries = 0, tab_entries = 0;
-  size_t off_flag = 0, off_counters = 0, off_lvlbase = 0, off_status = 0, ctrl_bytes = 0;
-  size_t off_tab = 0, off_bufA = 0, off_bufB = 0, total = 0;
+  size_t off_flag = 0, off_counters = 0, off_lvlbase = 0, off_status = 0, off_agg = 0, ctrl_bytes = 0;
+  size_t off_pre = 0, off_tab = 0, off_bufA = 0, off_bufB = 0, total = 0;
   // host-API extras (after total)
   size_t off_seq = 0, off_bits = 0, off_sb = 0, off_c = 0, host_total = 0;
 };
@@ -63,11 +83,12 @@ Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
   c.words = 16 * ((n + 511) / 512);
   c.nsb = (n + 511) / 512 + 1;
   c.c_len = (1ull << c.L) + 1;
-  const uint64_t tiles = (n + level_tile(width) - 1) / level_tile(width);
+  c.ntiles = (n + level_tile(width) - 1) / level_tile(width);
   const uint64_t scan_tiles = ((1ull << c.L) + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
   c.tab_entries = c.L >= 2 ? (1ull << (c.L - 1)) - 1 : 0;
   const uint64_t tab_tiles = (c.tab_entries + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
-  c.status_entries = std::max<uint64_t>(1, std::max(tiles, std::max(scan_tiles, tab_tiles)));
+  const uint64_t pre_tiles = (c.ntiles + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
+  c.status_entries = std::max<uint64_t>(1, std::max(pre_tiles, std::max(scan_tiles, tab_tiles)));
   size_t o = 0;
   c.off_flag = o;
   o += ALIGN;
@@ -77,7 +98,11 @@ Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
   o += align_up(64 * sizeof(uint64_t));
   c.off_status = o;
   o += align_up(c.status_entries * sizeof(uint64_t));
+  c.off_agg = o;
+  o += align_up((size_t)c.L * c.ntiles * sizeof(uint32_t));
   c.ctrl_bytes = o;
+  c.off_pre = o;
+  o += align_up(c.ntiles * sizeof(uint64_t));
   c.off_tab = o;
   o += align_up(c.tab_entries * sizeof(ulonglong2));
   const size_t seq_bytes = align_up(n * width);
@@ -125,7 +150,7 @@ struct Launcher {
   }
 };
 
-enum Kind : uint32_t { K_HIST = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5 };
+enum Kind : uint32_t { K_HIST = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6 };
 
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
 template <typename T>
@@ -142,6 +167,8 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   unsigned long long* lvlbase = reinterpret_cast<unsigned long long*>(ws + c.off_lvlbase);
   uint64_t* status = reinterpret_cast<uint64_t*>(ws + c.off_status);
   ulonglong2* tab = reinterpret_cast<ulonglong2*>(ws + c.off_tab);
+  uint32_t* agg = reinterpret_cast<uint32_t*>(ws + c.off_agg);
+  unsigned long long* pre = reinterpret_cast<unsigned long long*>(ws + c.off_pre);
   T* buf[2] = {reinterpret_cast<T*>(ws + c.off_bufA), reinterpret_cast<T*>(ws + c.off_bufB)};
   unsigned long long* C = dry ? nullptr : reinterpret_cast<unsigned long long*>(out->node_offsets);
   const uint32_t L = c.L;
@@ -168,17 +195,25 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
     if (L <= SMEM_HIST_MAX_L) {
       const uint32_t nbins = 1u << L;
-      uint32_t copies = (48u * 1024u) / (nbins * 4u);
+      uint32_t copies = (46u * 1024u) / (nbins * 4u);  // + static reduction scratch stays < 48 KiB
       copies = std::max(1u, std::min(copies, 16u));
       const uint64_t nvec = n / (16 / sizeof(T));
       const uint64_t want = (nvec + 511) / 512;
-      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 148 * 4));
-      wt::k_hist_smem<T><<<grid, 512, copies * nbins * 4, stream>>>(seq, n, sigma, nbins, copies, C, flag);
+      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 4ull * num_sms()));
+      wt::k_hist_smem<T><<<grid, 512, copies * nbins * 4, stream>>>(seq, n, sigma, L, copies, C, L ? agg : nullptr,
+                                                                    flag);
+    } else if (L <= 16) {
+      static cudaError_t attr = cudaFuncSetAttribute(wt::k_hist_smem16<T>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+      if (attr != cudaSuccess) return fail_cuda(attr, "k_hist_smem16 smem attribute");
+      const uint32_t nbins = 1u << L;
+      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n + 65535) / 65536, num_sms()));
+      wt::k_hist_smem16<T><<<grid, 1024, nbins * 2, stream>>>(seq, n, sigma, L, C, agg, flag);
     } else {
       const uint64_t nvec = n / (16 / sizeof(T));
       const uint64_t want = (nvec + 255) / 256;
-      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 148 * 8));
-      wt::k_hist_global<T><<<grid, 256, 0, stream>>>(seq, n, sigma, C, flag);
+      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 8ull * num_sms()));
+      wt::k_hist_global<T><<<grid, 512, 0, stream>>>(seq, n, sigma, L, C, agg, flag);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_hist");
     if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
@@ -223,10 +258,29 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   }
 
   // a3 / a4: one pass per level
-  constexpr uint64_t TILE = wt::LevelCfg<T>::TILE;
-  const uint32_t grid = (uint32_t)((n + TILE - 1) / TILE);
+  constexpr uint64_t TILE = wt::LvTile<T>::TILE;
+  const uint64_t ntiles = (n + TILE - 1) / TILE;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, 2ull * (uint64_t)num_sms());
+  const size_t lsmem = wt::level_smem_bytes<T>();
+  if (!dry) {
+    if ((e = level_kernel_setup<T, true>()) != cudaSuccess) return fail_cuda(e, "k_level smem attribute");
+    if ((e = level_kernel_setup<T, false>()) != cudaSuccess) return fail_cuda(e, "k_level smem attribute");
+  }
   for (uint32_t l = 0; l < L; ++l) {
     const bool last = (l + 1 == L);
+    // pre_l = exclusive scan of agg_l (ones of level l per tile)
+    note(K_TSCAN);
+    if (!dry) {
+      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      wt::OpTilePrefix op{agg + (uint64_t)l * c.ntiles, pre};
+      const uint32_t g = (uint32_t)((c.ntiles + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+      wt::k_scan<wt::OpTilePrefix><<<g, wt::SCAN_THREADS, 0, stream>>>(op, c.ntiles, status, counters + counter,
+                                                                       epoch, flag);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(tile prefix)");
+      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    }
+    ++epoch;
+    ++counter;
     note(last ? K_LAST : K_LEVEL);
     if (!dry) {
       const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
@@ -235,18 +289,17 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       const ulonglong2* t = last ? nullptr : tab + ((1ull << l) - 1);
       uint32_t* bits = out->bitmaps + (uint64_t)l * c.words;
       unsigned long long* sb = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
+      uint32_t* agg_next = last ? nullptr : agg + (uint64_t)(l + 1) * c.ntiles;
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
       if (last)
-        wt::k_level<T, false><<<grid, wt::LevelCfg<T>::THREADS, 0, stream>>>(
-            in, o, n, sh, t, bits, c.words, sb, c.nsb, status, counters + counter, epoch, flag);
+        wt::k_level<T, false><<<grid, wt::LV_THREADS, lsmem, stream>>>(in, o, n, sh, t, bits, c.words, sb, c.nsb,
+                                                                         pre, agg_next, flag);
       else
-        wt::k_level<T, true><<<grid, wt::LevelCfg<T>::THREADS, 0, stream>>>(
-            in, o, n, sh, t, bits, c.words, sb, c.nsb, status, counters + counter, epoch, flag);
+        wt::k_level<T, true><<<grid, wt::LV_THREADS, lsmem, stream>>>(in, o, n, sh, t, bits, c.words, sb, c.nsb,
+                                                                        pre, agg_next, flag);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_level");
       if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
     }
-    ++epoch;
-    ++counter;
   }
   if (count) *count = nk;
   return WT_OK;

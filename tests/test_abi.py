@@ -81,8 +81,10 @@ def test_build_validates_before_touching_the_device(wt):
 
 
 def test_launch_plan(wt):
-    assert wt.launch_plan(1 << 20, 256, 1) == ["hist", "scan", "tables", "tables"] + ["level"] * 7 + ["last_level"]
-    assert wt.launch_plan(1 << 20, 4, 1) == ["hist", "scan", "tables", "tables", "level", "last_level"]
-    assert wt.launch_plan(100, 2, 1) == ["hist", "scan", "last_level"]
+    lv = ["tile_scan", "level"]
+    last = ["tile_scan", "last_level"]
+    assert wt.launch_plan(1 << 20, 256, 1) == ["hist", "scan", "tables", "tables"] + lv * 7 + last
+    assert wt.launch_plan(1 << 20, 4, 1) == ["hist", "scan", "tables", "tables"] + lv + last
+    assert wt.launch_plan(100, 2, 1) == ["hist", "scan"] + last
     assert wt.launch_plan(100, 1, 1) == ["hist", "scan"]
     assert wt.launch_plan(0, 16, 1) == []
