@@ -52,10 +52,20 @@ int num_sms() {
 }
 
 // opt in to > 48 KiB dynamic shared memory once per level-kernel instantiation
+// and size the persistent grid: every resident CTA slot of every SM.
 template <typename T, bool SC>
-cudaError_t level_kernel_setup() {
-  static cudaError_t once = cudaFuncSetAttribute(wt::k_level<T, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)wt::level_smem_bytes<T>());
+cudaError_t level_kernel_setup(int* blocks_per_sm) {
+  static int bps = 0;
+  static cudaError_t once = [] {
+    cudaError_t e = cudaFuncSetAttribute(wt::k_level<T, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)wt::level_smem_bytes<T>());
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, wt::k_level<T, SC>, wt::LV_THREADS,
+                                                      wt::level_smem_bytes<T>());
+    if (bps < 1) bps = 1;
+    return e;
+  }();
+  *blocks_per_sm = bps;
   return once;
 }
 
@@ -260,12 +270,14 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   // a3 / a4: one pass per level
   constexpr uint64_t TILE = wt::LvTile<T>::TILE;
   const uint64_t ntiles = (n + TILE - 1) / TILE;
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, 2ull * (uint64_t)num_sms());
   const size_t lsmem = wt::level_smem_bytes<T>();
+  int bps_sc = 1, bps_last = 1;
   if (!dry) {
-    if ((e = level_kernel_setup<T, true>()) != cudaSuccess) return fail_cuda(e, "k_level smem attribute");
-    if ((e = level_kernel_setup<T, false>()) != cudaSuccess) return fail_cuda(e, "k_level smem attribute");
+    if ((e = level_kernel_setup<T, true>(&bps_sc)) != cudaSuccess) return fail_cuda(e, "k_level setup");
+    if ((e = level_kernel_setup<T, false>(&bps_last)) != cudaSuccess) return fail_cuda(e, "k_level setup");
   }
+  const uint32_t grid_sc = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_sc * (uint64_t)num_sms());
+  const uint32_t grid_last = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_last * (uint64_t)num_sms());
   for (uint32_t l = 0; l < L; ++l) {
     const bool last = (l + 1 == L);
     // pre_l = exclusive scan of agg_l (ones of level l per tile)
@@ -292,10 +304,10 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       uint32_t* agg_next = last ? nullptr : agg + (uint64_t)(l + 1) * c.ntiles;
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
       if (last)
-        wt::k_level<T, false><<<grid, wt::LV_THREADS, lsmem, stream>>>(in, o, n, sh, t, bits, c.words, sb, c.nsb,
+        wt::k_level<T, false><<<grid_last, wt::LV_THREADS, lsmem, stream>>>(in, o, n, sh, t, bits, c.words, sb, c.nsb,
                                                                          pre, agg_next, flag);
       else
-        wt::k_level<T, true><<<grid, wt::LV_THREADS, lsmem, stream>>>(in, o, n, sh, t, bits, c.words, sb, c.nsb,
+        wt::k_level<T, true><<<grid_sc, wt::LV_THREADS, lsmem, stream>>>(in, o, n, sh, t, bits, c.words, sb, c.nsb,
                                                                         pre, agg_next, flag);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_level");
       if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");

@@ -26,16 +26,16 @@ __device__ __forceinline__ uint32_t msb_mask32(uint32_t bit) {
 
 // Block-cooperative sweep over S in groups of HIST_G level tiles.  vec(v,
 // valid) is called warp-uniformly for each 16-byte vector (lanes of a warp
-// hold 32 consecutive vectors); scal(x) for the < 16 bytes past the last
-// whole vector.  red: shared scratch [2][B/32][HIST_G].
+// hold 32 consecutive vectors, always inside one level tile); scal(x) for the
+// < 16 bytes past the last whole vector.  red: shared scratch [HIST_G].
 template <typename T, int B, class VecFn, class ScalarFn>
 __device__ __forceinline__ void hist_tiles(const T* __restrict__ S, uint64_t n, uint32_t L,
                                            uint32_t* __restrict__ agg0, uint32_t* red, VecFn vec, ScalarFn scal) {
   constexpr uint32_t PER = 16 / sizeof(T);
   constexpr uint32_t TILE = LvTile<T>::TILE;
-  constexpr uint32_t VT = TILE / PER;  // vectors per tile (1024)
+  constexpr uint32_t VT = TILE / PER;  // vectors per level tile
   constexpr int K = HIST_G * (int)VT / B;
-  static_assert(K * B == HIST_G * (int)VT && (int)VT % B == 0, "group layout: B must divide a tile's vectors");
+  static_assert(K * B == HIST_G * (int)VT && VT % 32 == 0, "group layout");
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t bit = L ? L - 1 : 0;
   const uint32_t m32 = L ? msb_mask32<T>(bit) : 0u;
@@ -43,12 +43,10 @@ __device__ __forceinline__ void hist_tiles(const T* __restrict__ S, uint64_t n, 
   const uint64_t ngroups = (ntiles + HIST_G - 1) / HIST_G;
   const uint64_t nvec = n / PER;
   const uint64_t last_tile = ntiles ? ntiles - 1 : 0;
-  uint32_t parity = 0;
+  if (agg0 && tid < HIST_G) red[tid] = 0;
+  __syncthreads();
   for (uint64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
     const uint64_t v0 = g * HIST_G * VT;
-    uint32_t ones[HIST_G];
-#pragma unroll
-    for (int i = 0; i < HIST_G; ++i) ones[i] = 0;
     uint4 v[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -59,10 +57,14 @@ __device__ __forceinline__ void hist_tiles(const T* __restrict__ S, uint64_t n, 
     for (int k = 0; k < K; ++k) {
       const uint64_t idx = v0 + (uint64_t)k * B + tid;
       const bool valid = idx < nvec;
-      const int gi = (k * B) / (int)VT;
+      uint32_t ones = 0;
       if (valid)
-        ones[gi] += (uint32_t)(__popc(v[k].x & m32) + __popc(v[k].y & m32) + __popc(v[k].z & m32) +
-                               __popc(v[k].w & m32));
+        ones = (uint32_t)(__popc(v[k].x & m32) + __popc(v[k].y & m32) + __popc(v[k].z & m32) +
+                          __popc(v[k].w & m32));
+      if (agg0) {
+        const uint32_t w = __reduce_add_sync(FULL, ones);
+        if (lane == 0 && w) atomicAdd(&red[(k * B + (int)warp * 32) / (int)VT], w);
+      }
       vec(v[k], valid);
     }
     if (v0 + HIST_G * VT > nvec) {  // this group holds the scalar tail (all inside the last tile)
@@ -72,26 +74,16 @@ __device__ __forceinline__ void hist_tiles(const T* __restrict__ S, uint64_t n, 
         tail += (x >> bit) & 1u;
         scal(x);
       }
-      const uint64_t gi_tail = last_tile - g * HIST_G;
-#pragma unroll
-      for (int i = 0; i < HIST_G; ++i)
-        if ((uint64_t)i == gi_tail) ones[i] += L ? tail : 0u;
+      if (agg0 && L && tail) atomicAdd(&red[last_tile - g * HIST_G], tail);
     }
     if (agg0) {
-      uint32_t* r = red + parity * (B / 32) * HIST_G;
-#pragma unroll
-      for (int i = 0; i < HIST_G; ++i) {
-        const uint32_t s = __reduce_add_sync(FULL, ones[i]);
-        if (lane == 0) r[warp * HIST_G + i] = s;
-      }
       __syncthreads();
       if (tid < HIST_G) {
-        uint32_t s = 0;
-        for (int w = 0; w < B / 32; ++w) s += r[w * HIST_G + tid];
         const uint64_t t = g * HIST_G + tid;
-        if (t < ntiles) agg0[t] = s;
+        if (t < ntiles) agg0[t] = red[tid];
+        red[tid] = 0;
       }
-      parity ^= 1u;
+      __syncthreads();
     }
   }
 }
@@ -102,7 +94,7 @@ __global__ void __launch_bounds__(512) k_hist_smem(const T* __restrict__ S, uint
                                                    uint32_t copies, unsigned long long* __restrict__ H,
                                                    uint32_t* __restrict__ agg0, int32_t* __restrict__ flag) {
   extern __shared__ uint32_t sh_hist[];
-  __shared__ uint32_t red[2 * 16 * HIST_G];
+  __shared__ uint32_t red[HIST_G];
   const uint32_t nbins = 1u << L;
   for (uint32_t i = threadIdx.x; i < copies * nbins; i += blockDim.x) sh_hist[i] = 0;
   __syncthreads();
@@ -137,7 +129,7 @@ __global__ void __launch_bounds__(1024) k_hist_smem16(const T* __restrict__ S, u
                                                       uint32_t L, unsigned long long* __restrict__ H,
                                                       uint32_t* __restrict__ agg0, int32_t* __restrict__ flag) {
   extern __shared__ uint32_t sh16[];
-  __shared__ uint32_t red[2 * 32 * HIST_G];
+  __shared__ uint32_t red[HIST_G];
   const uint32_t nbins = 1u << L;
   for (uint32_t i = threadIdx.x; i < (nbins + 1) / 2; i += blockDim.x) sh16[i] = 0;
   __syncthreads();
@@ -177,7 +169,7 @@ template <typename T>
 __global__ void __launch_bounds__(512) k_hist_global(const T* __restrict__ S, uint64_t n, uint64_t sigma,
                                                      uint32_t L, unsigned long long* __restrict__ H,
                                                      uint32_t* __restrict__ agg0, int32_t* __restrict__ flag) {
-  __shared__ uint32_t red[2 * 16 * HIST_G];
+  __shared__ uint32_t red[HIST_G];
   constexpr uint32_t PER = 16 / sizeof(T);
   const uint32_t lane = threadIdx.x & 31;
   bool bad = false;

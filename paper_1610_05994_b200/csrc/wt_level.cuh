@@ -4,37 +4,38 @@
 // l < L-1, T_{l+1} = T_l stably partitioned inside every level-l node by bit
 // sh = L-1-l (Alg. 1 lines 8-13, with the "C[node]++" cursors
 // replaced by closed-form ranks; node of s at level l is s >> (sh+1),
-// Proposition 1).
+// Proposition 1).  Global destinations, with r(j) the ones of
+// level l before position j, ob[v] the ones before node v and Zn[v] the zeros
+// before the end of node v (node tables, built from C):
+//   b = 0: dest = j - r(j) + ob[v]            b = 1: dest = r(j) + Zn[v]
 //
-// Execution model (B200-first, not the paper's per-level thread):
-//   * persistent CTAs (2 per SM), tiles of 16 KiB assigned round-robin; each
-//     CTA keeps LV_STAGES tiles in flight with cp.async.bulk (TMA bulk copy)
-//     into shared memory, completion on mbarriers;
-//   * NO look-back: the ones of level l in every tile (agg_l[t]) were counted
-//     by the pass that wrote T_l (the histogram pass for l = 0), and a tiny
-//     scan turned them into pre_l[t] before this pass, so tiles are
-//     independent.  While writing T_{l+1} this pass counts agg_{l+1};
-//   * phase A  -- ballot: warp w turns 32 consecutive positions into one
-//                 bitmap word with __ballot_sync (bit = (s >> sh) & 1) and, in
-//                 the same sweep, a "segment head" word (node changes);
-//   * phase B  -- popcounts -> warp scan -> block scan + pre_l[tile] give the
-//                 global rank r(j); bitmap words and SB[t] = r(512 t) go
-//                 straight to HBM;
-//   * phase C  -- the tile's node segments become <= 2 runs each (zeros run ->
-//                 left child, ones run -> right child); every run gets a
-//                 shared-memory staging window whose start is congruent to its
-//                 HBM destination modulo 16 bytes;
-//   * phase D  -- every symbol is stored into its run's staging window
-//                 (stable: position inside the run = zeros/ones before it);
-//   * phase E  -- the staging windows are written out as aligned 16-byte
-//                 vectors (partial vectors only at run edges), counting the
-//                 next level's bit per destination tile (agg_{l+1}).
-//   Tiles with more than LV_MAXSEG node segments (very deep levels with tiny
-//   nodes) scatter each symbol directly instead of phases C-E.
-//
-// Global destinations (ob[v] = ones of level l before node v, Zn[v] = zeros
-// of level l before node v+1; both from the node tables built from C):
-//   b = 0: dest = (j - r(j)) + ob[v]        b = 1: dest = r(j) + Zn[v]
+// Execution model (B200-first, not the paper's thread-per-level):
+//   * persistent CTAs of 256 threads, several per SM; tiles of 8 KiB of
+//     symbols (a multiple of 512 positions: every bitmap word and superblock
+//     belongs to one tile), assigned round-robin; LV_STAGES tiles in flight per
+//     CTA with cp.async.bulk (TMA bulk copy) into shared memory on mbarriers;
+//   * NO look-back: the ones of level l in every tile (agg_l[t]) were counted by
+//     the pass that wrote T_l (the histogram pass for l = 0) and a tiny scan
+//     turned them into pre_l[t], so the tiles of a pass are independent;
+//   * phase A/B (thread owns 32 consecutive bytes): SWAR bit extraction, the
+//     bitmap word(s), warp + block scan of popcounts -> tile-local rank R(q),
+//     superblocks SB[t] = r(512 t);
+//   * the tile's symbols are partitioned IN PLACE in the shared stage buffer.
+//     Nodes are sorted along T_l, so the tile is: a first segment (node vF,
+//     may start before the tile), interior nodes (wholly inside the tile, so
+//     by node locality their destinations are exactly their own positions:
+//     an identity region), and a last segment (node vL, may run past the
+//     tile).  Interior symbols go to (dest - T0); the first and last
+//     segments' zeros/ones runs go to four side regions, each staged at an
+//     offset congruent to its HBM destination modulo 16 bytes;
+//   * phase D (thread handles 8 words, word w = tid + 256 k: lanes touch
+//     consecutive 32-bit words, so the byte stores are bank-conflict free)
+//     writes every symbol to its stage position;
+//   * phase E: one thread issues <= 5 TMA bulk stores (cp.async.bulk
+//     shared->global) for the 16-byte-aligned body of each region; threads
+//     store the <= 10 partial edge chunks and count, per destination tile, the
+//     next level's bit of the written symbols (agg_{l+1}), aggregated in
+//     shared memory and flushed with <= 10 global atomics per tile.
 #pragma once
 #include "wt_device.cuh"
 
@@ -64,6 +65,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -75,47 +90,41 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ uint32_t lanemask_le() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
-  return m;
-}
 
 // ------------------------------------------------------------ configuration
-constexpr int LV_THREADS = 512;
+constexpr int LV_THREADS = 256;
 constexpr int LV_WARPS = LV_THREADS / 32;
-constexpr int LV_STAGES = 3;
-constexpr int LV_MAXSEG = 256;
-constexpr int LV_MAXRUN = 2 * LV_MAXSEG;
-static_assert(LV_MAXRUN <= LV_THREADS, "one thread per run in phase C");
+constexpr int LV_STAGES = 4;
+constexpr int LV_MINB = 4;    // CTAs per SM the register budget is sized for
+constexpr int LV_NREG = 5;    // regions: identity, first zeros/ones, last zeros/ones
+constexpr int LV_NKEY = 2 * LV_NREG;
 
-// Every thread owns 32 consecutive bytes of the tile: E symbols.  For uint8 a
-// thread's E bits are exactly one 32-bit bitmap word.
 template <typename T>
 struct LvTile {
-  static constexpr int E = 32 / (int)sizeof(T);        // symbols per thread
-  static constexpr int TILE = LV_THREADS * E;          // 16 KiB, a multiple of 512 positions
-  static constexpr int A = 16 / (int)sizeof(T);        // symbols per 16-byte vector
-  static constexpr int TPW = 32 / E;                   // threads per bitmap word (1, 2, 4)
-  static constexpr int OUTCAP = TILE + A * LV_MAXRUN + A;
+  static constexpr int E = 32 / (int)sizeof(T);    // symbols per thread in phase A (32 bytes)
+  static constexpr int TILE = LV_THREADS * E;      // symbols per tile (8 KiB)
+  static constexpr int A = 16 / (int)sizeof(T);    // symbols per 16-byte chunk
+  static constexpr int SPW = 4 / (int)sizeof(T);   // symbols per 32-bit word
+  static constexpr int WPT = TILE / SPW / LV_THREADS;  // words per thread in phase D (8)
+  static constexpr int TPW = 32 / E;               // threads per bitmap word (1, 2, 4)
+  static constexpr int MARGIN = 4 * A;             // side-region slack before/after the tile
+  static constexpr int BUF = TILE + 2 * MARGIN;    // stage buffer (symbols)
+  static_assert(TILE % 512 == 0, "tiles hold whole superblocks");
+  static_assert(WPT == 8, "phase D reads the thread-owner info of 8-word groups");
 };
 
 template <typename T>
 struct LevelSmem {
   using C = LvTile<T>;
-  alignas(128) T in[LV_STAGES][C::TILE];
-  alignas(16) T out[C::OUTCAP];
-  uint32_t tmask[LV_THREADS];  // bit k = bit sh of the thread's k-th symbol
-  uint32_t tpre[LV_THREADS];   // tile-local exclusive prefix per thread, packed (heads << 16) | ones
-  uint32_t seg_start[LV_MAXSEG + 1];
-  int32_t run_base[LV_MAXRUN];  // staging base of run r (see phase D)
-  uint32_t run_s[LV_MAXRUN];    // staging start (symbols)
-  uint32_t run_len[LV_MAXRUN];
-  uint32_t run_chunk0[LV_MAXRUN + 1];
-  unsigned long long run_d[LV_MAXRUN];
+  alignas(128) T buf[LV_STAGES][C::BUF];  // TMA lands at buf[s][MARGIN]; partitioned in place
+  uint2 own[LV_THREADS];                  // per phase-A thread: {bit mask, tile-local ones before}
   uint32_t warp_tot[LV_WARPS];
-  uint32_t warp_tot2[LV_WARPS];
-  uint32_t total;
+  int32_t s1, am, Rs1, Ram;               // first-segment end, last-segment start, ranks there
+  int32_t K[4];                           // K0F, K1F, K0L, K1L (shared addresses in symbols)
+  int32_t rbase[LV_NREG], rlen[LV_NREG], ksplit[LV_NREG];
+  long long gofs[LV_NREG];                // HBM position of stage position q: q + gofs[r]
+  unsigned long long dtile[LV_NKEY];      // destination tile of each (region, half) key
+  uint32_t cnt[LV_NKEY];                  // next-level ones per key
   alignas(8) unsigned long long bar[LV_STAGES];
 };
 
@@ -163,30 +172,42 @@ __device__ __forceinline__ uint32_t sym_of(const uint32_t (&xw)[8], int k) {
   return xw[k];
 }
 
-// Adds `cnt` to agg[tau] once per group of lanes (in `mask`) that share tau.
-__device__ __forceinline__ void agg_add(uint32_t* agg, uint32_t mask, uint32_t tau, uint32_t cnt) {
-  const uint32_t grp = __match_any_sync(mask, tau);
-  const uint32_t tot = __reduce_add_sync(grp, cnt);
-  if (tot && (threadIdx.x & 31) == (uint32_t)(__ffs(grp) - 1)) atomicAdd(&agg[tau], tot);
+// st.shared of the low sizeof(T) bytes of v at shared byte address a
+template <typename T>
+__device__ __forceinline__ void st_shared(uint32_t a, uint32_t v) {
+  if (sizeof(T) == 1) asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
+  else if (sizeof(T) == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v));
+  else asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
 }
+
+template <typename T>
+__device__ __forceinline__ uint32_t sym_in_word(uint32_t x, int j) {
+  if (sizeof(T) == 1) return (x >> (8 * j)) & 0xffu;
+  if (sizeof(T) == 2) return (x >> (16 * j)) & 0xffffu;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t lowmask(uint32_t k) { return k >= 32 ? 0xffffffffu : ((1u << k) - 1u); }
 
 // ------------------------------------------------------------ the kernel
 template <typename T, bool SCATTER>
-__global__ void __launch_bounds__(LV_THREADS, 2)
+__global__ void __launch_bounds__(LV_THREADS, LV_MINB)
     k_level(const T* __restrict__ in, T* __restrict__ out, uint64_t n, uint32_t sh,
             const ulonglong2* __restrict__ tab, uint32_t* __restrict__ bits, uint64_t words_per_level,
             unsigned long long* __restrict__ sb, uint64_t nsb, const unsigned long long* __restrict__ pre,
             uint32_t* __restrict__ agg_next, const int32_t* __restrict__ flag) {
   using Cfg = LvTile<T>;
-  constexpr int TILE = Cfg::TILE, A = Cfg::A, E = Cfg::E, TPW = Cfg::TPW;
+  constexpr int TILE = Cfg::TILE, A = Cfg::A, E = Cfg::E, TPW = Cfg::TPW, SPW = Cfg::SPW, WPT = Cfg::WPT;
+  constexpr int MARGIN = Cfg::MARGIN;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LevelSmem<T>& S = *reinterpret_cast<LevelSmem<T>*>(smem_raw);
 
   if (*flag) return;
   const uint64_t ntiles = (n + TILE - 1) / TILE;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t nsh = sh + 1;                                   // node id = symbol >> nsh
   const uint32_t nb_mask = SCATTER ? bitmask32<T>(sh - 1) : 0u;  // next level's bit
-  const uint32_t i0 = tid * E;                                  // first tile position of this thread
+  const uint32_t i0 = tid * E;                                   // first tile position (phase A)
 
   auto tile_of = [&](uint32_t it) -> uint64_t { return (uint64_t)blockIdx.x + (uint64_t)it * gridDim.x; };
   auto issue = [&](int s, uint64_t t) {  // thread 0: bulk-copy tile t into stage s
@@ -195,7 +216,7 @@ __global__ void __launch_bounds__(LV_THREADS, 2)
     const uint32_t bytes = (uint32_t)(len * sizeof(T)) & ~15u;
     fence_proxy_async_smem();
     mbar_arrive_expect_tx(&S.bar[s], bytes);
-    if (bytes) bulk_g2s(S.in[s], in + T0, bytes, &S.bar[s]);
+    if (bytes) bulk_g2s(S.buf[s] + MARGIN, in + T0, bytes, &S.bar[s]);
   };
 
   if (tid == 0) {
@@ -204,6 +225,7 @@ __global__ void __launch_bounds__(LV_THREADS, 2)
     for (int s = 0; s < LV_STAGES; ++s)
       if (tile_of(s) < ntiles) issue(s, tile_of(s));
   }
+  if (SCATTER && tid < LV_NKEY) S.cnt[tid] = 0;
   __syncthreads();
 
   for (uint32_t it = 0;; ++it) {
@@ -212,45 +234,26 @@ __global__ void __launch_bounds__(LV_THREADS, 2)
     if (tile >= ntiles) break;
     const uint64_t T0 = tile * (uint64_t)TILE;
     const uint32_t len = (uint32_t)min((uint64_t)TILE, n - T0);
-    const uint64_t P = pre[tile];  // ones of this level before the tile
+    const unsigned long long P = __ldg(&pre[tile]);  // ones of this level before the tile
+    T* const B = S.buf[s] + MARGIN;                  // tile position q lives at B[q]
     mbar_wait(&S.bar[s], (it / LV_STAGES) & 1u);
-    const T* xin = S.in[s];
     if (len < TILE) {  // tail bytes the 16-byte bulk copy did not cover
       const uint32_t done = ((len * (uint32_t)sizeof(T)) & ~15u) / (uint32_t)sizeof(T);
-      for (uint32_t i = done + tid; i < len; i += LV_THREADS) S.in[s][i] = in[T0 + i];
+      for (uint32_t i = done + tid; i < len; i += LV_THREADS) B[i] = in[T0 + i];
       __syncthreads();
     }
 
-    // ---------------- phase A: the thread's 32 bytes -> E bits (+ segment heads)
+    // ---------------- phase A: the thread's 32 bytes -> E bits, bitmap word(s)
     uint32_t xw[8];
     {
-      const uint4* src = reinterpret_cast<const uint4*>(xin) + 2 * tid;
+      const uint4* src = reinterpret_cast<const uint4*>(B + i0);
       const uint4 va = src[0], vb = src[1];
       xw[0] = va.x, xw[1] = va.y, xw[2] = va.z, xw[3] = va.w;
       xw[4] = vb.x, xw[5] = vb.y, xw[6] = vb.z, xw[7] = vb.w;
     }
     const uint32_t nvalid = (i0 >= len) ? 0u : min((uint32_t)E, len - i0);
-    const uint32_t vmask = (nvalid >= 32) ? 0xffffffffu : ((1u << nvalid) - 1u);
-    const uint32_t m = swar_bits<T>(xw, sh) & vmask;
-    uint32_t hm = 0;
-    if (SCATTER) {
-      const uint32_t nf = sym_of<T>(xw, 0) >> (sh + 1);
-      const uint32_t nl = sym_of<T>(xw, E - 1) >> (sh + 1);
-      uint32_t prev = __shfl_up_sync(FULL, nl, 1);
-      if (lane == 0) prev = (tid > 0) ? ((uint32_t)xin[i0 - 1] >> (sh + 1)) : nf;
-      if (nvalid < (uint32_t)E || nf != nl || nf != prev) {
-        uint32_t p = prev;
-#pragma unroll
-        for (int k = 0; k < E; ++k) {
-          const uint32_t nd = sym_of<T>(xw, k) >> (sh + 1);
-          if (nd != p) hm |= 1u << k;
-          p = nd;
-        }
-        if (tid == 0) hm &= ~1u;  // the tile start is not a head
-        hm &= vmask;
-      }
-    }
-    // bitmap word(s): TPW threads per 32-bit word
+    const uint32_t m = swar_bits<T>(xw, sh) & lowmask(nvalid);
+    const uint32_t nbm = SCATTER ? (swar_bits<T>(xw, sh - 1) & lowmask(nvalid)) : 0u;  // next level's bits
     {
       uint32_t w = m;
       if (TPW > 1) {
@@ -261,187 +264,281 @@ __global__ void __launch_bounds__(LV_THREADS, 2)
       const uint64_t gw = (T0 + i0) / 32;
       if ((lane % TPW) == 0 && gw < words_per_level) bits[gw] = w;
     }
-    // ---------------- phase B: tile-local ranks (packed heads/ones), superblocks
-    const uint32_t c = ((uint32_t)__popc(hm) << 16) | (uint32_t)__popc(m);
+    const uint32_t c = (uint32_t)__popc(m);
     const uint32_t incl = warp_incl_scan_u32(c);
     if (lane == 31) S.warp_tot[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t wtot = (lane < (uint32_t)LV_WARPS) ? S.warp_tot[lane] : 0u;
-      const uint32_t wi = warp_incl_scan_u32(wtot);
-      if (lane < (uint32_t)LV_WARPS) S.warp_tot2[lane] = wi - wtot;
-      if (lane == 31) S.total = wi;
-    }
-    __syncthreads();
-    const uint32_t tot = S.total;
-    const uint32_t tot_ones = tot & 0xffffu;
-    const uint32_t nseg = (tot >> 16) + 1;
-    const uint32_t mypre = S.warp_tot2[warp] + incl - c;
-    if ((i0 & 511u) == 0 && T0 + i0 < n) sb[(T0 + i0) >> 9] = P + (mypre & 0xffffu);
-    if (tid == 0 && T0 + TILE >= n) sb[nsb - 1] = P + tot_ones;
 
+    uint32_t vF = 0, vL = 0;
+    ulonglong2 tabF = make_ulonglong2(0, 0), tabL = make_ulonglong2(0, 0);
+    uint32_t dw[WPT];
     if (SCATTER) {
-      if (nseg <= (uint32_t)LV_MAXSEG) {
-        S.tmask[tid] = m;
-        S.tpre[tid] = mypre;
-        if (hm) {  // segment starts
-          uint32_t h = hm, g = (mypre >> 16) + 1;
-          while (h) {
-            const int b = __ffs(h) - 1;
-            h &= h - 1;
-            S.seg_start[g++] = i0 + (uint32_t)b;
-          }
-        }
-        if (tid == 0) {
-          S.seg_start[0] = 0;
-          S.seg_start[nseg] = len;
-        }
-        __syncthreads();
-        // tile-local exclusive rank of position x in [0, len]
-        auto Rloc = [&](uint32_t x) -> uint32_t {
-          if (x >= len) return tot_ones;
-          const uint32_t t = x / E, r = x % E;
-          return (S.tpre[t] & 0xffffu) + (uint32_t)__popc(S.tmask[t] & ((1u << r) - 1u));
-        };
-        // ---------------- phase C: runs (2 per segment), staging windows
-        const uint32_t nrun = 2 * nseg;
-        uint32_t a = 0, Ra = 0;
-        if (tid < nrun) {
-          const uint32_t g = tid >> 1;
-          a = S.seg_start[g];
-          const uint32_t e = S.seg_start[g + 1];
-          Ra = Rloc(a);
-          const uint32_t Re = Rloc(e);
-          const uint32_t v = (uint32_t)xin[a] >> (sh + 1);
-          const ulonglong2 te = __ldg(&tab[v]);
-          if (tid & 1) {
-            S.run_len[tid] = Re - Ra;
-            S.run_d[tid] = P + Ra + te.y;
-          } else {
-            S.run_len[tid] = (e - Re) - (a - Ra);
-            S.run_d[tid] = (T0 - P) + (a - Ra) + te.x;
-          }
-        }
-        __syncthreads();
-        uint32_t packed = 0, pad = 0;
-        if (tid < nrun) {
-          const uint32_t L_ = S.run_len[tid];
-          const unsigned long long D_ = S.run_d[tid];
-          const uint32_t prev_end = tid ? (uint32_t)((S.run_d[tid - 1] + S.run_len[tid - 1]) & (A - 1)) : 0u;
-          pad = ((uint32_t)(D_ & (A - 1)) - prev_end) & (A - 1);
-          const uint32_t nch = L_ ? (uint32_t)((D_ + L_ + A - 1) / A - D_ / A) : 0u;
-          packed = (nch << 16) | (pad + L_);
-        }
-        const uint32_t pin = warp_incl_scan_u32(packed);
-        if (lane == 31) S.warp_tot[warp] = pin;
-        __syncthreads();
-        if (warp == 0) {
-          const uint32_t wtot = (lane < (uint32_t)LV_WARPS) ? S.warp_tot[lane] : 0u;
-          const uint32_t wi = warp_incl_scan_u32(wtot);
-          if (lane < (uint32_t)LV_WARPS) S.warp_tot2[lane] = wi - wtot;
-          if (lane == 31) S.run_chunk0[nrun] = wi >> 16;
-        }
-        __syncthreads();
-        if (tid < nrun) {
-          const uint32_t ex = S.warp_tot2[warp] + pin - packed;
-          const uint32_t sstart = (ex & 0xffffu) + pad;
-          S.run_s[tid] = sstart;
-          S.run_chunk0[tid] = ex >> 16;
-          // zeros run: pos = sstart + (i - R(i)) - (a - Ra);  ones run: pos = sstart + R(i) - Ra
-          S.run_base[tid] = (tid & 1) ? (int32_t)sstart - (int32_t)Ra : (int32_t)sstart - (int32_t)(a - Ra);
-        }
-        __syncthreads();
-        // ---------------- phase D: symbols into their staging windows
-        {
-          uint32_t g = mypre >> 16;
-          uint32_t R = mypre & 0xffffu;
-          int32_t po = S.run_base[2 * g + 1] + (int32_t)R;
-          int32_t pz = S.run_base[2 * g] + (int32_t)(i0 - R);
-          if (hm == 0 && nvalid == (uint32_t)E) {
+      vF = (uint32_t)B[0] >> nsh;
+      vL = (uint32_t)B[len - 1] >> nsh;
+      if (tid == 0) {
+        tabF = __ldg(&tab[vF]);
+        tabL = __ldg(&tab[vL]);
+      }
+      // phase D's words, read before anyone overwrites the stage
+      const uint32_t* W = reinterpret_cast<const uint32_t*>(B);
 #pragma unroll
-            for (int k = 0; k < E; ++k) {
-              const uint32_t b = (m >> k) & 1u;
-              S.out[b ? po : pz] = (T)sym_of<T>(xw, k);
-              po += (int32_t)b;
-              pz += 1 - (int32_t)b;
-            }
-          } else {
+      for (int k = 0; k < WPT; ++k) dw[k] = W[tid + LV_THREADS * k];
+    }
+    __syncthreads();  // B1: warp totals; every read of the stage's phase-A data done
+
+    if (!SCATTER) {
+      if (tid == 0 && tile_of(it + LV_STAGES) < ntiles) issue(s, tile_of(it + LV_STAGES));
+    } else if (tid < LV_NKEY) {  // flush the previous tile's next-level counts
+      const uint32_t v = S.cnt[tid];
+      if (v) {
+        atomicAdd(&agg_next[S.dtile[tid]], v);
+        S.cnt[tid] = 0;
+      }
+    }
+    // block prefix: every warp scans the LV_WARPS warp totals itself
+    uint32_t wpre, tot;
+    {
+      const uint32_t wt = (lane < (uint32_t)LV_WARPS) ? S.warp_tot[lane] : 0u;
+      const uint32_t wi = warp_incl_scan_u32(wt);
+      wpre = __shfl_sync(FULL, wi - wt, warp);
+      tot = __shfl_sync(FULL, wi, LV_WARPS - 1);
+    }
+    const uint32_t mypre = wpre + incl - c;
+    if ((i0 & 511u) == 0 && T0 + i0 < n) sb[(T0 + i0) >> 9] = P + mypre;
+    if (tid == 0 && T0 + TILE >= n) sb[nsb - 1] = P + tot;
+    if (!SCATTER) continue;
+
+    S.own[tid] = make_uint2(m, mypre);
+    if (vF != vL && nvalid > 0) {  // segment finders (nodes are non-decreasing along T_l)
+      const uint32_t prevnode = tid ? ((uint32_t)B[i0 - 1] >> nsh) : vF;
+      uint32_t nlast = 0;
 #pragma unroll
-            for (int k = 0; k < E; ++k) {
-              if ((uint32_t)k < nvalid) {
-                if ((hm >> k) & 1u) {
-                  ++g;
-                  const uint32_t Rk = R + (uint32_t)__popc(m & ((1u << k) - 1u));
-                  po = S.run_base[2 * g + 1] + (int32_t)Rk;
-                  pz = S.run_base[2 * g] + (int32_t)(i0 + k - Rk);
-                }
-                const uint32_t b = (m >> k) & 1u;
-                S.out[b ? po : pz] = (T)sym_of<T>(xw, k);
-                po += (int32_t)b;
-                pz += 1 - (int32_t)b;
-              }
-            }
+      for (int q = 0; q < E; ++q)
+        if ((uint32_t)q + 1 == nvalid) nlast = sym_of<T>(xw, q) >> nsh;
+      // monotone nodes: the boundary's offset in the thread's range is the
+      // number of its symbols before it (no dynamic register indexing)
+      if (prevnode == vF && nlast != vF) {
+        uint32_t k = 0;
+#pragma unroll
+        for (int q = 0; q < E; ++q) k += ((uint32_t)q < nvalid && (sym_of<T>(xw, q) >> nsh) == vF) ? 1u : 0u;
+        S.s1 = (int32_t)(i0 + k);
+        S.Rs1 = (int32_t)(mypre + __popc(m & lowmask(k)));
+      }
+      if (prevnode != vL && nlast == vL) {
+        uint32_t k = 0;
+#pragma unroll
+        for (int q = 0; q < E; ++q) k += ((uint32_t)q < nvalid && (sym_of<T>(xw, q) >> nsh) != vL) ? 1u : 0u;
+        S.am = (int32_t)(i0 + k);
+        S.Ram = (int32_t)(mypre + __popc(m & lowmask(k)));
+      }
+    }
+    __syncthreads();  // B2: own[], finder results
+
+    // ---------------- constants of the tile's regions (one thread)
+    if (tid == 0) {
+      const bool one = (vF == vL);
+      const int32_t s1 = one ? (int32_t)len : S.s1, am = one ? (int32_t)len : S.am;
+      const int32_t Rs1 = one ? (int32_t)tot : S.Rs1, Ram = one ? (int32_t)tot : S.Ram;
+      const int32_t z0 = s1 - Rs1, o0 = Rs1;
+      const int32_t om = (int32_t)tot - Ram, zm = ((int32_t)len - am) - om;
+      const long long D0z = (long long)T0 - (long long)P + (long long)tabF.x;
+      const long long D0o = (long long)P + (long long)tabF.y;
+      const long long Dmz = (long long)T0 + am - (long long)P - Ram + (long long)tabL.x;
+      const long long Dmo = (long long)P + Ram + (long long)tabL.y;
+      auto rup = [](int32_t x) { return (x + A - 1) / A * A; };
+      const int32_t b1 = (int32_t)(D0z & (A - 1));
+      const int32_t b2 = rup(b1 + z0) + (int32_t)(D0o & (A - 1));
+      const int32_t b3 = rup(MARGIN + am) + (int32_t)(Dmz & (A - 1));
+      const int32_t b4 = rup(b3 + zm) + (int32_t)(Dmo & (A - 1));
+      const int32_t base[LV_NREG] = {MARGIN + s1, b1, b2, b3, b4};
+      const int32_t rl[LV_NREG] = {am - s1, z0, o0, zm, om};
+      const long long go[LV_NREG] = {(long long)T0 - MARGIN, D0z - b1, D0o - b2, Dmz - b3, Dmo - b4};
+      const uint32_t sbuf = smem_u32(S.buf[s]) / (uint32_t)sizeof(T);  // in symbols
+      S.K[0] = (int32_t)sbuf + b1;
+      S.K[1] = (int32_t)sbuf + b2;
+      S.K[2] = (int32_t)sbuf + b3 - am + Ram;
+      S.K[3] = (int32_t)sbuf + b4 - Ram;
+      S.s1 = s1;
+      S.am = am;
+      S.Ram = Ram;
+#pragma unroll
+      for (int r = 0; r < LV_NREG; ++r) {
+        S.rbase[r] = base[r];
+        S.rlen[r] = rl[r];
+        S.gofs[r] = go[r];
+        const long long d0 = (long long)base[r] + go[r];  // HBM destination of the region's first symbol
+        const unsigned long long t0 = (unsigned long long)d0 / TILE;
+        S.dtile[2 * r] = (r == 0) ? tile : t0;
+        S.dtile[2 * r + 1] = t0 + 1;
+        // region symbols with rank < ksplit land in destination tile t0, the rest in t0 + 1
+        S.ksplit[r] = (r == 0) ? 0x7fffffff : (int32_t)min((long long)rl[r], (long long)(t0 + 1) * TILE - d0);
+      }
+    }
+    __syncthreads();  // B3: constants
+
+    // ---------------- next-level ones per (region, destination tile), thread-owned symbols
+    {
+      const int32_t s1 = S.s1, am = S.am, Ram = S.Ram;
+      const uint32_t vmask = lowmask(nvalid);
+      const uint32_t fm = lowmask((uint32_t)min(max(s1 - (int32_t)i0, 0), E));             // first segment
+      const uint32_t lm = vmask & ~lowmask((uint32_t)min(max(am - (int32_t)i0, 0), E));    // last segment
+      const uint32_t im = vmask & ~fm & ~lm;                                               // interior
+      // count of nbm bits among the set bits of M, split at the k-th (by rank
+      // rank0, rank0+1, ... of M's set bits in position order)
+      auto split = [&](uint32_t M, int32_t rank0, int32_t k, uint32_t& lo, uint32_t& hi) {
+        const int32_t nM = __popc(M);
+        uint32_t Mlo;
+        if (rank0 + nM <= k) Mlo = M;
+        else if (rank0 >= k) Mlo = 0;
+        else {  // the one thread per region holding the split
+          Mlo = 0;
+          uint32_t x = M;
+          for (int32_t j = k - rank0; j > 0; --j) {
+            Mlo |= x & (0u - x);
+            x &= x - 1;
           }
         }
-        __syncthreads();
-        // ---------------- phase E: aligned 16-byte write-out + next-level tile counts
-        const uint32_t nch_total = S.run_chunk0[nrun];
-        for (uint32_t base = 0; base < nch_total; base += LV_THREADS) {
-          const uint32_t ch = base + tid;
-          uint32_t tau = 0xffffffffu, cnt = 0;
-          if (ch < nch_total) {
-            uint32_t lo = 0, hi = nrun;  // largest r with run_chunk0[r] <= ch
-            while (hi - lo > 1) {
-              const uint32_t mid = (lo + hi) >> 1;
-              if (S.run_chunk0[mid] <= ch) lo = mid;
-              else hi = mid;
-            }
-            const unsigned long long Dr = S.run_d[lo];
-            const uint32_t Lr = S.run_len[lo], sr = S.run_s[lo];
-            const unsigned long long D = (Dr / A) * A + (unsigned long long)(ch - S.run_chunk0[lo]) * A;
-            const long long off = (long long)D - (long long)Dr;
-            tau = (uint32_t)(D / TILE);
-            if (off >= 0 && off + A <= (long long)Lr) {
-              const uint4 v = *reinterpret_cast<const uint4*>(&S.out[sr + off]);
-              *reinterpret_cast<uint4*>(out + D) = v;
-              cnt = (uint32_t)(__popc(v.x & nb_mask) + __popc(v.y & nb_mask) + __popc(v.z & nb_mask) +
-                               __popc(v.w & nb_mask));
-            } else {
+        lo = (uint32_t)__popc(nbm & Mlo);
+        hi = (uint32_t)__popc(nbm & M & ~Mlo);
+      };
+      uint32_t cnt[LV_NKEY];
+      if (vF == vL) {  // block-uniform: one segment, only the first-segment runs
+        split(vmask & ~m, (int32_t)(i0 - mypre), S.ksplit[1], cnt[2], cnt[3]);
+        split(m, (int32_t)mypre, S.ksplit[2], cnt[4], cnt[5]);
 #pragma unroll
-              for (int q = 0; q < A; ++q) {
-                const long long o = off + q;
-                if (o >= 0 && o < (long long)Lr) {
-                  const T x = S.out[sr + o];
-                  out[D + q] = x;
-                  cnt += ((uint32_t)x >> (sh - 1)) & 1u;
-                }
-              }
-            }
-          }
-          agg_add(agg_next, FULL, tau, cnt);
+        for (int key = 2; key < 6; ++key) {
+          const uint32_t sum = __reduce_add_sync(FULL, cnt[key]);
+          if (lane == 0 && sum) atomicAdd(&S.cnt[key], sum);
         }
       } else {
-        // deep level, many tiny nodes: scatter every symbol straight to HBM
-        uint64_t r = P + (mypre & 0xffffu);
+        cnt[0] = (uint32_t)__popc(nbm & im);
+        cnt[1] = 0;
+        split(fm & ~m, (int32_t)(i0 - mypre), S.ksplit[1], cnt[2], cnt[3]);
+        split(fm & m, (int32_t)mypre, S.ksplit[2], cnt[4], cnt[5]);
+        const int32_t qs = max((int32_t)i0, am);
+        const int32_t Rq = ((int32_t)i0 >= am) ? (int32_t)mypre : Ram;
+        split(lm & ~m, (qs - am) - (Rq - Ram), S.ksplit[3], cnt[6], cnt[7]);
+        split(lm & m, Rq - Ram, S.ksplit[4], cnt[8], cnt[9]);
 #pragma unroll
-        for (int k = 0; k < E; ++k) {
-          uint32_t tau = 0xffffffffu, cnt = 0;
-          if ((uint32_t)k < nvalid) {
-            const uint32_t x = sym_of<T>(xw, k);
-            const uint32_t b = (m >> k) & 1u;
-            const ulonglong2 e = __ldg(&tab[x >> (sh + 1)]);
-            const uint64_t dest = b ? (r + e.y) : (T0 + i0 + k - r + e.x);
-            out[dest] = (T)x;
-            r += b;
-            tau = (uint32_t)(dest / TILE);
-            cnt = (x >> (sh - 1)) & 1u;
-          }
-          agg_add(agg_next, FULL, tau, cnt);
+        for (int key = 0; key < LV_NKEY; ++key) {
+          if (key == 1) continue;
+          if (key > 1 && S.rlen[key >> 1] == 0) continue;  // block-uniform
+          const uint32_t sum = __reduce_add_sync(FULL, cnt[key]);
+          if (lane == 0 && sum) atomicAdd(&S.cnt[key], sum);
         }
       }
     }
-    __syncthreads();  // stage s and the staging buffer are free again
-    if (tid == 0 && tile_of(it + LV_STAGES) < ntiles) issue(s, tile_of(it + LV_STAGES));
+
+    // ---------------- phase D: every symbol to its stage position
+    {
+      const int32_t K0F = S.K[0], K1F = S.K[1], K0L = S.K[2], K1L = S.K[3];
+      const int32_t sbufM = (int32_t)(smem_u32(S.buf[s]) / (uint32_t)sizeof(T)) + MARGIN;
+      auto consts = [&](uint32_t v, int32_t& K0, int32_t& K1) {
+        if (v == vF) {
+          K0 = K0F;
+          K1 = K1F;
+        } else if (v == vL) {
+          K0 = K0L;
+          K1 = K1L;
+        } else {  // interior node: stage position = HBM destination - T0 + MARGIN
+          const ulonglong2 t = __ldg(&tab[v]);
+          K0 = (int32_t)((long long)t.x - (long long)P) + sbufM;
+          K1 = (int32_t)((long long)t.y + (long long)P - (long long)T0) + sbufM;
+        }
+      };
+      const uint32_t sub = (tid & 7u) * SPW;
+      const uint32_t submask = lowmask(sub);
+      if (vF == vL && len == (uint32_t)TILE) {  // block-uniform: one segment, full tile
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) {
+          const uint32_t w = tid + LV_THREADS * k;
+          const uint2 ow = S.own[w >> 3];
+          const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
+          const uint32_t m4 = ow.x >> sub;
+          const uint32_t x = dw[k];
+          int32_t az = (int32_t)(w * SPW - R) + K0F, ao = (int32_t)R + K1F;
+#pragma unroll
+          for (int j = 0; j < SPW; ++j) {
+            const bool b = (m4 >> j) & 1u;
+            st_shared<T>((uint32_t)(b ? ao : az) * (uint32_t)sizeof(T), x >> (8 * sizeof(T) * j));
+            if (b) ++ao;
+            else ++az;
+          }
+        }
+      } else
+#pragma unroll
+      for (int k = 0; k < WPT; ++k) {
+        const uint32_t w = tid + LV_THREADS * k;
+        const uint32_t q0 = w * SPW;
+        if (q0 >= len) break;
+        const uint2 ow = S.own[w >> 3];
+        const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
+        const uint32_t m4 = (ow.x >> sub) & ((1u << SPW) - 1u);
+        const uint32_t x = dw[k];
+        const uint32_t nv = min((uint32_t)SPW, len - q0);
+        const uint32_t v0 = sym_in_word<T>(x, 0) >> nsh;
+        const uint32_t vl = sym_in_word<T>(x, SPW - 1) >> nsh;
+        if (nv == (uint32_t)SPW && v0 == vl) {
+          int32_t K0, K1;
+          consts(v0, K0, K1);
+          int32_t az = (int32_t)(q0 - R) + K0, ao = (int32_t)R + K1;
+#pragma unroll
+          for (int j = 0; j < SPW; ++j) {
+            const uint32_t b = (m4 >> j) & 1u;
+            st_shared<T>((uint32_t)(b ? ao : az) * (uint32_t)sizeof(T), x >> (8 * sizeof(T) * j));
+            ao += (int32_t)b;
+            az += 1 - (int32_t)b;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < SPW; ++j) {
+            if ((uint32_t)j < nv) {
+              const uint32_t sym = sym_in_word<T>(x, j);
+              int32_t K0, K1;
+              consts(sym >> nsh, K0, K1);
+              const uint32_t Rj = R + (uint32_t)__popc(m4 & lowmask(j));
+              const uint32_t b = (m4 >> j) & 1u;
+              st_shared<T>((uint32_t)(b ? (int32_t)Rj + K1 : (int32_t)(q0 + j - Rj) + K0) * (uint32_t)sizeof(T), sym);
+            }
+          }
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();  // B4: stage partitioned
+
+    // ---------------- phase E: TMA bulk stores of the aligned bodies, element stores of the edges
+    if (tid == 0) {
+#pragma unroll
+      for (int r = 0; r < LV_NREG; ++r) {
+        const int32_t b = S.rbase[r], l = S.rlen[r];
+        const int32_t fs = (b + A - 1) / A * A, fe = (b + l) / A * A;
+        if (l > 0 && fe > fs)
+          bulk_s2g(out + (S.gofs[r] + fs), S.buf[s] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
+      }
+      bulk_commit();
+    }
+    if (tid < (uint32_t)(2 * A * LV_NREG)) {
+      const int r = (int)(tid / (2 * A)), e = (int)(tid % (2 * A));
+      const int32_t b = S.rbase[r], l = S.rlen[r], end = b + l;
+      const int32_t fs = (b + A - 1) / A * A, fe = (b + l) / A * A;
+      const int32_t hend = min(fs, end);                             // head edge [b, hend), < A symbols
+      const int32_t q = (e < A) ? b + e : max(fe, hend) + (e - A);  // tail edge [max(fe, hend), end), < A
+      if (l > 0 && ((e < A) ? (q < hend) : (q < end))) out[S.gofs[r] + q] = S.buf[s][q];
+    }
+    // refill the previous tile's stage once its bulk stores have read it
+    if (tid == 0) {
+      bulk_wait_read<1>();
+      if (it >= 1 && tile_of(it - 1 + LV_STAGES) < ntiles)
+        issue((int)((it - 1) % LV_STAGES), tile_of(it - 1 + LV_STAGES));
+    }
+  }
+  if (SCATTER) {
+    __syncthreads();
+    if (tid < LV_NKEY) {
+      const uint32_t v = S.cnt[tid];
+      if (v) atomicAdd(&agg_next[S.dtile[tid]], v);
+    }
+    if (tid == 0) bulk_wait<0>();
   }
 }
 
