@@ -94,29 +94,31 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
 // ------------------------------------------------------------ configuration
 constexpr int LV_THREADS = 256;
 constexpr int LV_WARPS = LV_THREADS / 32;
-constexpr int LV_STAGES = 4;
-constexpr int LV_MINB = 4;    // CTAs per SM the register budget is sized for
 constexpr int LV_NREG = 5;    // regions: identity, first zeros/ones, last zeros/ones
 constexpr int LV_NKEY = 2 * LV_NREG;
 
 template <typename T>
 struct LvTile {
-  static constexpr int E = 32 / (int)sizeof(T);    // symbols per thread in phase A (32 bytes)
-  static constexpr int TILE = LV_THREADS * E;      // symbols per tile (8 KiB)
-  static constexpr int A = 16 / (int)sizeof(T);    // symbols per 16-byte chunk
-  static constexpr int SPW = 4 / (int)sizeof(T);   // symbols per 32-bit word
-  static constexpr int WPT = TILE / SPW / LV_THREADS;  // words per thread in phase D (8)
-  static constexpr int TPW = 32 / E;               // threads per bitmap word (1, 2, 4)
+  static constexpr int W = (int)sizeof(T);
+  static constexpr int E = (W == 4) ? 16 : 32;     // symbols per thread in phase A
+  static constexpr int TILE = LV_THREADS * E;      // symbols per tile: 8192 / 8192 / 4096
+  static constexpr int A = 16 / W;                 // symbols per 16-byte chunk
+  static constexpr int SPW = 4 / W;                // symbols per 32-bit word
+  static constexpr int XW = E * W / 4;             // 32-bit words per phase-A thread (8 / 16 / 16)
+  static constexpr int WPT = TILE / SPW / LV_THREADS;  // words per thread in phase D (== XW)
+  static constexpr int TPW = 32 / E;               // threads per bitmap word (1, 1, 2)
   static constexpr int MARGIN = 4 * A;             // side-region slack before/after the tile
-  static constexpr int BUF = TILE + 2 * MARGIN;    // stage buffer (symbols)
+  static constexpr int BUF = TILE + 2 * MARGIN;    // ring buffer (symbols)
+  static constexpr int NB = (W == 1) ? 5 : 4;      // ring buffers per CTA
+  static constexpr int MINB = (W == 1) ? 4 : 3;    // CTAs per SM the register budget is sized for
   static_assert(TILE % 512 == 0, "tiles hold whole superblocks");
-  static_assert(WPT == 8, "phase D reads the thread-owner info of 8-word groups");
+  static_assert(WPT == XW && LV_THREADS % XW == 0, "phase D word / owner layout");
 };
 
 template <typename T>
 struct LevelSmem {
   using C = LvTile<T>;
-  alignas(128) T buf[LV_STAGES][C::BUF];  // TMA lands at buf[s][MARGIN]; partitioned in place
+  alignas(128) T buf[C::NB][C::BUF];      // ring: input tiles land at buf[b][MARGIN], outputs are staged
   uint2 own[LV_THREADS];                  // per phase-A thread: {bit mask, tile-local ones before}
   uint32_t warp_tot[LV_WARPS];
   int32_t s1, am, Rs1, Ram;               // first-segment end, last-segment start, ranks there
@@ -125,7 +127,7 @@ struct LevelSmem {
   long long gofs[LV_NREG];                // HBM position of stage position q: q + gofs[r]
   unsigned long long dtile[LV_NKEY];      // destination tile of each (region, half) key
   uint32_t cnt[LV_NKEY];                  // next-level ones per key
-  alignas(8) unsigned long long bar[LV_STAGES];
+  alignas(8) unsigned long long bar[C::NB];
 };
 
 template <typename T>
@@ -141,32 +143,32 @@ __device__ __forceinline__ uint32_t bitmask32(uint32_t bit) {  // `bit` of every
   return 1u << bit;
 }
 
-// bit `sh` of the E symbols held in xw[8] (32 bytes), symbol k -> bit k.
-template <typename T>
-__device__ __forceinline__ uint32_t swar_bits(const uint32_t (&xw)[8], uint32_t sh) {
+// bit `sh` of the symbols held in xw[NW] (little-endian), symbol k -> bit k.
+template <typename T, int NW>
+__device__ __forceinline__ uint32_t swar_bits(const uint32_t (&xw)[NW], uint32_t sh) {
   uint32_t m = 0;
   if (sizeof(T) == 1) {
     // gather bit sh of the 4 bytes of a word with one multiply:
     // (x & 0x01010101<<sh) * (1 + 2^7 + 2^14 + 2^21) puts byte j's bit at 21+sh+j
     const uint32_t msk = 0x01010101u << sh;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) m |= ((((xw[k] & msk) * 0x00204081u) >> (21 + sh)) & 0xfu) << (4 * k);
+    for (int k = 0; k < NW; ++k) m |= ((((xw[k] & msk) * 0x00204081u) >> (21 + sh)) & 0xfu) << (4 * k);
   } else if (sizeof(T) == 2) {
     const uint32_t msk = 0x00010001u << sh;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < NW; ++k) {
       const uint32_t t = xw[k] & msk;
       m |= (((t >> sh) | (t >> (sh + 15))) & 3u) << (2 * k);
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) m |= ((xw[k] >> sh) & 1u) << k;
+    for (int k = 0; k < NW; ++k) m |= ((xw[k] >> sh) & 1u) << k;
   }
   return m;
 }
 
-template <typename T>
-__device__ __forceinline__ uint32_t sym_of(const uint32_t (&xw)[8], int k) {
+template <typename T, int NW>
+__device__ __forceinline__ uint32_t sym_of(const uint32_t (&xw)[NW], int k) {
   if (sizeof(T) == 1) return (xw[k >> 2] >> (8 * (k & 3))) & 0xffu;
   if (sizeof(T) == 2) return (xw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
   return xw[k];
@@ -191,69 +193,78 @@ __device__ __forceinline__ uint32_t lowmask(uint32_t k) { return k >= 32 ? 0xfff
 
 // ------------------------------------------------------------ the kernel
 template <typename T, bool SCATTER>
-__global__ void __launch_bounds__(LV_THREADS, LV_MINB)
+__global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
     k_level(const T* __restrict__ in, T* __restrict__ out, uint64_t n, uint32_t sh,
             const ulonglong2* __restrict__ tab, uint32_t* __restrict__ bits, uint64_t words_per_level,
             unsigned long long* __restrict__ sb, uint64_t nsb, const unsigned long long* __restrict__ pre,
             uint32_t* __restrict__ agg_next, const int32_t* __restrict__ flag) {
   using Cfg = LvTile<T>;
   constexpr int TILE = Cfg::TILE, A = Cfg::A, E = Cfg::E, TPW = Cfg::TPW, SPW = Cfg::SPW, WPT = Cfg::WPT;
-  constexpr int MARGIN = Cfg::MARGIN;
+  constexpr int MARGIN = Cfg::MARGIN, NB = Cfg::NB, XW = Cfg::XW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LevelSmem<T>& S = *reinterpret_cast<LevelSmem<T>*>(smem_raw);
 
   if (*flag) return;
   const uint64_t ntiles = (n + TILE - 1) / TILE;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t nsh = sh + 1;                                   // node id = symbol >> nsh
-  const uint32_t nb_mask = SCATTER ? bitmask32<T>(sh - 1) : 0u;  // next level's bit
-  const uint32_t i0 = tid * E;                                   // first tile position (phase A)
+  const uint32_t nsh = sh + 1;  // node id = symbol >> nsh
+  const uint32_t i0 = tid * E;  // first tile position of this thread (phase A)
 
+  // Ring of NB buffers: tile `it` (the CTA's it-th) is loaded into buf[it % NB];
+  // with SCATTER its partitioned output is staged in buf[(it - 1) % NB] (the
+  // previous tile's input, free once that tile's phase D is done), whose
+  // bulk stores are read-complete one iteration later, when the buffer is
+  // refilled.  Without SCATTER every buffer is an input stage.
   auto tile_of = [&](uint32_t it) -> uint64_t { return (uint64_t)blockIdx.x + (uint64_t)it * gridDim.x; };
-  auto issue = [&](int s, uint64_t t) {  // thread 0: bulk-copy tile t into stage s
+  auto issue = [&](uint32_t it) {  // thread 0: bulk-copy the CTA's it-th tile into buf[it % NB]
+    const uint64_t t = tile_of(it);
+    if (t >= ntiles) return;
+    const int b = (int)(it % NB);
     const uint64_t T0 = t * (uint64_t)TILE;
     const uint64_t len = min((uint64_t)TILE, n - T0);
     const uint32_t bytes = (uint32_t)(len * sizeof(T)) & ~15u;
     fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&S.bar[s], bytes);
-    if (bytes) bulk_g2s(S.buf[s] + MARGIN, in + T0, bytes, &S.bar[s]);
+    mbar_arrive_expect_tx(&S.bar[b], bytes);
+    if (bytes) bulk_g2s(S.buf[b] + MARGIN, in + T0, bytes, &S.bar[b]);
   };
 
   if (tid == 0) {
-    for (int s = 0; s < LV_STAGES; ++s) mbar_init(&S.bar[s], 1);
+    for (int b = 0; b < NB; ++b) mbar_init(&S.bar[b], 1);
     fence_mbar_init();
-    for (int s = 0; s < LV_STAGES; ++s)
-      if (tile_of(s) < ntiles) issue(s, tile_of(s));
+    for (int b = 0; b < (SCATTER ? NB - 1 : NB); ++b) issue((uint32_t)b);
   }
   if (SCATTER && tid < LV_NKEY) S.cnt[tid] = 0;
   __syncthreads();
 
   for (uint32_t it = 0;; ++it) {
-    const int s = (int)(it % LV_STAGES);
     const uint64_t tile = tile_of(it);
     if (tile >= ntiles) break;
+    const int ib = (int)(it % NB), ob = (int)((it + NB - 1) % NB);
     const uint64_t T0 = tile * (uint64_t)TILE;
     const uint32_t len = (uint32_t)min((uint64_t)TILE, n - T0);
     const unsigned long long P = __ldg(&pre[tile]);  // ones of this level before the tile
-    T* const B = S.buf[s] + MARGIN;                  // tile position q lives at B[q]
-    mbar_wait(&S.bar[s], (it / LV_STAGES) & 1u);
+    T* const B = S.buf[ib] + MARGIN;                 // tile position q lives at B[q]
+    mbar_wait(&S.bar[ib], (it / NB) & 1u);
     if (len < TILE) {  // tail bytes the 16-byte bulk copy did not cover
       const uint32_t done = ((len * (uint32_t)sizeof(T)) & ~15u) / (uint32_t)sizeof(T);
       for (uint32_t i = done + tid; i < len; i += LV_THREADS) B[i] = in[T0 + i];
       __syncthreads();
     }
 
-    // ---------------- phase A: the thread's 32 bytes -> E bits, bitmap word(s)
-    uint32_t xw[8];
+    // ---------------- phase A: the thread's E symbols -> E bits, bitmap word(s)
+    uint32_t xw[XW];
     {
       const uint4* src = reinterpret_cast<const uint4*>(B + i0);
-      const uint4 va = src[0], vb = src[1];
-      xw[0] = va.x, xw[1] = va.y, xw[2] = va.z, xw[3] = va.w;
-      xw[4] = vb.x, xw[5] = vb.y, xw[6] = vb.z, xw[7] = vb.w;
+#pragma unroll
+      for (int v = 0; v < XW / 4; ++v) {
+        const uint4 q = src[v];
+        xw[4 * v] = q.x, xw[4 * v + 1] = q.y, xw[4 * v + 2] = q.z, xw[4 * v + 3] = q.w;
+      }
     }
     const uint32_t nvalid = (i0 >= len) ? 0u : min((uint32_t)E, len - i0);
-    const uint32_t m = swar_bits<T>(xw, sh) & lowmask(nvalid);
-    const uint32_t nbm = SCATTER ? (swar_bits<T>(xw, sh - 1) & lowmask(nvalid)) : 0u;  // next level's bits
+    const uint32_t vmask = lowmask(nvalid);
+    const uint32_t m = swar_bits<T>(xw, sh) & vmask;
+    const uint32_t nbm = SCATTER ? (swar_bits<T>(xw, sh - 1) & vmask) : 0u;  // next level's bits
     {
       uint32_t w = m;
       if (TPW > 1) {
@@ -270,7 +281,7 @@ __global__ void __launch_bounds__(LV_THREADS, LV_MINB)
 
     uint32_t vF = 0, vL = 0;
     ulonglong2 tabF = make_ulonglong2(0, 0), tabL = make_ulonglong2(0, 0);
-    uint32_t dw[WPT];
+    uint32_t nfirst = 0, nlast = 0;
     if (SCATTER) {
       vF = (uint32_t)B[0] >> nsh;
       vL = (uint32_t)B[len - 1] >> nsh;
@@ -278,16 +289,18 @@ __global__ void __launch_bounds__(LV_THREADS, LV_MINB)
         tabF = __ldg(&tab[vF]);
         tabL = __ldg(&tab[vL]);
       }
-      // phase D's words, read before anyone overwrites the stage
-      const uint32_t* W = reinterpret_cast<const uint32_t*>(B);
+      if (vF != vL) {
+        nfirst = tid ? ((uint32_t)B[i0 - 1] >> nsh) : vF;  // node just before the thread's range
 #pragma unroll
-      for (int k = 0; k < WPT; ++k) dw[k] = W[tid + LV_THREADS * k];
+        for (int q = 0; q < E; ++q)
+          if ((uint32_t)q + 1 == nvalid) nlast = sym_of<T>(xw, q) >> nsh;
+      }
     }
-    __syncthreads();  // B1: warp totals; every read of the stage's phase-A data done
+    __syncthreads();  // B1: warp totals
 
     if (!SCATTER) {
-      if (tid == 0 && tile_of(it + LV_STAGES) < ntiles) issue(s, tile_of(it + LV_STAGES));
-    } else if (tid < LV_NKEY) {  // flush the previous tile's next-level counts
+      if (tid == 0) issue(it + NB);  // every read of this buffer is done
+    } else if (tid < LV_NKEY) {      // flush the previous tile's next-level counts
       const uint32_t v = S.cnt[tid];
       if (v) {
         atomicAdd(&agg_next[S.dtile[tid]], v);
@@ -309,21 +322,16 @@ __global__ void __launch_bounds__(LV_THREADS, LV_MINB)
 
     S.own[tid] = make_uint2(m, mypre);
     if (vF != vL && nvalid > 0) {  // segment finders (nodes are non-decreasing along T_l)
-      const uint32_t prevnode = tid ? ((uint32_t)B[i0 - 1] >> nsh) : vF;
-      uint32_t nlast = 0;
-#pragma unroll
-      for (int q = 0; q < E; ++q)
-        if ((uint32_t)q + 1 == nvalid) nlast = sym_of<T>(xw, q) >> nsh;
       // monotone nodes: the boundary's offset in the thread's range is the
       // number of its symbols before it (no dynamic register indexing)
-      if (prevnode == vF && nlast != vF) {
+      if (nfirst == vF && nlast != vF) {
         uint32_t k = 0;
 #pragma unroll
         for (int q = 0; q < E; ++q) k += ((uint32_t)q < nvalid && (sym_of<T>(xw, q) >> nsh) == vF) ? 1u : 0u;
         S.s1 = (int32_t)(i0 + k);
         S.Rs1 = (int32_t)(mypre + __popc(m & lowmask(k)));
       }
-      if (prevnode != vL && nlast == vL) {
+      if (nfirst != vL && nlast == vL) {
         uint32_t k = 0;
 #pragma unroll
         for (int q = 0; q < E; ++q) k += ((uint32_t)q < nvalid && (sym_of<T>(xw, q) >> nsh) != vL) ? 1u : 0u;
@@ -352,11 +360,11 @@ __global__ void __launch_bounds__(LV_THREADS, LV_MINB)
       const int32_t base[LV_NREG] = {MARGIN + s1, b1, b2, b3, b4};
       const int32_t rl[LV_NREG] = {am - s1, z0, o0, zm, om};
       const long long go[LV_NREG] = {(long long)T0 - MARGIN, D0z - b1, D0o - b2, Dmz - b3, Dmo - b4};
-      const uint32_t sbuf = smem_u32(S.buf[s]) / (uint32_t)sizeof(T);  // in symbols
-      S.K[0] = (int32_t)sbuf + b1;
-      S.K[1] = (int32_t)sbuf + b2;
-      S.K[2] = (int32_t)sbuf + b3 - am + Ram;
-      S.K[3] = (int32_t)sbuf + b4 - Ram;
+      const int32_t sbuf = (int32_t)(smem_u32(S.buf[ob]) / (uint32_t)sizeof(T));  // in symbols
+      S.K[0] = sbuf + b1;
+      S.K[1] = sbuf + b2;
+      S.K[2] = sbuf + b3 - am + Ram;
+      S.K[3] = sbuf + b4 - Ram;
       S.s1 = s1;
       S.am = am;
       S.Ram = Ram;
@@ -377,13 +385,8 @@ __global__ void __launch_bounds__(LV_THREADS, LV_MINB)
 
     // ---------------- next-level ones per (region, destination tile), thread-owned symbols
     {
-      const int32_t s1 = S.s1, am = S.am, Ram = S.Ram;
-      const uint32_t vmask = lowmask(nvalid);
-      const uint32_t fm = lowmask((uint32_t)min(max(s1 - (int32_t)i0, 0), E));             // first segment
-      const uint32_t lm = vmask & ~lowmask((uint32_t)min(max(am - (int32_t)i0, 0), E));    // last segment
-      const uint32_t im = vmask & ~fm & ~lm;                                               // interior
-      // count of nbm bits among the set bits of M, split at the k-th (by rank
-      // rank0, rank0+1, ... of M's set bits in position order)
+      // count of nbm bits among the set bits of M, split at rank k (the set
+      // bits of M have ranks rank0, rank0+1, ... in position order)
       auto split = [&](uint32_t M, int32_t rank0, int32_t k, uint32_t& lo, uint32_t& hi) {
         const int32_t nM = __popc(M);
         uint32_t Mlo;
@@ -410,6 +413,10 @@ __global__ void __launch_bounds__(LV_THREADS, LV_MINB)
           if (lane == 0 && sum) atomicAdd(&S.cnt[key], sum);
         }
       } else {
+        const int32_t s1 = S.s1, am = S.am, Ram = S.Ram;
+        const uint32_t fm = lowmask((uint32_t)min(max(s1 - (int32_t)i0, 0), E));           // first segment
+        const uint32_t lm = vmask & ~lowmask((uint32_t)min(max(am - (int32_t)i0, 0), E));  // last segment
+        const uint32_t im = vmask & ~fm & ~lm;                                             // interior
         cnt[0] = (uint32_t)__popc(nbm & im);
         cnt[1] = 0;
         split(fm & ~m, (int32_t)(i0 - mypre), S.ksplit[1], cnt[2], cnt[3]);
@@ -428,10 +435,11 @@ __global__ void __launch_bounds__(LV_THREADS, LV_MINB)
       }
     }
 
-    // ---------------- phase D: every symbol to its stage position
+    // ---------------- phase D: every symbol from the input buffer to its stage position
     {
       const int32_t K0F = S.K[0], K1F = S.K[1], K0L = S.K[2], K1L = S.K[3];
-      const int32_t sbufM = (int32_t)(smem_u32(S.buf[s]) / (uint32_t)sizeof(T)) + MARGIN;
+      const int32_t sbufM = (int32_t)(smem_u32(S.buf[ob]) / (uint32_t)sizeof(T)) + MARGIN;
+      const uint32_t* Win = reinterpret_cast<const uint32_t*>(B);
       auto consts = [&](uint32_t v, int32_t& K0, int32_t& K1) {
         if (v == vF) {
           K0 = K0F;
@@ -445,16 +453,16 @@ __global__ void __launch_bounds__(LV_THREADS, LV_MINB)
           K1 = (int32_t)((long long)t.y + (long long)P - (long long)T0) + sbufM;
         }
       };
-      const uint32_t sub = (tid & 7u) * SPW;
+      const uint32_t sub = (tid % (uint32_t)XW) * SPW;  // word w = tid + 256 k: owner w / XW, offset (w % XW) * SPW
       const uint32_t submask = lowmask(sub);
       if (vF == vL && len == (uint32_t)TILE) {  // block-uniform: one segment, full tile
 #pragma unroll
         for (int k = 0; k < WPT; ++k) {
           const uint32_t w = tid + LV_THREADS * k;
-          const uint2 ow = S.own[w >> 3];
+          const uint2 ow = S.own[w / XW];
           const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
           const uint32_t m4 = ow.x >> sub;
-          const uint32_t x = dw[k];
+          const uint32_t x = Win[w];
           int32_t az = (int32_t)(w * SPW - R) + K0F, ao = (int32_t)R + K1F;
 #pragma unroll
           for (int j = 0; j < SPW; ++j) {
@@ -464,47 +472,49 @@ __global__ void __launch_bounds__(LV_THREADS, LV_MINB)
             else ++az;
           }
         }
-      } else
+      } else {
 #pragma unroll
-      for (int k = 0; k < WPT; ++k) {
-        const uint32_t w = tid + LV_THREADS * k;
-        const uint32_t q0 = w * SPW;
-        if (q0 >= len) break;
-        const uint2 ow = S.own[w >> 3];
-        const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
-        const uint32_t m4 = (ow.x >> sub) & ((1u << SPW) - 1u);
-        const uint32_t x = dw[k];
-        const uint32_t nv = min((uint32_t)SPW, len - q0);
-        const uint32_t v0 = sym_in_word<T>(x, 0) >> nsh;
-        const uint32_t vl = sym_in_word<T>(x, SPW - 1) >> nsh;
-        if (nv == (uint32_t)SPW && v0 == vl) {
-          int32_t K0, K1;
-          consts(v0, K0, K1);
-          int32_t az = (int32_t)(q0 - R) + K0, ao = (int32_t)R + K1;
+        for (int k = 0; k < WPT; ++k) {
+          const uint32_t w = tid + LV_THREADS * k;
+          const uint32_t q0 = w * SPW;
+          if (q0 >= len) break;
+          const uint2 ow = S.own[w / XW];
+          const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
+          const uint32_t m4 = (ow.x >> sub) & ((1u << SPW) - 1u);
+          const uint32_t x = Win[w];
+          const uint32_t nv = min((uint32_t)SPW, len - q0);
+          const uint32_t v0 = sym_in_word<T>(x, 0) >> nsh;
+          const uint32_t vl = sym_in_word<T>(x, SPW - 1) >> nsh;
+          if (nv == (uint32_t)SPW && v0 == vl) {
+            int32_t K0, K1;
+            consts(v0, K0, K1);
+            int32_t az = (int32_t)(q0 - R) + K0, ao = (int32_t)R + K1;
 #pragma unroll
-          for (int j = 0; j < SPW; ++j) {
-            const uint32_t b = (m4 >> j) & 1u;
-            st_shared<T>((uint32_t)(b ? ao : az) * (uint32_t)sizeof(T), x >> (8 * sizeof(T) * j));
-            ao += (int32_t)b;
-            az += 1 - (int32_t)b;
-          }
-        } else {
+            for (int j = 0; j < SPW; ++j) {
+              const bool b = (m4 >> j) & 1u;
+              st_shared<T>((uint32_t)(b ? ao : az) * (uint32_t)sizeof(T), x >> (8 * sizeof(T) * j));
+              if (b) ++ao;
+              else ++az;
+            }
+          } else {
 #pragma unroll
-          for (int j = 0; j < SPW; ++j) {
-            if ((uint32_t)j < nv) {
-              const uint32_t sym = sym_in_word<T>(x, j);
-              int32_t K0, K1;
-              consts(sym >> nsh, K0, K1);
-              const uint32_t Rj = R + (uint32_t)__popc(m4 & lowmask(j));
-              const uint32_t b = (m4 >> j) & 1u;
-              st_shared<T>((uint32_t)(b ? (int32_t)Rj + K1 : (int32_t)(q0 + j - Rj) + K0) * (uint32_t)sizeof(T), sym);
+            for (int j = 0; j < SPW; ++j) {
+              if ((uint32_t)j < nv) {
+                const uint32_t sym = sym_in_word<T>(x, j);
+                int32_t K0, K1;
+                consts(sym >> nsh, K0, K1);
+                const uint32_t Rj = R + (uint32_t)__popc(m4 & lowmask(j));
+                const uint32_t b = (m4 >> j) & 1u;
+                st_shared<T>((uint32_t)(b ? (int32_t)Rj + K1 : (int32_t)(q0 + j - Rj) + K0) * (uint32_t)sizeof(T),
+                             sym);
+              }
             }
           }
         }
       }
     }
     fence_proxy_async_smem();
-    __syncthreads();  // B4: stage partitioned
+    __syncthreads();  // B4: stage partitioned (and the input buffer fully read)
 
     // ---------------- phase E: TMA bulk stores of the aligned bodies, element stores of the edges
     if (tid == 0) {
@@ -513,7 +523,7 @@ __global__ void __launch_bounds__(LV_THREADS, LV_MINB)
         const int32_t b = S.rbase[r], l = S.rlen[r];
         const int32_t fs = (b + A - 1) / A * A, fe = (b + l) / A * A;
         if (l > 0 && fe > fs)
-          bulk_s2g(out + (S.gofs[r] + fs), S.buf[s] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
+          bulk_s2g(out + (S.gofs[r] + fs), S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
       }
       bulk_commit();
     }
@@ -523,13 +533,12 @@ __global__ void __launch_bounds__(LV_THREADS, LV_MINB)
       const int32_t fs = (b + A - 1) / A * A, fe = (b + l) / A * A;
       const int32_t hend = min(fs, end);                             // head edge [b, hend), < A symbols
       const int32_t q = (e < A) ? b + e : max(fe, hend) + (e - A);  // tail edge [max(fe, hend), end), < A
-      if (l > 0 && ((e < A) ? (q < hend) : (q < end))) out[S.gofs[r] + q] = S.buf[s][q];
+      if (l > 0 && ((e < A) ? (q < hend) : (q < end))) out[S.gofs[r] + q] = S.buf[ob][q];
     }
-    // refill the previous tile's stage once its bulk stores have read it
+    // the previous tile's output buffer: once its bulk stores have read it, load a new tile into it
     if (tid == 0) {
       bulk_wait_read<1>();
-      if (it >= 1 && tile_of(it - 1 + LV_STAGES) < ntiles)
-        issue((int)((it - 1) % LV_STAGES), tile_of(it - 1 + LV_STAGES));
+      if (it >= 1) issue(it + NB - 2);
     }
   }
   if (SCATTER) {
