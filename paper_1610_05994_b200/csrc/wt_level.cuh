@@ -111,6 +111,9 @@ struct LvTile {
   static constexpr int BUF = TILE + 2 * MARGIN;    // ring buffer (symbols)
   static constexpr int NB = (W == 1) ? 5 : 4;      // ring buffers per CTA
   static constexpr int MINB = (W == 1) ? 4 : 3;    // CTAs per SM the register budget is sized for
+  // segment table capacity (u8 scatter levels have <= 64 nodes); tiles with
+  // more segments look the node tables up in global memory instead
+  static constexpr int MAXSEG = (W == 1) ? 128 : 512;
   static_assert(TILE % 512 == 0, "tiles hold whole superblocks");
   static_assert(WPT == XW && LV_THREADS % XW == 0, "phase D word / owner layout");
 };
@@ -119,10 +122,14 @@ template <typename T>
 struct LevelSmem {
   using C = LvTile<T>;
   alignas(128) T buf[C::NB][C::BUF];      // ring: input tiles land at buf[b][MARGIN], outputs are staged
-  uint2 own[LV_THREADS];                  // per phase-A thread: {bit mask, tile-local ones before}
+  uint4 own[LV_THREADS];                  // per phase-A thread: {bit mask, ones | heads << 16 before, head mask, -}
+  uint16_t seg_a[C::MAXSEG + 1];          // segment g starts at tile position seg_a[g] (g >= 1)
+  uint16_t seg_R[C::MAXSEG + 1];          // tile-local ones before seg_a[g]
+  short2 kt[C::MAXSEG];                   // segment g: stage offsets {K0, K1} relative to the output buffer
+  uint32_t lut[16];                       // in-word stable partition selectors (partition_lut_entry)
   uint32_t warp_tot[LV_WARPS];
   int32_t s1, am, Rs1, Ram;               // first-segment end, last-segment start, ranks there
-  int32_t K[4];                           // K0F, K1F, K0L, K1L (shared addresses in symbols)
+  int32_t K[4];                           // K0F, K1F, K0L, K1L (relative to the output buffer, in symbols)
   int32_t rbase[LV_NREG], rlen[LV_NREG], ksplit[LV_NREG];
   long long gofs[LV_NREG];                // HBM position of stage position q: q + gofs[r]
   unsigned long long dtile[LV_NKEY];      // destination tile of each (region, half) key
@@ -174,12 +181,29 @@ __device__ __forceinline__ uint32_t sym_of(const uint32_t (&xw)[NW], int k) {
   return xw[k];
 }
 
-// st.shared of the low sizeof(T) bytes of v at shared byte address a
-template <typename T>
+// st.shared of the low sizeof(T) bytes of v at shared byte address a + OFF
+template <typename T, int OFF = 0>
 __device__ __forceinline__ void st_shared(uint32_t a, uint32_t v) {
-  if (sizeof(T) == 1) asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
-  else if (sizeof(T) == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v));
-  else asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
+  if (sizeof(T) == 1) asm volatile("st.shared.u8 [%0+%2], %1;" ::"r"(a), "r"(v), "n"(OFF));
+  else if (sizeof(T) == 2) asm volatile("st.shared.u16 [%0+%2], %1;" ::"r"(a), "r"(v), "n"(OFF));
+  else asm volatile("st.shared.u32 [%0+%2], %1;" ::"r"(a), "r"(v), "n"(OFF));
+}
+
+// Stable in-word partition of the SPW symbols of a 32-bit word by their bits
+// (bit j of `bits` = bit of symbol j): a PRMT selector that moves the zero
+// symbols to the low end (in order) and the one symbols after them (in
+// order), plus the number of zeros in bits 16..18.
+template <typename T>
+__host__ __device__ constexpr uint32_t partition_lut_entry(uint32_t bits) {
+  uint32_t sel = 0, k = 0, nz = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (uint32_t j = 0; j < 4 / sizeof(T); ++j)
+      if (((bits >> j) & 1u) == (uint32_t)pass) {
+        for (uint32_t byte = 0; byte < sizeof(T); ++byte) sel |= (j * sizeof(T) + byte) << (4 * (k * sizeof(T) + byte));
+        ++k;
+        nz += pass == 0;
+      }
+  return sel | (nz << 16);
 }
 
 template <typename T>
@@ -234,6 +258,7 @@ __global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
     for (int b = 0; b < (SCATTER ? NB - 1 : NB); ++b) issue((uint32_t)b);
   }
   if (SCATTER && tid < LV_NKEY) S.cnt[tid] = 0;
+  if (SCATTER && tid < 16) S.lut[tid] = partition_lut_entry<T>(tid);
   __syncthreads();
 
   for (uint32_t it = 0;; ++it) {
@@ -252,6 +277,11 @@ __global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
     }
 
     // ---------------- phase A: the thread's E symbols -> E bits, bitmap word(s)
+    uint32_t vF = 0, vL = 0;
+    if (SCATTER) {
+      vF = (uint32_t)B[0] >> nsh;
+      vL = (uint32_t)B[len - 1] >> nsh;
+    }
     uint32_t xw[XW];
     {
       const uint4* src = reinterpret_cast<const uint4*>(B + i0);
@@ -275,26 +305,25 @@ __global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
       const uint64_t gw = (T0 + i0) / 32;
       if ((lane % TPW) == 0 && gw < words_per_level) bits[gw] = w;
     }
-    const uint32_t c = (uint32_t)__popc(m);
+    // segment heads: positions q > 0 of the tile whose node differs from q-1's
+    uint32_t hm = 0;
+    if (SCATTER && vF != vL) {  // block-uniform
+      uint32_t prev = tid ? ((uint32_t)B[i0 - 1] >> nsh) : vF;
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        const uint32_t nd = sym_of<T>(xw, q) >> nsh;
+        hm |= (nd != prev ? 1u : 0u) << q;
+        prev = nd;
+      }
+      hm &= vmask;
+    }
+    const uint32_t c = ((uint32_t)__popc(hm) << 16) | (uint32_t)__popc(m);  // packed heads | ones
     const uint32_t incl = warp_incl_scan_u32(c);
     if (lane == 31) S.warp_tot[warp] = incl;
-
-    uint32_t vF = 0, vL = 0;
     ulonglong2 tabF = make_ulonglong2(0, 0), tabL = make_ulonglong2(0, 0);
-    uint32_t nfirst = 0, nlast = 0;
-    if (SCATTER) {
-      vF = (uint32_t)B[0] >> nsh;
-      vL = (uint32_t)B[len - 1] >> nsh;
-      if (tid == 0) {
-        tabF = __ldg(&tab[vF]);
-        tabL = __ldg(&tab[vL]);
-      }
-      if (vF != vL) {
-        nfirst = tid ? ((uint32_t)B[i0 - 1] >> nsh) : vF;  // node just before the thread's range
-#pragma unroll
-        for (int q = 0; q < E; ++q)
-          if ((uint32_t)q + 1 == nvalid) nlast = sym_of<T>(xw, q) >> nsh;
-      }
+    if (SCATTER && warp == 0) {
+      tabF = __ldg(&tab[vF]);
+      tabL = __ldg(&tab[vL]);
     }
     __syncthreads();  // B1: warp totals
 
@@ -308,42 +337,48 @@ __global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
       }
     }
     // block prefix: every warp scans the LV_WARPS warp totals itself
-    uint32_t wpre, tot;
+    uint32_t wpre, totp;
     {
       const uint32_t wt = (lane < (uint32_t)LV_WARPS) ? S.warp_tot[lane] : 0u;
       const uint32_t wi = warp_incl_scan_u32(wt);
       wpre = __shfl_sync(FULL, wi - wt, warp);
-      tot = __shfl_sync(FULL, wi, LV_WARPS - 1);
+      totp = __shfl_sync(FULL, wi, LV_WARPS - 1);
     }
-    const uint32_t mypre = wpre + incl - c;
+    const uint32_t prep = wpre + incl - c;
+    const uint32_t mypre = prep & 0xffffu, hpre = prep >> 16;
+    const uint32_t tot = totp & 0xffffu, nseg = (totp >> 16) + 1;
     if ((i0 & 511u) == 0 && T0 + i0 < n) sb[(T0 + i0) >> 9] = P + mypre;
     if (tid == 0 && T0 + TILE >= n) sb[nsb - 1] = P + tot;
     if (!SCATTER) continue;
 
-    S.own[tid] = make_uint2(m, mypre);
-    if (vF != vL && nvalid > 0) {  // segment finders (nodes are non-decreasing along T_l)
-      // monotone nodes: the boundary's offset in the thread's range is the
-      // number of its symbols before it (no dynamic register indexing)
-      if (nfirst == vF && nlast != vF) {
-        uint32_t k = 0;
-#pragma unroll
-        for (int q = 0; q < E; ++q) k += ((uint32_t)q < nvalid && (sym_of<T>(xw, q) >> nsh) == vF) ? 1u : 0u;
-        S.s1 = (int32_t)(i0 + k);
-        S.Rs1 = (int32_t)(mypre + __popc(m & lowmask(k)));
-      }
-      if (nfirst != vL && nlast == vL) {
-        uint32_t k = 0;
-#pragma unroll
-        for (int q = 0; q < E; ++q) k += ((uint32_t)q < nvalid && (sym_of<T>(xw, q) >> nsh) != vL) ? 1u : 0u;
-        S.am = (int32_t)(i0 + k);
-        S.Ram = (int32_t)(mypre + __popc(m & lowmask(k)));
+    S.own[tid] = make_uint4(m, prep, hm, 0u);
+    {  // segment table: start and rank of every segment g >= 1
+      uint32_t h = hm, g = hpre + 1;
+      while (h) {
+        const uint32_t k = (uint32_t)(__ffs(h) - 1);
+        h &= h - 1;
+        const int32_t a_ = (int32_t)(i0 + k), R_ = (int32_t)(mypre + __popc(m & lowmask(k)));
+        if (g <= (uint32_t)Cfg::MAXSEG) {
+          S.seg_a[g] = (uint16_t)a_;
+          S.seg_R[g] = (uint16_t)R_;
+        }
+        if (g == 1) {
+          S.s1 = a_;
+          S.Rs1 = R_;
+        }
+        if (g == nseg - 1) {
+          S.am = a_;
+          S.Ram = R_;
+        }
+        ++g;
       }
     }
-    __syncthreads();  // B2: own[], finder results
+    __syncthreads();  // B2: own[], segment table
 
-    // ---------------- constants of the tile's regions (one thread)
-    if (tid == 0) {
-      const bool one = (vF == vL);
+    const bool segtab = nseg <= (uint32_t)Cfg::MAXSEG;  // block-uniform
+    // ---------------- constants of the tile's regions (warp 0, lane r writes region r)
+    if (warp == 0) {
+      const bool one = (nseg == 1);
       const int32_t s1 = one ? (int32_t)len : S.s1, am = one ? (int32_t)len : S.am;
       const int32_t Rs1 = one ? (int32_t)tot : S.Rs1, Ram = one ? (int32_t)tot : S.Ram;
       const int32_t z0 = s1 - Rs1, o0 = Rs1;
@@ -357,29 +392,37 @@ __global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
       const int32_t b2 = rup(b1 + z0) + (int32_t)(D0o & (A - 1));
       const int32_t b3 = rup(MARGIN + am) + (int32_t)(Dmz & (A - 1));
       const int32_t b4 = rup(b3 + zm) + (int32_t)(Dmo & (A - 1));
-      const int32_t base[LV_NREG] = {MARGIN + s1, b1, b2, b3, b4};
-      const int32_t rl[LV_NREG] = {am - s1, z0, o0, zm, om};
-      const long long go[LV_NREG] = {(long long)T0 - MARGIN, D0z - b1, D0o - b2, Dmz - b3, Dmo - b4};
-      const int32_t sbuf = (int32_t)(smem_u32(S.buf[ob]) / (uint32_t)sizeof(T));  // in symbols
-      S.K[0] = sbuf + b1;
-      S.K[1] = sbuf + b2;
-      S.K[2] = sbuf + b3 - am + Ram;
-      S.K[3] = sbuf + b4 - Ram;
-      S.s1 = s1;
-      S.am = am;
-      S.Ram = Ram;
-#pragma unroll
-      for (int r = 0; r < LV_NREG; ++r) {
-        S.rbase[r] = base[r];
-        S.rlen[r] = rl[r];
-        S.gofs[r] = go[r];
-        const long long d0 = (long long)base[r] + go[r];  // HBM destination of the region's first symbol
-        const unsigned long long t0 = (unsigned long long)d0 / TILE;
+      const int32_t K0L = b3 - am + Ram, K1L = b4 - Ram;
+      if (lane < 4) S.K[lane] = lane == 0 ? b1 : lane == 1 ? b2 : lane == 2 ? K0L : K1L;
+      if (segtab) {
+        if (lane == 0) S.kt[0] = make_short2((short)b1, (short)b2);
+        if (lane == 1 && !one) S.kt[nseg - 1] = make_short2((short)K0L, (short)K1L);
+      }
+      if (lane == 5) {
+        S.s1 = s1;
+        S.am = am;
+        S.Ram = Ram;
+      }
+      if (lane < (uint32_t)LV_NREG) {
+        const int r = (int)lane;
+        const int32_t base = r == 0 ? MARGIN + s1 : r == 1 ? b1 : r == 2 ? b2 : r == 3 ? b3 : b4;
+        const int32_t rl = r == 0 ? am - s1 : r == 1 ? z0 : r == 2 ? o0 : r == 3 ? zm : om;
+        const long long D = r == 0 ? (long long)T0 + s1 : r == 1 ? D0z : r == 2 ? D0o : r == 3 ? Dmz : Dmo;
+        S.rbase[r] = base;
+        S.rlen[r] = rl;
+        S.gofs[r] = D - base;  // HBM destination of stage position q: q + gofs
+        const unsigned long long t0 = (unsigned long long)D / TILE;
         S.dtile[2 * r] = (r == 0) ? tile : t0;
         S.dtile[2 * r + 1] = t0 + 1;
         // region symbols with rank < ksplit land in destination tile t0, the rest in t0 + 1
-        S.ksplit[r] = (r == 0) ? 0x7fffffff : (int32_t)min((long long)rl[r], (long long)(t0 + 1) * TILE - d0);
+        S.ksplit[r] = (r == 0) ? 0x7fffffff : (int32_t)min((long long)rl, (long long)(t0 + 1) * TILE - D);
       }
+    } else if (segtab) {
+      // interior segment g (1 <= g <= nseg-2) lies wholly inside the tile: its
+      // stage positions are its own positions, zeros first then ones:
+      //   b = 0: q - R(q) + R(a_g) + MARGIN     b = 1: R(q) + a_{g+1} - R(a_{g+1}) + MARGIN
+      for (uint32_t g = tid - 31; g + 1 < nseg; g += LV_THREADS - 32)
+        S.kt[g] = make_short2((short)(S.seg_R[g] + MARGIN), (short)(S.seg_a[g + 1] - S.seg_R[g + 1] + MARGIN));
     }
     __syncthreads();  // B3: constants
 
@@ -392,19 +435,19 @@ __global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
         uint32_t Mlo;
         if (rank0 + nM <= k) Mlo = M;
         else if (rank0 >= k) Mlo = 0;
-        else {  // the one thread per region holding the split
-          Mlo = 0;
-          uint32_t x = M;
-          for (int32_t j = k - rank0; j > 0; --j) {
-            Mlo |= x & (0u - x);
-            x &= x - 1;
-          }
+        else {  // the one thread per region holding the split: lowest (k - rank0) set bits of M
+          const int32_t j = k - rank0;
+          uint32_t p = 0;
+#pragma unroll
+          for (uint32_t st = 16; st; st >>= 1)
+            if (__popc(M & lowmask(p + st)) <= j) p += st;
+          Mlo = M & lowmask(p);
         }
         lo = (uint32_t)__popc(nbm & Mlo);
         hi = (uint32_t)__popc(nbm & M & ~Mlo);
       };
       uint32_t cnt[LV_NKEY];
-      if (vF == vL) {  // block-uniform: one segment, only the first-segment runs
+      if (nseg == 1) {  // block-uniform: one segment, only the first-segment runs
         split(vmask & ~m, (int32_t)(i0 - mypre), S.ksplit[1], cnt[2], cnt[3]);
         split(m, (int32_t)mypre, S.ksplit[2], cnt[4], cnt[5]);
 #pragma unroll
@@ -437,65 +480,109 @@ __global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
 
     // ---------------- phase D: every symbol from the input buffer to its stage position
     {
-      const int32_t K0F = S.K[0], K1F = S.K[1], K0L = S.K[2], K1L = S.K[3];
-      const int32_t sbufM = (int32_t)(smem_u32(S.buf[ob]) / (uint32_t)sizeof(T)) + MARGIN;
+      const int32_t sbuf = (int32_t)(smem_u32(S.buf[ob]) / (uint32_t)sizeof(T));  // in symbols
       const uint32_t* Win = reinterpret_cast<const uint32_t*>(B);
-      auto consts = [&](uint32_t v, int32_t& K0, int32_t& K1) {
-        if (v == vF) {
-          K0 = K0F;
-          K1 = K1F;
-        } else if (v == vL) {
-          K0 = K0L;
-          K1 = K1L;
-        } else {  // interior node: stage position = HBM destination - T0 + MARGIN
-          const ulonglong2 t = __ldg(&tab[v]);
-          K0 = (int32_t)((long long)t.x - (long long)P) + sbufM;
-          K1 = (int32_t)((long long)t.y + (long long)P - (long long)T0) + sbufM;
+      const uint32_t sub = (tid % (uint32_t)XW) * SPW;  // word w = tid + 256 k: owner w / XW, offset (w % XW) * SPW
+      const uint32_t submask = lowmask(sub), subhead = lowmask(sub + 1);
+      // stores the SPW symbols of word x (tile position q0, R ones before it,
+      // bits m4) into segment (K0, K1) (stage offsets relative to the buffer)
+      auto lut_of = [&](uint32_t m4) -> uint32_t { return SPW == 1 ? 0u : S.lut[m4 & ((1u << SPW) - 1u)]; };
+      auto word_one_segment = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, int32_t K0, int32_t K1,
+                                  uint32_t e) {
+        const int32_t az = sbuf + (int32_t)(q0 - R) + K0;
+        if (SPW == 1) {
+          st_shared<T>((uint32_t)((m4 & 1u) ? sbuf + (int32_t)R + K1 : az) * (uint32_t)sizeof(T), x);
+        } else {
+          const uint32_t y = __byte_perm(x, 0u, e);
+          const int32_t nz = (int32_t)(e >> 16);
+          const int32_t a1 = sbuf + (int32_t)R + K1 - nz;  // the ones go to a1 + k for k >= nz
+          const uint32_t A0 = (uint32_t)az * (uint32_t)sizeof(T), A1 = (uint32_t)a1 * (uint32_t)sizeof(T);
+          st_shared<T, 0>(nz > 0 ? A0 : A1, y);
+          if (SPW > 1) st_shared<T, sizeof(T)>(nz > 1 ? A0 : A1, y >> (8 * sizeof(T)));
+          if (SPW > 2) {
+            st_shared<T, 2 * sizeof(T)>(nz > 2 ? A0 : A1, y >> 16);
+            st_shared<T, 3 * sizeof(T)>(nz > 3 ? A0 : A1, y >> 24);
+          }
         }
       };
-      const uint32_t sub = (tid % (uint32_t)XW) * SPW;  // word w = tid + 256 k: owner w / XW, offset (w % XW) * SPW
-      const uint32_t submask = lowmask(sub);
-      if (vF == vL && len == (uint32_t)TILE) {  // block-uniform: one segment, full tile
+      if (nseg == 1 && len == (uint32_t)TILE) {  // block-uniform: one segment, full tile
+        const int32_t K0F = S.K[0], K1F = S.K[1];
+        // all shared loads first (independent), then the stores
+        uint32_t xs[WPT], Rs[WPT], ms[WPT], es[WPT];
 #pragma unroll
         for (int k = 0; k < WPT; ++k) {
           const uint32_t w = tid + LV_THREADS * k;
-          const uint2 ow = S.own[w / XW];
-          const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
-          const uint32_t m4 = ow.x >> sub;
-          const uint32_t x = Win[w];
-          int32_t az = (int32_t)(w * SPW - R) + K0F, ao = (int32_t)R + K1F;
-#pragma unroll
-          for (int j = 0; j < SPW; ++j) {
-            const bool b = (m4 >> j) & 1u;
-            st_shared<T>((uint32_t)(b ? ao : az) * (uint32_t)sizeof(T), x >> (8 * sizeof(T) * j));
-            if (b) ++ao;
-            else ++az;
-          }
+          const uint2 ow = *reinterpret_cast<const uint2*>(&S.own[w / XW]);
+          xs[k] = Win[w];
+          Rs[k] = (ow.y & 0xffffu) + (uint32_t)__popc(ow.x & submask);
+          ms[k] = ow.x >> sub;
         }
-      } else {
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) es[k] = lut_of(ms[k]);
+#pragma unroll
+        for (int k = 0; k < WPT; ++k)
+          word_one_segment(xs[k], (tid + LV_THREADS * k) * SPW, Rs[k], ms[k], K0F, K1F, es[k]);
+      } else if (segtab) {  // segment table in shared memory
 #pragma unroll
         for (int k = 0; k < WPT; ++k) {
           const uint32_t w = tid + LV_THREADS * k;
           const uint32_t q0 = w * SPW;
           if (q0 >= len) break;
-          const uint2 ow = S.own[w / XW];
-          const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
-          const uint32_t m4 = (ow.x >> sub) & ((1u << SPW) - 1u);
+          const uint4 ow = S.own[w / XW];
+          const uint32_t R = (ow.y & 0xffffu) + (uint32_t)__popc(ow.x & submask);
+          uint32_t g = (ow.y >> 16) + (uint32_t)__popc(ow.z & subhead);  // segment of the word's first symbol
+          const uint32_t m4 = ow.x >> sub;
+          const uint32_t h4 = (ow.z >> sub) & ((1u << SPW) - 2u);         // heads inside the word
           const uint32_t x = Win[w];
           const uint32_t nv = min((uint32_t)SPW, len - q0);
-          const uint32_t v0 = sym_in_word<T>(x, 0) >> nsh;
-          const uint32_t vl = sym_in_word<T>(x, SPW - 1) >> nsh;
-          if (nv == (uint32_t)SPW && v0 == vl) {
-            int32_t K0, K1;
-            consts(v0, K0, K1);
-            int32_t az = (int32_t)(q0 - R) + K0, ao = (int32_t)R + K1;
+          if (nv == (uint32_t)SPW && h4 == 0) {
+            const short2 kk = S.kt[g];
+            word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4));
+          } else {
 #pragma unroll
             for (int j = 0; j < SPW; ++j) {
-              const bool b = (m4 >> j) & 1u;
-              st_shared<T>((uint32_t)(b ? ao : az) * (uint32_t)sizeof(T), x >> (8 * sizeof(T) * j));
-              if (b) ++ao;
-              else ++az;
+              if ((uint32_t)j < nv) {
+                g += (h4 >> j) & 1u;
+                const short2 kk = S.kt[g];
+                const uint32_t Rj = R + (uint32_t)__popc(m4 & lowmask(j));
+                const uint32_t b = (m4 >> j) & 1u;
+                st_shared<T>((uint32_t)(sbuf + (b ? (int32_t)Rj + kk.y : (int32_t)(q0 + j - Rj) + kk.x)) *
+                                 (uint32_t)sizeof(T),
+                             sym_in_word<T>(x, j));
+              }
             }
+          }
+        }
+      } else {  // too many segments for the table: node tables from global memory
+        const int32_t K0F = S.K[0], K1F = S.K[1], K0L = S.K[2], K1L = S.K[3];
+        auto consts = [&](uint32_t v, int32_t& K0, int32_t& K1) {
+          if (v == vF) {
+            K0 = K0F;
+            K1 = K1F;
+          } else if (v == vL) {
+            K0 = K0L;
+            K1 = K1L;
+          } else {  // interior node: stage position = HBM destination - T0 + MARGIN
+            const ulonglong2 t = __ldg(&tab[v]);
+            K0 = (int32_t)((long long)t.x - (long long)P) + MARGIN;
+            K1 = (int32_t)((long long)t.y + (long long)P - (long long)T0) + MARGIN;
+          }
+        };
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) {
+          const uint32_t w = tid + LV_THREADS * k;
+          const uint32_t q0 = w * SPW;
+          if (q0 >= len) break;
+          const uint4 ow = S.own[w / XW];
+          const uint32_t R = (ow.y & 0xffffu) + (uint32_t)__popc(ow.x & submask);
+          const uint32_t m4 = ow.x >> sub;
+          const uint32_t h4 = (ow.z >> sub) & ((1u << SPW) - 2u);
+          const uint32_t x = Win[w];
+          const uint32_t nv = min((uint32_t)SPW, len - q0);
+          if (nv == (uint32_t)SPW && h4 == 0) {
+            int32_t K0, K1;
+            consts(sym_in_word<T>(x, 0) >> nsh, K0, K1);
+            word_one_segment(x, q0, R, m4, K0, K1, lut_of(m4));
           } else {
 #pragma unroll
             for (int j = 0; j < SPW; ++j) {
@@ -505,7 +592,8 @@ __global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
                 consts(sym >> nsh, K0, K1);
                 const uint32_t Rj = R + (uint32_t)__popc(m4 & lowmask(j));
                 const uint32_t b = (m4 >> j) & 1u;
-                st_shared<T>((uint32_t)(b ? (int32_t)Rj + K1 : (int32_t)(q0 + j - Rj) + K0) * (uint32_t)sizeof(T),
+                st_shared<T>((uint32_t)(sbuf + (b ? (int32_t)Rj + K1 : (int32_t)(q0 + j - Rj) + K0)) *
+                                 (uint32_t)sizeof(T),
                              sym);
               }
             }
@@ -517,14 +605,11 @@ __global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
     __syncthreads();  // B4: stage partitioned (and the input buffer fully read)
 
     // ---------------- phase E: TMA bulk stores of the aligned bodies, element stores of the edges
-    if (tid == 0) {
-#pragma unroll
-      for (int r = 0; r < LV_NREG; ++r) {
-        const int32_t b = S.rbase[r], l = S.rlen[r];
-        const int32_t fs = (b + A - 1) / A * A, fe = (b + l) / A * A;
-        if (l > 0 && fe > fs)
-          bulk_s2g(out + (S.gofs[r] + fs), S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
-      }
+    if (tid < (uint32_t)LV_NREG) {  // lane r of warp 0: region r's 16-byte-aligned body
+      const int32_t b = S.rbase[tid], l = S.rlen[tid];
+      const int32_t fs = (b + A - 1) / A * A, fe = (b + l) / A * A;
+      if (l > 0 && fe > fs)
+        bulk_s2g(out + (S.gofs[tid] + fs), S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
       bulk_commit();
     }
     if (tid < (uint32_t)(2 * A * LV_NREG)) {
@@ -536,9 +621,10 @@ __global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
       if (l > 0 && ((e < A) ? (q < hend) : (q < end))) out[S.gofs[r] + q] = S.buf[ob][q];
     }
     // the previous tile's output buffer: once its bulk stores have read it, load a new tile into it
-    if (tid == 0) {
-      bulk_wait_read<1>();
-      if (it >= 1) issue(it + NB - 2);
+    if (warp == 0) {
+      if (lane < (uint32_t)LV_NREG) bulk_wait_read<1>();  // each lane's own bulk groups
+      __syncwarp();
+      if (lane == 0 && it >= 1) issue(it + NB - 2);
     }
   }
   if (SCATTER) {
@@ -547,7 +633,7 @@ __global__ void __launch_bounds__(LV_THREADS, LvTile<T>::MINB)
       const uint32_t v = S.cnt[tid];
       if (v) atomicAdd(&agg_next[S.dtile[tid]], v);
     }
-    if (tid == 0) bulk_wait<0>();
+    if (tid < (uint32_t)LV_NREG) bulk_wait<0>();
   }
 }
 
