@@ -61,7 +61,7 @@ def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
     if kind == "scan":        # read + write 2^L counters
         return 16 * (1 << L)
     if kind == "tile_scan":
-        tile = {1: 8192, 2: 8192, 4: 4096}[w]
+        tile = {1: 2048, 2: 1024, 4: 512}[w]
         return 12 * ((n + tile - 1) // tile)
     if kind == "tables":
         return 16 * max(0, (1 << max(L - 1, 0)) - 1)

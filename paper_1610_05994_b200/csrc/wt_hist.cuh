@@ -15,7 +15,7 @@
 
 namespace wt {
 
-constexpr int HIST_G = 4;  // level tiles per block iteration
+constexpr int HIST_G = 8;  // level tiles per block iteration
 
 template <typename T>
 __device__ __forceinline__ uint32_t msb_mask32(uint32_t bit) {

@@ -11,7 +11,7 @@ import wt_inputs
 
 pytestmark = pytest.mark.gpu
 
-TILE = {1: 8192, 2: 8192, 4: 4096}   # level-pass tile (positions) per symbol width
+TILE = {1: 2048, 2: 1024, 4: 512}   # level-pass tile (positions) per symbol width
 
 
 @pytest.fixture(scope="module")
