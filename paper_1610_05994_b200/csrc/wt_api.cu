@@ -203,7 +203,11 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   note(K_HIST);
   if (!dry) {
     if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-    if (L <= SMEM_HIST_MAX_L) {
+    if (L <= 2) {
+      const uint64_t nvec = n / (16 / sizeof(T));
+      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((nvec + 511) / 512, 4ull * num_sms()));
+      wt::k_hist_bits<T><<<grid, 512, 0, stream>>>(seq, n, sigma, L, C, L ? agg : nullptr, flag);
+    } else if (L <= SMEM_HIST_MAX_L) {
       const uint32_t nbins = 1u << L;
       uint32_t copies = (46u * 1024u) / (nbins * 4u);  // + static reduction scratch stays < 48 KiB
       copies = std::max(1u, std::min(copies, 16u));

@@ -88,6 +88,74 @@ __device__ __forceinline__ void hist_tiles(const T* __restrict__ S, uint64_t n, 
   }
 }
 
+// ---- tiny alphabets (L <= 2, sigma <= 4): no bins at all.  Per 32-bit word,
+// SWAR lane accumulators count symbols with bit 0 set, bit 1 set and both;
+// H[0..3] follow by inclusion-exclusion.  Symbols outside [0, 2^L) are
+// caught by a mask test, values in [sigma, 2^L) by their counts.
+template <typename T>
+__global__ void __launch_bounds__(512) k_hist_bits(const T* __restrict__ S, uint64_t n, uint64_t sigma, uint32_t L,
+                                                   unsigned long long* __restrict__ H, uint32_t* __restrict__ agg0,
+                                                   int32_t* __restrict__ flag) {
+  __shared__ uint32_t red[HIST_G];
+  __shared__ unsigned long long tot[4];
+  if (threadIdx.x < 4) tot[threadIdx.x] = 0;
+  constexpr uint32_t PER = 16 / sizeof(T);
+  const uint32_t lo = msb_mask32<T>(0);                                   // bit 0 of every symbol
+  const uint32_t badm = ~(lo * ((1u << L) - 1u));                         // bits no symbol < 2^L has
+  const uint32_t msk2 = L >= 2 ? lo : 0u;
+  unsigned long long c1 = 0, c2 = 0, c3 = 0, cnt = 0;
+  uint32_t badbits = 0;
+  auto lanesum = [](uint32_t a) -> uint32_t {  // sum of the per-symbol lanes of a
+    if (sizeof(T) == 1) return (a * 0x01010101u) >> 24;
+    if (sizeof(T) == 2) return (a * 0x00010001u) >> 16;
+    return a;
+  };
+  hist_tiles<T, 512>(S, n, L, agg0, red,
+                     [&](const uint4& v, bool valid) {
+                       if (!valid) return;
+                       const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                       uint32_t a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+                       for (int k = 0; k < 4; ++k) {
+                         badbits |= w[k] & badm;
+                         const uint32_t b = w[k] & lo, t = (w[k] >> 1) & msk2;
+                         a1 += b;
+                         a2 += t;
+                         a3 += b & t;
+                       }
+                       c1 += lanesum(a1);
+                       c2 += lanesum(a2);
+                       c3 += lanesum(a3);
+                       cnt += PER;
+                     },
+                     [&](uint32_t x) {
+                       badbits |= (x >> L);
+                       c1 += x & 1u;
+                       c2 += (x >> 1) & (L >= 2 ? 1u : 0u);
+                       c3 += x & (x >> 1) & (L >= 2 ? 1u : 0u);
+                       cnt += 1;
+                     });
+  // block totals of H[0..3]
+  unsigned long long h[4] = {cnt - c1 - c2 + c3, c1 - c3, c2 - c3, c3};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    unsigned long long x = h[k];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(&tot[k], x);
+  }
+  if (__syncthreads_or(badbits != 0)) {
+    if (threadIdx.x == 0) *flag = 2;  // WT_ERR_SYMBOL_RANGE
+  }
+  if (threadIdx.x < (1u << L)) {
+    const unsigned long long x = tot[threadIdx.x];
+    if (x) {
+      atomicAdd(&H[threadIdx.x], x);
+      if (threadIdx.x >= sigma) *flag = 2;
+    }
+  }
+}
+
 // ---- small alphabets: u32 shared bins, `copies` copies (warp w uses w % copies)
 template <typename T>
 __global__ void __launch_bounds__(512) k_hist_smem(const T* __restrict__ S, uint64_t n, uint64_t sigma, uint32_t L,
