@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwt.so")
+LIB_PATH = os.environ.get("WT_LIB") or os.path.join(_HERE, "libwt.so")  # WT_LIB: experiment builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -282,7 +282,11 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   }
   const uint32_t grid_sc = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_sc * (uint64_t)num_sms());
   const uint32_t grid_last = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_last * (uint64_t)num_sms());
+#ifdef WT_EXP_LEVELS  // experiment builds: only the first level passes (timing studies)
+  for (uint32_t l = 0; l < std::min<uint32_t>(L, WT_EXP_LEVELS); ++l) {
+#else
   for (uint32_t l = 0; l < L; ++l) {
+#endif
     const bool last = (l + 1 == L);
     // pre_l = exclusive scan of agg_l (ones of level l per tile)
     note(K_TSCAN);

@@ -59,8 +59,8 @@ struct LvTile {
   static constexpr int XW = 16;                  // 32-bit words per lane (phase A and phase D)
   static constexpr int MARGIN = 4 * A;           // side-region slack before/after the tile
   static constexpr int BUF = TILE + 2 * MARGIN;  // ring buffer (symbols)
-  static constexpr int NB = 3;                   // ring buffers per warp
-  static constexpr int MINB = 24;                // warps (CTAs) per SM the register budget is sized for
+  static constexpr int NB = 4;                   // ring buffers per warp
+  static constexpr int MINB = 20;                // warps (CTAs) per SM the register budget is sized for
   static constexpr int MAXSEG = 64;              // segment table capacity (else global node tables)
   static_assert(TILE % 512 == 0, "tiles hold whole superblocks");
   static_assert(NH == 1 || NH == 2, "mask halves");
@@ -75,6 +75,7 @@ struct LevelSmem {
   uint16_t seg_R[C::MAXSEG + 1];      // tile-local ones before seg_a[g]
   short2 kt[C::MAXSEG];               // segment g: stage offsets {K0, K1} relative to the output buffer
   uint32_t lut[16];                   // in-word stable partition selectors (partition_lut_entry)
+  uint4 lutz[16];                     // lutz[bits].k = 1 if slot k of the partitioned word is a zero
   int32_t s1, am, Rs1, Ram;           // first-segment end, last-segment start, ranks there
   alignas(8) unsigned long long bar[C::NB];
 };
@@ -123,7 +124,11 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     fence_mbar_init();
     for (int b = 0; b < (SCATTER ? NB - 1 : NB); ++b) issue((uint32_t)b);
   }
-  if (SCATTER && lane < 16) S.lut[lane] = partition_lut_entry<T>(lane);
+  if (SCATTER && lane < 16) {
+    const uint32_t e = partition_lut_entry<T>(lane), nz = e >> 16;
+    S.lut[lane] = e;
+    S.lutz[lane] = make_uint4(nz > 0, nz > 1, nz > 2, nz > 3);
+  }
   __syncwarp();
 
   for (uint32_t it = 0;; ++it) {
@@ -261,12 +266,10 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const int32_t b3 = rup(MARGIN + am) + (int32_t)(Dmz & (A - 1));
     const int32_t b4 = rup(b3 + zm) + (int32_t)(Dmo & (A - 1));
     const int32_t K0F = b1, K1F = b2, K0L = b3 - am + Ram, K1L = b4 - Ram;
-    // region of this lane (lanes >= LV_NREG hold an empty region)
-    const int rr = (int)min(lane, (uint32_t)LV_NREG);
-    const int32_t rbase = rr == 0 ? MARGIN + s1 : rr == 1 ? b1 : rr == 2 ? b2 : rr == 3 ? b3 : b4;
-    const int32_t rlen = rr == 0 ? am - s1 : rr == 1 ? z0 : rr == 2 ? o0 : rr == 3 ? zm : rr == 4 ? om : 0;
-    const long long rD = rr == 0 ? (long long)T0 + s1 : rr == 1 ? D0z : rr == 2 ? D0o : rr == 3 ? Dmz : Dmo;
-    const long long rgofs = rD - rbase;  // HBM destination of stage position q: q + rgofs
+    // the five regions (warp-uniform): identity, first zeros, first ones, last zeros, last ones
+    const int32_t rb[LV_NREG] = {MARGIN + s1, b1, b2, b3, b4};
+    const int32_t rl[LV_NREG] = {am - s1, z0, o0, zm, om};
+    const long long rD[LV_NREG] = {(long long)T0 + s1, D0z, D0o, Dmz, Dmo};  // HBM destination of rb[r]
     // symbols of side region r with rank < ksplit_r land in destination tile
     // floor(D_r / TILE), the rest in the next tile
     auto ksplit = [&](long long D, int32_t l) {
@@ -284,6 +287,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
 
     // ---------------- next-level ones per (region, destination tile), lane-owned symbols
     uint32_t mycnt = 0;  // lane k < LV_NKEY: count of key k = 2 r + half
+#ifndef WT_EXP_SKIP_COUNT
     {
       // count of nbm bits among the set bits of M, split at rank k (the set
       // bits of M have ranks rank0, rank0+1, ... in position order)
@@ -308,18 +312,19 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           rank0 += nM;
         }
       };
-      auto put = [&](int key, uint32_t v) {
-        const uint32_t sum = __reduce_add_sync(FULL, v);
-        if (lane == (uint32_t)key) mycnt = sum;
+      auto put2 = [&](int key, uint32_t lo, uint32_t hi) {  // keys (key, key+1) in one reduction
+        const uint32_t sum = __reduce_add_sync(FULL, lo | (hi << 16));
+        if (lane == (uint32_t)key) mycnt = sum & 0xffffu;
+        if (lane == (uint32_t)key + 1) mycnt = sum >> 16;
       };
       uint32_t M[NH], lo, hi;
       if (one) {  // warp-uniform: one segment, only the first-segment runs
 #pragma unroll
         for (int h = 0; h < NH; ++h) M[h] = vm[h] & ~m[h];
         split(M, (int32_t)(i0 - mypre), ksplit(D0z, z0), lo, hi);
-        put(2, lo), put(3, hi);
+        put2(2, lo, hi);
         split(m, (int32_t)mypre, ksplit(D0o, o0), lo, hi);
-        put(4, lo), put(5, hi);
+        put2(4, lo, hi);
       } else {
         uint32_t fm[NH], lm[NH];
 #pragma unroll
@@ -330,30 +335,32 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         uint32_t c0 = 0;
 #pragma unroll
         for (int h = 0; h < NH; ++h) c0 += (uint32_t)__popc(nbm[h] & vm[h] & ~fm[h] & ~lm[h]);
-        put(0, c0);
+        put2(0, c0, 0u);
 #pragma unroll
         for (int h = 0; h < NH; ++h) M[h] = fm[h] & ~m[h];
         split(M, (int32_t)(i0 - mypre), ksplit(D0z, z0), lo, hi);
-        put(2, lo), put(3, hi);
+        put2(2, lo, hi);
 #pragma unroll
         for (int h = 0; h < NH; ++h) M[h] = fm[h] & m[h];
         split(M, (int32_t)mypre, ksplit(D0o, o0), lo, hi);
-        put(4, lo), put(5, hi);
+        put2(4, lo, hi);
         const int32_t qs = max((int32_t)i0, am);
         const int32_t Rq = ((int32_t)i0 < am) ? Ram : (int32_t)mypre;  // tile-local ones before qs
 #pragma unroll
         for (int h = 0; h < NH; ++h) M[h] = lm[h] & ~m[h];
         split(M, (qs - am) - (Rq - Ram), ksplit(Dmz, zm), lo, hi);
-        put(6, lo), put(7, hi);
+        put2(6, lo, hi);
 #pragma unroll
         for (int h = 0; h < NH; ++h) M[h] = lm[h] & m[h];
         split(M, Rq - Ram, ksplit(Dmo, om), lo, hi);
-        put(8, lo), put(9, hi);
+        put2(8, lo, hi);
       }
     }
+#endif
     if (segtab && !one) __syncwarp();  // kt[]
 
     // ---------------- phase D: every symbol from the input buffer to its stage position
+#ifndef WT_EXP_SKIP_D
     {
       const int32_t sbuf = (int32_t)(smem_u32(S.buf[ob]) / (uint32_t)sizeof(T));  // in symbols
       const uint32_t* Win = reinterpret_cast<const uint32_t*>(B);
@@ -364,40 +371,57 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       const uint32_t submask = lowmask(sub), subhead = lowmask(sub + 1);
       const uint4* own = S.own[NH == 1 ? 0 : hh];
       auto lut_of = [&](uint32_t m4) -> uint32_t { return SPW == 1 ? 0u : S.lut[m4 & ((1u << SPW) - 1u)]; };
+      auto lutz_of = [&](uint32_t m4) -> uint4 {
+        return SPW == 1 ? make_uint4(0, 0, 0, 0) : S.lutz[m4 & ((1u << SPW) - 1u)];
+      };
       // stores the SPW symbols of word x (tile position q0, R ones before it,
-      // bits m4, in-word partition e) into segment (K0, K1) (stage offsets)
+      // bits m4, in-word partition e / zero slots z) into segment (K0, K1)
+      // (stage offsets).  Slot k of the partitioned word y goes to
+      // Ao + k + z_k (Az - Ao): the slot choice is a multiply-add (FMA pipe)
+      // and the symbol extraction a multiply-high, keeping the ALU pipe free.
       auto word_one_segment = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, int32_t K0, int32_t K1,
-                                  uint32_t e) {
-        const int32_t az = sbuf + (int32_t)(q0 - R) + K0;
+                                  uint32_t e, uint4 z) {
         if constexpr (SPW == 1) {
+          const int32_t az = sbuf + (int32_t)(q0 - R) + K0;
           st_shared<T>((uint32_t)((m4 & 1u) ? sbuf + (int32_t)R + K1 : az) * (uint32_t)sizeof(T), x);
         } else {
           const uint32_t y = __byte_perm(x, 0u, e);
           const int32_t nz = (int32_t)(e >> 16);
-          const int32_t a1 = sbuf + (int32_t)R + K1 - nz;  // the ones go to a1 + k for k >= nz
-          const uint32_t A0 = (uint32_t)az * (uint32_t)sizeof(T), A1 = (uint32_t)a1 * (uint32_t)sizeof(T);
-          st_shared<T, 0>(nz > 0 ? A0 : A1, y);
-          st_shared<T, sizeof(T)>(nz > 1 ? A0 : A1, y >> (8 * sizeof(T)));
+          const uint32_t Az = (uint32_t)(sbuf + (int32_t)(q0 - R) + K0) * (uint32_t)sizeof(T);
+          const uint32_t Ao = (uint32_t)(sbuf + (int32_t)R + K1 - nz) * (uint32_t)sizeof(T);
+          const uint32_t d = Az - Ao;
+          st_shared<T, 0>(Ao + z.x * d, y);
+          st_shared<T, sizeof(T)>(Ao + z.y * d, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
           if constexpr (SPW > 2) {
-            st_shared<T, 2 * sizeof(T)>(nz > 2 ? A0 : A1, y >> 16);
-            st_shared<T, 3 * sizeof(T)>(nz > 3 ? A0 : A1, y >> 24);
+            st_shared<T, 2>(Ao + z.z * d, __umulhi(y, 1u << 16));
+            st_shared<T, 3>(Ao + z.w * d, __umulhi(y, 1u << 8));
           }
         }
       };
       if (one && len == (uint32_t)TILE) {  // warp-uniform: one segment, full tile
-        uint32_t xs[XW], Rs[XW], ms[XW], es[XW];
+        // batches of BK words: the batch's shared loads first (independent), then its stores
+        constexpr int BK = 4;
 #pragma unroll
-        for (int k = 0; k < XW; ++k) {
-          const uint32_t w = lane + 32 * k;
-          const uint2 ow = *reinterpret_cast<const uint2*>(&own[w / XW]);
-          xs[k] = Win[w];
-          Rs[k] = (ow.y & 0xffffu) + (uint32_t)__popc(ow.x & submask);
-          ms[k] = ow.x >> sub;
+        for (int k0 = 0; k0 < XW; k0 += BK) {
+          uint32_t xs[BK], Rs[BK], ms[BK], es[BK];
+          uint4 zs[BK];
+#pragma unroll
+          for (int k = 0; k < BK; ++k) {
+            const uint32_t w = lane + 32 * (k0 + k);
+            const uint2 ow = *reinterpret_cast<const uint2*>(&own[w / XW]);
+            xs[k] = Win[w];
+            Rs[k] = (ow.y & 0xffffu) + (uint32_t)__popc(ow.x & submask);
+            ms[k] = ow.x >> sub;
+          }
+#pragma unroll
+          for (int k = 0; k < BK; ++k) {
+            es[k] = lut_of(ms[k]);
+            zs[k] = lutz_of(ms[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < BK; ++k)
+            word_one_segment(xs[k], (lane + 32 * (k0 + k)) * SPW, Rs[k], ms[k], K0F, K1F, es[k], zs[k]);
         }
-#pragma unroll
-        for (int k = 0; k < XW; ++k) es[k] = lut_of(ms[k]);
-#pragma unroll
-        for (int k = 0; k < XW; ++k) word_one_segment(xs[k], (lane + 32 * k) * SPW, Rs[k], ms[k], K0F, K1F, es[k]);
       } else if (segtab) {  // segment table in shared memory
 #pragma unroll
         for (int k = 0; k < XW; ++k) {
@@ -413,7 +437,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           const uint32_t nv = min((uint32_t)SPW, len - q0);
           if (nv == (uint32_t)SPW && h4 == 0) {
             const short2 kk = S.kt[g];
-            word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4));
+            word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4), lutz_of(m4));
           } else {
 #pragma unroll
             for (int j = 0; j < SPW; ++j) {
@@ -457,7 +481,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           if (nv == (uint32_t)SPW && h4 == 0) {
             int32_t K0, K1;
             consts(sym_in_word<T>(x, 0) >> nsh, K0, K1);
-            word_one_segment(x, q0, R, m4, K0, K1, lut_of(m4));
+            word_one_segment(x, q0, R, m4, K0, K1, lut_of(m4), lutz_of(m4));
           } else {
 #pragma unroll
             for (int j = 0; j < SPW; ++j) {
@@ -476,42 +500,38 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         }
       }
     }
+#endif
     fence_proxy_async_smem();
     __syncwarp();  // stage partitioned (and the input buffer fully read)
 
     // ---------------- phase E: TMA bulk stores of the aligned bodies, element stores of the edges
-    const int32_t fs = (rbase + A - 1) / A * A, fe = (rbase + rlen) / A * A;
-    if (lane < (uint32_t)LV_NREG) {  // lane r: region r's 16-byte-aligned body
-      if (rlen > 0 && fe > fs)
-        bulk_s2g(out + (rgofs + fs), S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
-      bulk_commit();
-    }
-    {
-      // head edge [b, min(fs, end)) and tail edge [max(fe, that), end) of each
-      // region, each < A symbols: element stores
-      const int32_t end = rbase + rlen, hend = min(fs, end), tst = max(fe, hend);
 #pragma unroll
-      for (uint32_t base = 0; base < (uint32_t)(2 * A * LV_NREG); base += 32) {
-        const uint32_t idx = base + lane;
-        const int r = (int)min(idx / (2 * A), (uint32_t)LV_NREG), e = (int)(idx % (2 * A));
-        const int32_t b_ = __shfl_sync(FULL, rbase, r), end_ = __shfl_sync(FULL, end, r);
-        const int32_t hend_ = __shfl_sync(FULL, hend, r), tst_ = __shfl_sync(FULL, tst, r);
-        const long long go_ = __shfl_sync(FULL, rgofs, r);
-        const int32_t q = (e < A) ? b_ + e : tst_ + (e - A);
-        if (idx < (uint32_t)(2 * A * LV_NREG) && ((e < A) ? (q < hend_) : (q < end_))) out[go_ + q] = S.buf[ob][q];
-      }
+    for (int r = 0; r < LV_NREG; ++r) {
+      if (rl[r] <= 0) continue;  // warp-uniform
+      const int32_t b = rb[r], end = b + rl[r];
+      const int32_t fs = (b + A - 1) / A * A, fe = end / A * A;
+      const long long go = rD[r] - b;  // HBM destination of stage position q: q + go
+      if (lane == 0 && fe > fs)
+        bulk_s2g(out + (go + fs), S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
+      // head edge [b, min(fs, end)) and tail edge [max(fe, that), end), each < A symbols
+      const int32_t hend = min(fs, end), tst = max(fe, hend);
+      const int32_t q = (lane < (uint32_t)A) ? b + (int32_t)lane : tst + (int32_t)lane - A;
+      if (lane < (uint32_t)(2 * A) && ((lane < (uint32_t)A) ? (q < hend) : (q < end))) out[go + q] = S.buf[ob][q];
     }
-    {  // next-level ones per destination tile
-      const long long Dk = __shfl_sync(FULL, rD, (int)min(lane >> 1, (uint32_t)(LV_NREG - 1)));
-      if (lane < (uint32_t)LV_NKEY && mycnt)
-        atomicAdd(&agg_next[lane < 2 ? tile : (unsigned long long)Dk / TILE + (lane & 1)], mycnt);
+    if (lane == 0) bulk_commit();
+    if (lane < (uint32_t)LV_NKEY && mycnt) {  // next-level ones per destination tile
+      const int r = (int)(lane >> 1);
+      long long D = rD[0];
+#pragma unroll
+      for (int k = 1; k < LV_NREG; ++k) D = (r == k) ? rD[k] : D;
+      atomicAdd(&agg_next[r == 0 ? tile : (unsigned long long)D / TILE + (lane & 1)], mycnt);
     }
     // the previous tile's output buffer: once its bulk stores have read it, load a new tile into it
-    if (lane < (uint32_t)LV_NREG) bulk_wait_read<1>();  // each lane's own bulk groups
+    if (lane == 0) bulk_wait_read<1>();
     __syncwarp();
     if (lane == 0 && it >= 1) issue(it + NB - 2);
   }
-  if (SCATTER && lane < (uint32_t)LV_NREG) bulk_wait<0>();
+  if (SCATTER && lane == 0) bulk_wait<0>();
 }
 
 }  // namespace wt

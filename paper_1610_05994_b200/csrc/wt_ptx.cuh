@@ -69,13 +69,22 @@ __device__ __forceinline__ uint32_t swar_bits(const uint32_t (&xa)[XN], uint32_t
   static_assert(OFF + NW <= XN, "word range");
   const uint32_t* xw = xa + OFF;
   uint32_t m = 0;
-  if (sizeof(T) == 1) {
+  if constexpr (sizeof(T) == 1) {
     // gather bit sh of the 4 bytes of a word with one multiply:
     // (x & 0x01010101<<sh) * (1 + 2^7 + 2^14 + 2^21) puts byte j's bit at 21+sh+j
+    // gather bit sh of the 4 bytes of a word with one multiply: (x & 0x01010101<<sh)
+    // * ((1 + 2^7 + 2^14 + 2^21) << (7-sh)) puts byte j's bit at 28+j (no carries);
+    // a multiply-high moves the nibble to 4k.  2 ALU + 2 FMA-pipe ops per word.
+    static_assert(NW <= 8, "u8: at most 8 words per 32-bit mask");
     const uint32_t msk = 0x01010101u << sh;
+    const uint32_t magic = 0x00204081u << (7 - sh);
 #pragma unroll
-    for (int k = 0; k < NW; ++k) m |= ((((xw[k] & msk) * 0x00204081u) >> (21 + sh)) & 0xfu) << (4 * k);
-  } else if (sizeof(T) == 2) {
+    for (int k = 0; k < NW; ++k) {
+      const uint32_t p = (xw[k] & msk) * magic;
+      const uint32_t v = (k == 7) ? p : __umulhi(p, 1u << (4 + 4 * k));
+      m |= v & (0xfu << (4 * k));
+    }
+  } else if constexpr (sizeof(T) == 2) {
     const uint32_t msk = 0x00010001u << sh;
 #pragma unroll
     for (int k = 0; k < NW; ++k) {
