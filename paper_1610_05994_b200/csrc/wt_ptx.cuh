@@ -85,11 +85,16 @@ __device__ __forceinline__ uint32_t swar_bits(const uint32_t (&xa)[XN], uint32_t
       m |= v & (0xfu << (4 * k));
     }
   } else if constexpr (sizeof(T) == 2) {
+    // bits sh and 16+sh of the word -> bits 30, 31 by one multiply
+    // (x & msk) * (2^(30-sh) + 2^(15-sh)), then a multiply-high to 2k.
+    static_assert(NW <= 16, "u16: at most 16 words per 32-bit mask");
     const uint32_t msk = 0x00010001u << sh;
+    const uint32_t magic = (1u << (30 - sh)) | (1u << (15 - sh));
 #pragma unroll
     for (int k = 0; k < NW; ++k) {
-      const uint32_t t = xw[k] & msk;
-      m |= (((t >> sh) | (t >> (sh + 15))) & 3u) << (2 * k);
+      const uint32_t p = (xw[k] & msk) * magic;
+      const uint32_t v = (k == 15) ? p : __umulhi(p, 1u << (2 + 2 * k));
+      m |= v & (3u << (2 * k));
     }
   } else {
 #pragma unroll
