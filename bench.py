@@ -2,7 +2,7 @@
 """Benchmark: levelwise wavelet-tree build on B200 (BASELINE.json metric
 "wavelet tree build Gsymbols/s and achieved HBM GB/s vs roofline on 1 B200").
 
-A step = one whole build (histogram, scans, node tables, every level pass) of
+A step = one whole build (pass over S, scans, node tables, every level pass) of
 one config's sequence, through the C ABI (wt_build_async), inputs resident in
 HBM.  Default workload = BASELINE configs[1] (cfg2, DNA-like, n=2^30 uint8,
 sigma=4).  Prints ONE JSON line on rank 0.
@@ -56,15 +56,17 @@ def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
         return 2 * n * w + bitmap + 8 * nsb
     if kind == "last_level":  # read T_{L-1}, bitmap words, superblocks
         return n * w + bitmap + 8 * nsb
-    if kind == "hist":        # read S once (+ the 2^L counters)
-        return n * w + 8 * (1 << L)
-    if kind == "scan":        # read + write 2^L counters
-        return 16 * (1 << L)
+    if kind == "prologue":    # read S once (range check, level-0 tile ones)
+        return n * w
+    if kind == "scan":        # node_offsets: read 2^L uint32 leaf counts, write 2^L + 1 uint64
+        return 4 * (1 << L) + 8 * ((1 << L) + 1)
     if kind == "tile_scan":
         tile = {1: 2048, 2: 1024, 4: 512}[w]
         return 12 * ((n + tile - 1) // tile)
-    if kind == "tables":
-        return 16 * max(0, (1 << max(L - 1, 0)) - 1)
+    if kind == "tables":      # level l: read 2^(l+1) uint32 counts, write 2^l {ob, Zn}; average per launch
+        return sum(4 * (2 << l) + 16 * (1 << l) for l in range(max(L - 1, 0))) // max(L - 1, 1)
+    if kind == "memset":      # zero 2^(l+2) uint32 counts before pass l; average per launch
+        return sum(4 * (4 << l) for l in range(max(L - 1, 0))) // max(L - 1, 1)
     return 0
 
 

@@ -90,16 +90,20 @@ typedef struct {
  * wt_sizes: sizes of every output and of the workspace for a build of n
  * symbols of `width` bytes over [0, sigma).  Pure host arithmetic.
  * Errors: WT_ERR_ARG if width not in {1,2,4}, sigma == 0,
- * sigma > 2^(8*width), L > 30, or out == NULL.
+ * sigma > 2^(8*width), L > 30, n >= 2^32 (node counts are 32-bit), or
+ * out == NULL.
  */
 wt_status wt_sizes(uint64_t n, uint64_t sigma, uint32_t width, wt_sizes_t* out);
 
 /*
  * wt_build_async: enqueue the whole construction on `stream`:
- *   a1 histogram + symbol-range check, a2 exclusive scan -> node_offsets and
- *   the per-level node tables, a3 one stable bit-partition pass per level
- *   l < L-1 (bitmap words, superblocks, T_{l+1}), a4 the last level
- *   (bitmap + superblocks).  No host synchronisation; CUDA-graph capturable.
+ *   a1 one pass over S (symbol-range check, level-0 tile ones), a3 one
+ *   stable bit-partition pass per level l < L-1 (bitmap words, superblocks,
+ *   T_{l+1}, and -- progressive counting -- the sizes of the level-(l+2)
+ *   nodes), each preceded by a2 scans building that level's node tables;
+ *   the last scatter pass counts the leaves, whose exclusive scan is
+ *   node_offsets; a4 the last level (bitmap + superblocks).  No host
+ *   synchronisation; CUDA-graph capturable.
  * d_seq       n symbols, little-endian, `width` bytes each; 16-byte aligned
  *             (any torch/cudaMalloc allocation is).  Read only.
  * out         device pointers sized per wt_sizes (bitmaps, superblocks,
@@ -164,9 +168,15 @@ wt_status wt_select(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uin
                     wt_stream_t stream);
 
 /* Kernel launches one wt_build_async(n, sigma, width) enqueues, and their kinds
- * (kinds may be NULL): 1 histogram, 2 scan, 3 node tables, 4 level pass with
- * scatter (a3), 5 last level (a4), 6 memset. */
+ * (kinds may be NULL): 1 pass over S (prologue), 2 scan of node_offsets,
+ * 3 node-table scan, 4 level pass with scatter (a3), 5 last level (a4),
+ * 6 tile-prefix scan, 7 memset of a node-count buffer. */
 uint32_t wt_launch_plan(uint64_t n, uint64_t sigma, uint32_t width, uint32_t* kinds, uint32_t cap);
+
+/* Debug aid: byte offsets inside the workspace of wt_build_async(n, sigma,
+ * width): {flag, ones0, agg, pre, node tables, node counts, node-count buffer
+ * stride, T_odd, T_even, tiles per level}.  Returns the number of entries. */
+uint32_t wt_debug_offsets(uint64_t n, uint64_t sigma, uint32_t width, uint64_t* offsets, uint32_t cap);
 
 /* Profiling hook (thread-local): when events != NULL, the next wt_build_async
  * calls on this thread record events[2k] before and events[2k+1] after launch

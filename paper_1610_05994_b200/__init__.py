@@ -30,7 +30,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 WT_OK, WT_ERR_ARG, WT_ERR_SYMBOL_RANGE, WT_ERR_INDEX, WT_ERR_CUDA, WT_ERR_WORKSPACE = range(6)
-KIND_NAMES = {1: "hist", 2: "scan", 3: "tables", 4: "level", 5: "last_level", 6: "tile_scan"}
+KIND_NAMES = {1: "prologue", 2: "scan", 3: "tables", 4: "level", 5: "last_level", 6: "tile_scan", 7: "memset"}
 
 
 class WtSizes(ctypes.Structure):
@@ -63,6 +63,8 @@ _lib.wt_rank.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _u64, _vp
 _lib.wt_select.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
 _lib.wt_launch_plan.argtypes = [_u64, _u64, _u32, _vp, _u32]
 _lib.wt_launch_plan.restype = _u32
+_lib.wt_debug_offsets.argtypes = [_u64, _u64, _u32, _vp, _u32]
+_lib.wt_debug_offsets.restype = _u32
 _lib.wt_set_profile_events.argtypes = [_vp, _u32]
 _lib.wt_set_profile_events.restype = None
 _lib.wt_status_string.argtypes = [ctypes.c_int]
@@ -74,7 +76,8 @@ for _f in (_lib.wt_sizes, _lib.wt_build_async, _lib.wt_build, _lib.wt_build_from
     _f.restype = ctypes.c_int
 
 EXPORTS = ["wt_sizes", "wt_build_async", "wt_build", "wt_build_from_host", "wt_access", "wt_rank",
-           "wt_select", "wt_launch_plan", "wt_set_profile_events", "wt_status_string", "wt_last_error"]
+           "wt_select", "wt_launch_plan", "wt_debug_offsets", "wt_set_profile_events", "wt_status_string",
+           "wt_last_error"]
 
 
 class WtError(RuntimeError):
@@ -114,6 +117,14 @@ def launch_plan(n: int, sigma: int, width: int) -> list[str]:
     buf = (ctypes.c_uint32 * max(cnt, 1))()
     _lib.wt_launch_plan(n, sigma, width, ctypes.cast(buf, _vp), cnt)
     return [KIND_NAMES.get(buf[i], str(buf[i])) for i in range(cnt)]
+
+
+def debug_offsets(n: int, sigma: int, width: int) -> dict:
+    """Workspace layout of a build (debug aid)."""
+    buf = (ctypes.c_uint64 * 16)()
+    k = _lib.wt_debug_offsets(n, sigma, width, ctypes.cast(buf, _vp), 16)
+    names = ["flag", "ones0", "agg", "pre", "tab", "cnt", "cnt_stride", "bufA", "bufB", "ntiles"]
+    return dict(zip(names, [int(buf[i]) for i in range(k)]))
 
 
 def set_profile_events(events: list | None):

@@ -2,6 +2,7 @@
 // the launch sequence of the levelwise build.  The C ABI is declared (and
 // documented, with the paper citations) in include/wt.h.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -19,7 +20,7 @@ wt_status fail(wt_status st, const char* what) {
   return st;
 }
 wt_status fail_cuda(cudaError_t e, const char* what) {
-  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  g_last_error = (g_last_error.empty() ? std::string() : g_last_error + ": ") + what + ": " + cudaGetErrorString(e);
   return WT_ERR_CUDA;
 }
 
@@ -69,20 +70,24 @@ cudaError_t level_kernel_setup(int* blocks_per_sm) {
   return once;
 }
 
-constexpr uint32_t SMEM_HIST_MAX_L = 12;  // 4096 bins * 4 B fit several copies in 48 KiB
-constexpr int MAX_LOOKBACK_LAUNCHES = 64;
+
+constexpr int MAX_LOOKBACK_LAUNCHES = 128;
 
 // Workspace carve (all offsets 256-byte aligned).  The control block
 // [0, ctrl_bytes) is zeroed once per build: range flag, tile counters (one per
-// look-back scan launch), level bases, look-back status words (shared by every
+// look-back scan launch), ones0, look-back status words (shared by every
 // look-back scan of the build, told apart by epoch) and the per-level,
-// per-tile ones counts agg[l][t] (filled by the pass that writes T_l).
+// per-tile ones counts agg[l][t] (filled by the pass that writes T_l).  Then:
+// the tile prefixes pre[t], the node tables {ob, Zn} of levels 0..L-2, the
+// two ping-pong level-node count buffers cnt[2][2^L] (uint32: pass l counts
+// the level-(l+2) node sizes into cnt[l % 2]) and the ping-pong sequences
+// T_1, T_2, ...
 struct Carve {
   uint32_t L = 0;
   uint64_t words = 0, nsb = 0, c_len = 0, ntiles = 0;
-  uint64_t status_entries = 0, tab_entries = 0;
-  size_t off_flag = 0, off_counters = 0, off_lvlbase = 0, off_status = 0, off_agg = 0, ctrl_bytes = 0;
-  size_t off_pre = 0, off_tab = 0, off_bufA = 0, off_bufB = 0, total = 0;
+  uint64_t status_entries = 0, tab_entries = 0, cnt_entries = 0;
+  size_t off_flag = 0, off_counters = 0, off_ones0 = 0, off_status = 0, off_value = 0, off_agg = 0, ctrl_bytes = 0;
+  size_t off_pre = 0, off_tab = 0, off_cnt = 0, off_bufA = 0, off_bufB = 0, total = 0;
   // host-API extras (after total)
   size_t off_seq = 0, off_bits = 0, off_sb = 0, off_c = 0, host_total = 0;
 };
@@ -96,25 +101,29 @@ Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
   c.ntiles = (n + level_tile(width) - 1) / level_tile(width);
   const uint64_t scan_tiles = ((1ull << c.L) + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
   c.tab_entries = c.L >= 2 ? (1ull << (c.L - 1)) - 1 : 0;
-  const uint64_t tab_tiles = (c.tab_entries + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
+  c.cnt_entries = c.L >= 2 ? (1ull << c.L) : 0;
   const uint64_t pre_tiles = (c.ntiles + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
-  c.status_entries = std::max<uint64_t>(1, std::max(pre_tiles, std::max(scan_tiles, tab_tiles)));
+  c.status_entries = std::max<uint64_t>(1, std::max(pre_tiles, scan_tiles));
   size_t o = 0;
   c.off_flag = o;
   o += ALIGN;
   c.off_counters = o;
   o += align_up(MAX_LOOKBACK_LAUNCHES * sizeof(uint32_t));
-  c.off_lvlbase = o;
-  o += align_up(64 * sizeof(uint64_t));
+  c.off_ones0 = o;
+  o += ALIGN;
   c.off_status = o;
-  o += align_up(c.status_entries * sizeof(uint64_t));
+  o += align_up(c.status_entries * sizeof(uint32_t));
   c.off_agg = o;
   o += align_up((size_t)c.L * c.ntiles * sizeof(uint32_t));
   c.ctrl_bytes = o;
+  c.off_value = o;  // look-back values: written before their status, never read stale
+  o += align_up(2 * c.status_entries * sizeof(uint64_t));
   c.off_pre = o;
   o += align_up(c.ntiles * sizeof(uint64_t));
   c.off_tab = o;
   o += align_up(c.tab_entries * sizeof(ulonglong2));
+  c.off_cnt = o;
+  o += 2 * align_up(c.cnt_entries * sizeof(uint32_t));
   const size_t seq_bytes = align_up(n * width);
   c.off_bufA = o;
   if (c.L >= 2) o += seq_bytes;  // T_1, T_3, ...
@@ -139,7 +148,7 @@ wt_status check_args(uint64_t n, uint64_t sigma, uint32_t width) {
   if (sigma == 0) return fail(WT_ERR_ARG, "sigma must be >= 1");
   if (sigma > (1ull << (8 * width))) return fail(WT_ERR_ARG, "sigma exceeds the symbol width");
   if (levels_of(sigma) > 30) return fail(WT_ERR_ARG, "more than 30 levels");
-  if (n > (1ull << 50)) return fail(WT_ERR_ARG, "n too large");
+  if (n >= (1ull << 32)) return fail(WT_ERR_ARG, "n must be < 2^32 (32-bit node counts)");
   return WT_OK;
 }
 
@@ -155,12 +164,23 @@ struct Launcher {
   cudaError_t post() {
     cudaError_t e = cudaSuccess;
     if (g_events && 2 * k + 1 < g_event_count) e = cudaEventRecord((cudaEvent_t)g_events[2 * k + 1], s);
+    if (e == cudaSuccess && debug_sync()) {  // WT_DEBUG_SYNC=1: locate a faulting launch
+      e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) g_last_error = "launch " + std::to_string(k) + " faulted";
+    }
     ++k;
     return e;
   }
+  static bool debug_sync() {
+    static const bool on = [] {
+      const char* v = std::getenv("WT_DEBUG_SYNC");
+      return v && *v && *v != '0';
+    }();
+    return on;
+  }
 };
 
-enum Kind : uint32_t { K_HIST = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6 };
+enum Kind : uint32_t { K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7 };
 
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
 template <typename T>
@@ -174,11 +194,14 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   };
   int32_t* flag = reinterpret_cast<int32_t*>(ws + c.off_flag);
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + c.off_counters);
-  unsigned long long* lvlbase = reinterpret_cast<unsigned long long*>(ws + c.off_lvlbase);
-  uint64_t* status = reinterpret_cast<uint64_t*>(ws + c.off_status);
+  unsigned long long* ones0 = reinterpret_cast<unsigned long long*>(ws + c.off_ones0);
+  const wt::LookbackState status{reinterpret_cast<uint32_t*>(ws + c.off_status),
+                                 reinterpret_cast<uint64_t*>(ws + c.off_value), c.status_entries};
   ulonglong2* tab = reinterpret_cast<ulonglong2*>(ws + c.off_tab);
   uint32_t* agg = reinterpret_cast<uint32_t*>(ws + c.off_agg);
   unsigned long long* pre = reinterpret_cast<unsigned long long*>(ws + c.off_pre);
+  uint32_t* cnt[2] = {reinterpret_cast<uint32_t*>(ws + c.off_cnt),
+                      reinterpret_cast<uint32_t*>(ws + c.off_cnt + align_up(c.cnt_entries * sizeof(uint32_t)))};
   T* buf[2] = {reinterpret_cast<T*>(ws + c.off_bufA), reinterpret_cast<T*>(ws + c.off_bufB)};
   unsigned long long* C = dry ? nullptr : reinterpret_cast<unsigned long long*>(out->node_offsets);
   const uint32_t L = c.L;
@@ -187,8 +210,8 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
 
   if (!dry) {
     if ((e = cudaMemsetAsync(ws, 0, c.ctrl_bytes, stream)) != cudaSuccess) return fail_cuda(e, "memset ctrl");
-    if ((e = cudaMemsetAsync(C, 0, c.c_len * 8, stream)) != cudaSuccess) return fail_cuda(e, "memset C");
     if (n == 0) {
+      if ((e = cudaMemsetAsync(C, 0, c.c_len * 8, stream)) != cudaSuccess) return fail_cuda(e, "memset C");
       if (L && (e = cudaMemsetAsync(out->superblocks, 0, (size_t)L * c.nsb * 8, stream)) != cudaSuccess)
         return fail_cuda(e, "memset sb");
       if (count) *count = 0;
@@ -198,77 +221,42 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     if (count) *count = 0;
     return WT_OK;
   }
-
-  // a1: histogram + range check
-  note(K_HIST);
-  if (!dry) {
-    if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-    if (L <= 2) {
-      const uint64_t nvec = n / (16 / sizeof(T));
-      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((nvec + 511) / 512, 4ull * num_sms()));
-      wt::k_hist_bits<T><<<grid, 512, 0, stream>>>(seq, n, sigma, L, C, L ? agg : nullptr, flag);
-    } else if (L <= SMEM_HIST_MAX_L) {
-      const uint32_t nbins = 1u << L;
-      uint32_t copies = (46u * 1024u) / (nbins * 4u);  // + static reduction scratch stays < 48 KiB
-      copies = std::max(1u, std::min(copies, 16u));
-      const uint64_t nvec = n / (16 / sizeof(T));
-      const uint64_t want = (nvec + 511) / 512;
-      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 4ull * num_sms()));
-      wt::k_hist_smem<T><<<grid, 512, copies * nbins * 4, stream>>>(seq, n, sigma, L, copies, C, L ? agg : nullptr,
-                                                                    flag);
-    } else if (L <= 16) {
-      static cudaError_t attr = cudaFuncSetAttribute(wt::k_hist_smem16<T>,
-                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
-      if (attr != cudaSuccess) return fail_cuda(attr, "k_hist_smem16 smem attribute");
-      const uint32_t nbins = 1u << L;
-      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n + 65535) / 65536, num_sms()));
-      wt::k_hist_smem16<T><<<grid, 1024, nbins * 2, stream>>>(seq, n, sigma, L, C, agg, flag);
-    } else {
-      const uint64_t nvec = n / (16 / sizeof(T));
-      const uint64_t want = (nvec + 255) / 256;
-      const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 8ull * num_sms()));
-      wt::k_hist_global<T><<<grid, 512, 0, stream>>>(seq, n, sigma, L, C, agg, flag);
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_hist");
-    if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-  }
-
-  // a2: C = exclusive_scan(H) in place
   uint32_t epoch = 1, counter = 0;
-  note(K_SCAN);
-  if (!dry) {
-    if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-    const uint64_t cnt = 1ull << L;
-    wt::OpNodeOffsets op{C, cnt};
-    const uint32_t grid = (uint32_t)((cnt + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
-    wt::k_scan<wt::OpNodeOffsets><<<grid, wt::SCAN_THREADS, 0, stream>>>(op, cnt, status, counters + counter,
-                                                                         epoch, flag);
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(C)");
-    if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-  }
-  ++epoch;
-  ++counter;
-
-  // a2': node tables {ob, Zn} for levels 0..L-2
-  if (L >= 2) {
-    note(K_TABLES);
-    note(K_TABLES);
+  // one decoupled look-back scan launch
+  auto scan = [&](auto op, uint64_t cnt_, const char* what) -> wt_status {
     if (!dry) {
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      wt::OpTables op{C, tab, lvlbase, L};
-      const uint32_t grid = (uint32_t)((c.tab_entries + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
-      wt::k_scan<wt::OpTables><<<grid, wt::SCAN_THREADS, 0, stream>>>(op, c.tab_entries, status,
-                                                                      counters + counter, epoch, flag);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(tables)");
-      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      const uint32_t g2 = (uint32_t)std::min<uint64_t>((c.tab_entries + 255) / 256, 148 * 16);
-      wt::k_tables_fix<<<g2, 256, 0, stream>>>(C, tab, lvlbase, L, c.tab_entries, flag);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_tables_fix");
+      const uint32_t g = (uint32_t)((cnt_ + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+      wt::k_scan<decltype(op)><<<g, wt::SCAN_THREADS, 0, stream>>>(op, cnt_, status, counters + counter, epoch, flag);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, what);
       if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
     }
     ++epoch;
     ++counter;
+    return WT_OK;
+  };
+  wt_status st;
+
+  // a1: the pass over S: range check, level-0 tile ones agg0, ones0
+  note(K_PRO);
+  if (!dry) {
+    if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    const uint64_t tiles = (n + wt::LvTile<T>::TILE - 1) / wt::LvTile<T>::TILE;  // one warp per tile
+    const uint32_t grid = (uint32_t)std::max<uint64_t>(
+        1, std::min<uint64_t>((tiles + wt::PRO_THREADS / 32 - 1) / (wt::PRO_THREADS / 32), 8ull * num_sms()));
+    wt::k_prologue<T><<<grid, wt::PRO_THREADS, 0, stream>>>(seq, n, sigma, L, L ? agg : nullptr, ones0, flag);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_prologue");
+    if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+  }
+  if (L == 0) {  // sigma = 1: C = [0, n]
+    note(K_SCAN);
+    if ((st = scan(wt::OpLeafC{nullptr, C, 1, n, nullptr}, 1, "k_scan(C)")) != WT_OK) return st;
+  } else if (L == 1) {
+    note(K_SCAN);
+    if ((st = scan(wt::OpLeafC{nullptr, C, 2, n, ones0}, 2, "k_scan(C)")) != WT_OK) return st;
+  } else {
+    note(K_TABLES);
+    if ((st = scan(wt::OpLevelTab{nullptr, tab, n, ones0}, 1, "k_scan(level-0 table)")) != WT_OK) return st;
   }
 
   // a3 / a4: one pass per level
@@ -283,24 +271,30 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   const uint32_t grid_sc = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_sc * (uint64_t)num_sms());
   const uint32_t grid_last = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_last * (uint64_t)num_sms());
 #ifdef WT_EXP_LEVELS  // experiment builds: only the first level passes (timing studies)
-  for (uint32_t l = 0; l < std::min<uint32_t>(L, WT_EXP_LEVELS); ++l) {
+  const uint32_t Lrun = std::min<uint32_t>(L, WT_EXP_LEVELS);
 #else
-  for (uint32_t l = 0; l < L; ++l) {
+  const uint32_t Lrun = L;
 #endif
+  for (uint32_t l = 0; l < Lrun; ++l) {
     const bool last = (l + 1 == L);
+    if (!last && l >= 1) {  // node tables of level l from the level-(l+1) node sizes counted by pass l-1
+      note(K_TABLES);
+      wt::OpLevelTab op{dry ? nullptr : cnt[(l - 1) & 1], tab + ((1ull << l) - 1), n, nullptr};
+      if ((st = scan(op, 1ull << l, "k_scan(level table)")) != WT_OK) return st;
+    }
+    if (!last) {  // pass l counts the level-(l+2) node sizes into cnt[l % 2]
+      note(K_MEMSET);
+      if (!dry) {
+        if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+        if ((e = cudaMemsetAsync(cnt[l & 1], 0, (4ull << l) * sizeof(uint32_t), stream)) != cudaSuccess)
+          return fail_cuda(e, "memset counts");
+        if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      }
+    }
     // pre_l = exclusive scan of agg_l (ones of level l per tile)
     note(K_TSCAN);
-    if (!dry) {
-      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      wt::OpTilePrefix op{agg + (uint64_t)l * c.ntiles, pre};
-      const uint32_t g = (uint32_t)((c.ntiles + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
-      wt::k_scan<wt::OpTilePrefix><<<g, wt::SCAN_THREADS, 0, stream>>>(op, c.ntiles, status, counters + counter,
-                                                                       epoch, flag);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(tile prefix)");
-      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-    }
-    ++epoch;
-    ++counter;
+    if ((st = scan(wt::OpTilePrefix{agg + (uint64_t)l * c.ntiles, pre}, c.ntiles, "k_scan(tile prefix)")) != WT_OK)
+      return st;
     note(last ? K_LAST : K_LEVEL);
     if (!dry) {
       const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
@@ -310,15 +304,22 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       uint32_t* bits = out->bitmaps + (uint64_t)l * c.words;
       unsigned long long* sb = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
       uint32_t* agg_next = last ? nullptr : agg + (uint64_t)(l + 1) * c.ntiles;
+      uint32_t* cn = last ? nullptr : cnt[l & 1];
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
       if (last)
-        wt::k_level<T, false><<<grid_last, wt::LV_THREADS, lsmem, stream>>>(in, o, n, sh, t, bits, c.words, sb, c.nsb,
-                                                                         pre, agg_next, flag);
+        wt::k_level<T, false><<<grid_last, wt::LV_THREADS, lsmem, stream>>>(in, o, n, sh, t, bits, c.words, sb,
+                                                                           c.nsb, pre, agg_next, cn, flag);
       else
         wt::k_level<T, true><<<grid_sc, wt::LV_THREADS, lsmem, stream>>>(in, o, n, sh, t, bits, c.words, sb, c.nsb,
-                                                                        pre, agg_next, flag);
+                                                                         pre, agg_next, cn, flag);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_level");
       if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    }
+    if (l + 2 == L) {  // pass L-2 counted the leaves: C = exclusive scan of the leaf counts
+      note(K_SCAN);
+      if ((st = scan(wt::OpLeafC{dry ? nullptr : cnt[l & 1], C, 1ull << L, n, nullptr}, 1ull << L, "k_scan(C)")) !=
+          WT_OK)
+        return st;
     }
   }
   if (count) *count = nk;
@@ -500,6 +501,16 @@ uint32_t wt_launch_plan(uint64_t n, uint64_t sigma, uint32_t width, uint32_t* ki
   uint32_t count = 0;
   dispatch(nullptr, n, sigma, width, nullptr, nullptr, c, nullptr, kinds, cap, &count);
   return count;
+}
+
+uint32_t wt_debug_offsets(uint64_t n, uint64_t sigma, uint32_t width, uint64_t* offsets, uint32_t cap) {
+  if (check_args(n, sigma, width) != WT_OK) return 0;
+  const Carve c = carve(n, sigma, width);
+  const uint64_t v[] = {c.off_flag, c.off_ones0, c.off_agg, c.off_pre, c.off_tab, c.off_cnt,
+                        align_up(c.cnt_entries * sizeof(uint32_t)), c.off_bufA, c.off_bufB, c.ntiles};
+  const uint32_t k = (uint32_t)(sizeof(v) / sizeof(v[0]));
+  for (uint32_t i = 0; i < k && i < cap; ++i) offsets[i] = v[i];
+  return k;
 }
 
 void wt_set_profile_events(wt_event_t* events, uint32_t count) {

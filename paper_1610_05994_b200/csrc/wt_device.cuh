@@ -9,15 +9,24 @@ namespace wt {
 constexpr uint32_t FULL = 0xffffffffu;
 
 // ---------------------------------------------------------------- look-back
-// Decoupled look-back (single-pass prefix scan across tiles).  One 64-bit
-// status word per tile: [63:62] flag, [61:54] epoch, [53:0] value.  The value
-// travels inside the same word as the flag, so relaxed single-copy-atomic
-// 64-bit loads/stores are sufficient (no separate payload to order).  The
-// epoch distinguishes the look-back launches of one build, so the status
-// array is zeroed once per build instead of once per launch.
-enum : uint64_t { ST_INVALID = 0, ST_AGG = 1, ST_PREFIX = 2 };
-constexpr uint64_t VALUE_MASK = (1ull << 54) - 1;
+// Decoupled look-back (single-pass prefix scan across tiles).  Per tile a
+// 32-bit status word ([31:30] flag, [7:0] epoch) and two 64-bit values (the
+// tile aggregate and the inclusive prefix, separate so that publishing the
+// prefix never changes a value a reader of the aggregate flag is about to
+// read): the value is stored first (relaxed), then the status with release
+// semantics; a reader acquires the status before reading the value.  The epoch tells the
+// look-back launches of one build apart, so the status array is zeroed once
+// per build instead of once per launch.  Values are full 64-bit.
+enum : uint32_t { ST_INVALID = 0, ST_AGG = 1, ST_PREFIX = 2 };
 
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -26,33 +35,41 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
 __device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ uint64_t pack_status(uint64_t flag, uint32_t epoch, uint64_t value) {
-  return (flag << 62) | ((uint64_t)(epoch & 0xff) << 54) | (value & VALUE_MASK);
+
+struct LookbackState {
+  uint32_t* status;  // [tiles]
+  uint64_t* value;   // [2][tiles]: aggregates, then inclusive prefixes
+  uint64_t tiles;
+};
+
+__device__ __forceinline__ void lb_publish(LookbackState lb, uint64_t tile, uint32_t flag, uint32_t epoch,
+                                           uint64_t v) {
+  st_relaxed_u64(&lb.value[(flag == ST_PREFIX ? lb.tiles : 0) + tile], v);
+  st_release_u32(&lb.status[tile], (flag << 30) | (epoch & 0xffu));
 }
 
 // Called by all 32 lanes of ONE warp.  Publishes `aggregate` for `tile`,
 // returns the exclusive prefix of all earlier tiles and publishes the
 // inclusive prefix.  Tile ids must be handed out in launch order by an atomic
 // counter (forward progress: every earlier tile is owned by a resident CTA).
-__device__ __forceinline__ uint64_t lookback(uint64_t* status, uint64_t tile, uint64_t aggregate,
-                                             uint32_t epoch) {
+__device__ __forceinline__ uint64_t lookback(LookbackState lb, uint64_t tile, uint64_t aggregate, uint32_t epoch) {
   const uint32_t lane = threadIdx.x & 31;
   if (tile == 0) {
-    if (lane == 0) st_relaxed_u64(&status[0], pack_status(ST_PREFIX, epoch, aggregate));
+    if (lane == 0) lb_publish(lb, 0, ST_PREFIX, epoch, aggregate);
     return 0;
   }
-  if (lane == 0) st_relaxed_u64(&status[tile], pack_status(ST_AGG, epoch, aggregate));
+  if (lane == 0) lb_publish(lb, tile, ST_AGG, epoch, aggregate);
   uint64_t exclusive = 0;
   int64_t base = (int64_t)tile - 1;
   while (true) {
     const int64_t idx = base - (int64_t)lane;
-    uint64_t flag, val;
+    uint32_t flag;
+    uint64_t val;
     while (true) {
       if (idx >= 0) {
-        const uint64_t w = ld_relaxed_u64(&status[idx]);
-        const uint32_t ep = (uint32_t)(w >> 54) & 0xffu;
-        flag = (ep == (epoch & 0xffu)) ? (w >> 62) : ST_INVALID;
-        val = w & VALUE_MASK;
+        const uint32_t w = ld_acquire_u32(&lb.status[idx]);
+        flag = ((w & 0xffu) == (epoch & 0xffu)) ? (w >> 30) : ST_INVALID;
+        val = (flag != ST_INVALID) ? ld_relaxed_u64(&lb.value[(flag == ST_PREFIX ? lb.tiles : 0) + idx]) : 0;
       } else {
         flag = ST_PREFIX;
         val = 0;
@@ -69,7 +86,7 @@ __device__ __forceinline__ uint64_t lookback(uint64_t* status, uint64_t tile, ui
     if (pm) break;
     base -= 32;
   }
-  if (lane == 0) st_relaxed_u64(&status[tile], pack_status(ST_PREFIX, epoch, exclusive + aggregate));
+  if (lane == 0) lb_publish(lb, tile, ST_PREFIX, epoch, exclusive + aggregate);
   return exclusive;
 }
 

@@ -31,7 +31,7 @@ constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 // Exclusive scan of uint64 values over [0, count) with a decoupled look-back.
 // Op supplies load(i) and store(i, exclusive, value).
 template <class Op>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan(Op op, uint64_t count, uint64_t* status,
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan(Op op, uint64_t count, LookbackState status,
                                                        uint32_t* tile_counter, uint32_t epoch,
                                                        const int32_t* __restrict__ flag) {
   __shared__ uint64_t s_warp[SCAN_THREADS / 32];
@@ -70,19 +70,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Op op, uint64_t count, ui
   }
 }
 
-// C = exclusive_scan(H), in place; C[count] = total.
-struct OpNodeOffsets {
-  unsigned long long* C;
-  uint64_t count;
-  __device__ uint64_t load(uint64_t i) const { return C[i]; }
-  __device__ void store(uint64_t i, uint64_t excl, uint64_t val) const {
-    C[i] = excl;
-    if (i + 1 == count) C[count] = excl + val;
-  }
-};
-
-// Per-level tile prefixes: pre[t] = sum_{t' < t} agg[t'] (ones of the level
-// before tile t), from the per-tile ones counted by the previous pass.
+// Per-tile prefixes: pre[t] = sum_{t' < t} agg[t'] (ones of the level before
+// tile t), from the per-tile ones counted by the previous pass.
 struct OpTilePrefix {
   const uint32_t* agg;
   unsigned long long* pre;
@@ -90,55 +79,55 @@ struct OpTilePrefix {
   __device__ void store(uint64_t i, uint64_t excl, uint64_t) const { pre[i] = excl; }
 };
 
-// Node tables.  Level l (0 <= l <= L-2), node v, s = L - l; entry k = 2^l - 1 + v.
-//   leftsize(v) = C[(2v+1) << (s-1)] - C[2v << (s-1)]   (left child size)
-//   Zn[v] = sum_{v' <= v} leftsize(v')  (zeros of level l before node v+1)
-//   ob[v] = C[v << s] - (Zn[v] - leftsize(v))  (ones of level l before node v)
-// The scan below runs over all levels concatenated and stores the global
-// inclusive value; k_tables_fix subtracts the level's base.
-__device__ __forceinline__ void level_of(uint64_t k, uint32_t& l, uint64_t& v) {
-  l = 63u - (uint32_t)__clzll((long long)(k + 1));
-  v = k + 1 - (1ull << l);
-}
-struct OpTables {
-  const unsigned long long* C;
-  ulonglong2* tab;
-  unsigned long long* lvlbase;  // lvlbase[l+1] = global inclusive at the end of level l
-  uint32_t L;
-  __device__ uint64_t load(uint64_t k) const {
-    uint32_t l;
-    uint64_t v;
-    level_of(k, l, v);
-    const uint32_t s = L - l;
-    return C[(2 * v + 1) << (s - 1)] - C[(2 * v) << (s - 1)];
+// Node tables of level l from the sizes of the level-(l+1) nodes
+// (cnt[u], u < 2^(l+1); counted by pass l-1, or by the prologue for l = 0:
+// cnt1 = ones0, cnt0 = n - ones0).  For level-l node v:
+//   left(v) = cnt[2v]                         (its left child)
+//   N(v)    = sum_{u < 2v} cnt[u]             (its first position)
+//   Zn[v]   = sum_{v' <= v} left(v')          (zeros of level l before node v+1)
+//   ob[v]   = N(v) - (Zn[v] - left(v))        (ones of level l before node v)
+// One scan over v of the packed pair (left | total << 32); n < 2^32.
+struct OpLevelTab {
+  const uint32_t* cnt;
+  ulonglong2* tab;  // the level's slice
+  uint64_t n;
+  const unsigned long long* ones0;  // non-null for level 0
+  __device__ uint64_t load(uint64_t v) const {
+    uint64_t l, r;
+    if (ones0) {
+      r = *ones0;
+      l = n - r;
+    } else {
+      l = cnt[2 * v];
+      r = cnt[2 * v + 1];
+    }
+    return l | ((l + r) << 32);
   }
-  __device__ void store(uint64_t k, uint64_t excl, uint64_t val) const {
-    uint32_t l;
-    uint64_t v;
-    level_of(k, l, v);
-    tab[k].y = excl + val;
-    if (v + 1 == (1ull << l)) lvlbase[l + 1] = excl + val;
+  __device__ void store(uint64_t v, uint64_t excl, uint64_t val) const {
+    const uint64_t left = val & 0xffffffffull;
+    const uint64_t zn = (excl & 0xffffffffull) + left, N = excl >> 32;
+    tab[v] = make_ulonglong2(N - (zn - left), zn);
   }
 };
 
-__global__ void __launch_bounds__(256) k_tables_fix(const unsigned long long* __restrict__ C,
-                                                    ulonglong2* __restrict__ tab,
-                                                    const unsigned long long* __restrict__ lvlbase,
-                                                    uint32_t L, uint64_t count,
-                                                    const int32_t* __restrict__ flag) {
-  if (*flag) return;
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t l;
-    uint64_t v;
-    level_of(k, l, v);
-    const uint32_t s = L - l;
-    const uint64_t left = C[(2 * v + 1) << (s - 1)] - C[(2 * v) << (s - 1)];
-    const uint64_t zn = tab[k].y - (l ? lvlbase[l] : 0ull);
-    const uint64_t ob = C[v << s] - (zn - left);
-    tab[k] = make_ulonglong2(ob, zn);
+// Leaf node offsets C[c] = sum_{c' < c} H[c'] (the output), C[2^L] = n, from
+// the leaf counts H = sizes of the level-L nodes (counted by pass L-2, or by
+// the prologue when L = 1).
+struct OpLeafC {
+  const uint32_t* cnt;
+  unsigned long long* C;
+  uint64_t count, n;
+  const unsigned long long* ones0;  // non-null when L = 1 (cnt and ones0 null when L = 0)
+  __device__ uint64_t load(uint64_t i) const {
+    if (ones0) return i ? *ones0 : n - *ones0;  // L = 1
+    if (!cnt) return n;                         // L = 0: one leaf
+    return cnt[i];
   }
-}
+  __device__ void store(uint64_t i, uint64_t excl, uint64_t val) const {
+    C[i] = excl;
+    if (i + 1 == count) C[count] = excl + val;
+  }
+};
 
 }  // namespace wt
 

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     k_level(const T* __restrict__ in, T* __restrict__ out, uint64_t n, uint32_t sh,
             const ulonglong2* __restrict__ tab, uint32_t* __restrict__ bits, uint64_t words_per_level,
             unsigned long long* __restrict__ sb, uint64_t nsb, const unsigned long long* __restrict__ pre,
-            uint32_t* __restrict__ agg_next, const int32_t* __restrict__ flag) {
+            uint32_t* __restrict__ agg_next, uint32_t* __restrict__ cnt_next, const int32_t* __restrict__ flag) {
   using Cfg = LvTile<T>;
   constexpr int TILE = Cfg::TILE, A = Cfg::A, E = Cfg::E, SPW = Cfg::SPW, XW = Cfg::XW, NH = Cfg::NH;
   constexpr int MARGIN = Cfg::MARGIN, NB = Cfg::NB;
@@ -130,6 +130,17 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     S.lutz[lane] = make_uint4(nz > 0, nz > 1, nz > 2, nz > 3);
   }
   __syncwarp();
+
+  // sizes of the level-(l+2) nodes below the node this warp's tiles were in
+  // (lane k < 4: node 4 v + k), flushed when the node changes
+  uint32_t cc_node = 0xffffffffu, cc_acc = 0;
+  auto cc_flush = [&]() {  // lanes 0 and 2 add (k, k+1) pairs with one 64-bit atomic
+    const uint32_t hi = __shfl_down_sync(FULL, cc_acc, 1);
+    const unsigned long long pair = (unsigned long long)cc_acc | ((unsigned long long)hi << 32);
+    if ((lane == 0 || lane == 2) && pair)
+      atomicAdd(reinterpret_cast<unsigned long long*>(cnt_next + 4ull * cc_node + lane), pair);
+    cc_acc = 0;
+  };
 
   for (uint32_t it = 0;; ++it) {
     const uint64_t tile = tile_of(it);
@@ -357,6 +368,42 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       }
     }
 #endif
+    // ---------------- progressive counting: level-(l+2) node sizes, i.e. the
+    // symbols of each level-l node by their (level-l, level-(l+1)) bit pair
+#ifndef WT_EXP_SKIP_PCOUNT
+    if (one) {  // warp-uniform: all symbols in node vF.  The (b, nb) pair counts
+      // follow from the next-level ones already reduced above (keys 2..5: nb
+      // ones among the zeros / the ones, split by destination tile)
+      const uint32_t c01 = __shfl_sync(FULL, mycnt, 2) + __shfl_sync(FULL, mycnt, 3);
+      const uint32_t c11 = __shfl_sync(FULL, mycnt, 4) + __shfl_sync(FULL, mycnt, 5);
+      if (vF != cc_node) {
+        cc_flush();
+        cc_node = vF;
+      }
+      cc_acc += lane == 0 ? (len - tot) - c01 : lane == 1 ? c01 : lane == 2 ? tot - c11 : c11;
+    } else if (nvalid) {  // the lane's pieces: maximal runs of its symbols inside one node
+      uint64_t M = m[0], NB = nbm[0], V = vm[0], H = hm[0];
+      if constexpr (NH == 2) {
+        M |= (uint64_t)m[1] << 32, NB |= (uint64_t)nbm[1] << 32;
+        V |= (uint64_t)vm[1] << 32, H |= (uint64_t)hm[1] << 32;
+      }
+      uint64_t starts = (H | 1ull) & V;
+      while (starts) {
+        const int p = __ffsll((long long)starts) - 1;
+        starts &= starts - 1;
+        const int pend = starts ? __ffsll((long long)starts) - 1 : 64;
+        const uint64_t pm = V & ((pend >= 64 ? ~0ull : ((1ull << pend) - 1)) & ~((1ull << p) - 1));
+        const uint64_t z = pm & ~M, o = pm & M;
+        const uint64_t c01 = (uint64_t)__popcll(z & ~NB) | ((uint64_t)__popcll(z & NB) << 32);
+        const uint64_t c23 = (uint64_t)__popcll(o & ~NB) | ((uint64_t)__popcll(o & NB) << 32);
+        // two node counts per 64-bit atomic (each stays < 2^32: no carry)
+        unsigned long long* dst =
+            reinterpret_cast<unsigned long long*>(cnt_next + 4ull * ((uint32_t)B[i0 + p] >> nsh));
+        if (c01) atomicAdd(dst, (unsigned long long)c01);
+        if (c23) atomicAdd(dst + 1, (unsigned long long)c23);
+      }
+    }
+#endif
     if (segtab && !one) __syncwarp();  // kt[]
 
     // ---------------- phase D: every symbol from the input buffer to its stage position
@@ -531,7 +578,10 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     __syncwarp();
     if (lane == 0 && it >= 1) issue(it + NB - 2);
   }
-  if (SCATTER && lane == 0) bulk_wait<0>();
+  if (SCATTER) {
+    cc_flush();
+    if (lane == 0) bulk_wait<0>();
+  }
 }
 
 }  // namespace wt

@@ -48,8 +48,9 @@ def test_sizes(wt):
     s = wt.sizes(1 << 28, 1 << 24, 4)
     assert s.levels == 24 and s.words_per_level == (1 << 28) // 32 and s.sb_per_level == (1 << 19) + 1
     assert s.bitmap_bytes == 24 * (1 << 23) * 4 and s.superblock_bytes == 24 * ((1 << 19) + 1) * 8
-    # two ping-pong permuted copies of the sequence at most
-    assert 2 * (1 << 30) <= s.workspace_bytes < 2 * (1 << 30) + 300 * (1 << 20)
+    # two ping-pong permuted copies of the sequence at most, plus node tables,
+    # two 2^L uint32 node-count buffers and per-tile counts
+    assert 2 * (1 << 30) <= s.workspace_bytes < 2 * (1 << 30) + 450 * (1 << 20)
     assert s.host_workspace_bytes > s.workspace_bytes + (1 << 30)
     assert wt.sizes(5, 1, 1).levels == 0
     assert wt.sizes(5, 2, 1).workspace_bytes < 1 << 20   # L=1: no permuted copy
@@ -58,7 +59,7 @@ def test_sizes(wt):
 
 
 @pytest.mark.parametrize("n,sigma,width", [(10, 4, 3), (10, 0, 1), (10, 257, 1), (10, 1 << 17, 2),
-                                           (10, (1 << 31), 4)])
+                                           (10, (1 << 31), 4), (1 << 32, 256, 1)])
 def test_sizes_rejects_bad_args(wt, n, sigma, width):
     with pytest.raises(wt.WtError) as e:
         wt.sizes(n, sigma, width)
@@ -81,10 +82,11 @@ def test_build_validates_before_touching_the_device(wt):
 
 
 def test_launch_plan(wt):
-    lv = ["tile_scan", "level"]
+    lv = ["tables", "memset", "tile_scan", "level"]
     last = ["tile_scan", "last_level"]
-    assert wt.launch_plan(1 << 20, 256, 1) == ["hist", "scan", "tables", "tables"] + lv * 7 + last
-    assert wt.launch_plan(1 << 20, 4, 1) == ["hist", "scan", "tables", "tables"] + lv + last
-    assert wt.launch_plan(100, 2, 1) == ["hist", "scan"] + last
-    assert wt.launch_plan(100, 1, 1) == ["hist", "scan"]
+    assert wt.launch_plan(1 << 20, 256, 1) == (["prologue", "tables", "memset", "tile_scan", "level"] + lv * 6
+                                               + ["scan"] + last)
+    assert wt.launch_plan(1 << 20, 4, 1) == ["prologue", "tables", "memset", "tile_scan", "level", "scan"] + last
+    assert wt.launch_plan(100, 2, 1) == ["prologue", "scan"] + last
+    assert wt.launch_plan(100, 1, 1) == ["prologue", "scan"]
     assert wt.launch_plan(0, 16, 1) == []
