@@ -170,8 +170,23 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const uint32_t nvalid = (i0 >= len) ? 0u : min((uint32_t)E, len - i0);
     uint32_t m[NH], nbm[NH], vm[NH];
     vm[0] = lowmask(min(nvalid, 32u)) & EM;
-    m[0] = swar_bits<T, XW / NH, 0>(xw, sh) & vm[0];
-    nbm[0] = SCATTER ? (swar_bits<T, XW / NH, 0>(xw, sh - 1) & vm[0]) : 0u;  // next level's bits
+    if constexpr (sizeof(T) == 4) {
+      // one funnel rotation per symbol serves both masks: rotr(x, sh - k)
+      // puts bit sh at k and bit sh-1 at k-1 (mod 32); nbm is accumulated
+      // rotated by one and fixed at the end
+      uint32_t mm = 0, nn = 0;
+#pragma unroll
+      for (int k = 0; k < XW; ++k) {
+        const uint32_t r = __funnelshift_r(xw[k], xw[k], sh - (uint32_t)k);
+        mm |= r & (1u << k);
+        if (SCATTER) nn |= r & (1u << ((k + 31) & 31));
+      }
+      m[0] = mm & vm[0];
+      nbm[0] = SCATTER ? (__funnelshift_l(nn, nn, 1) & vm[0]) : 0u;  // next level's bits
+    } else {
+      m[0] = swar_bits<T, XW / NH, 0>(xw, sh) & vm[0];
+      nbm[0] = SCATTER ? (swar_bits<T, XW / NH, 0>(xw, sh - 1) & vm[0]) : 0u;  // next level's bits
+    }
     if constexpr (NH == 2) {
       vm[NH - 1] = lowmask(nvalid > 32 ? nvalid - 32 : 0u);
       m[NH - 1] = swar_bits<T, XW / 2, XW / 2>(xw, sh) & vm[NH - 1];
@@ -301,27 +316,24 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
 #ifndef WT_EXP_SKIP_COUNT
     {
       // count of nbm bits among the set bits of M, split at rank k (the set
-      // bits of M have ranks rank0, rank0+1, ... in position order)
+      // bits of M have ranks rank0, rank0+1, ... in position order).  Only
+      // the lane holding rank k searches for its k-th set bit.
       auto split = [&](const uint32_t(&M)[NH], int32_t rank0, int32_t k, uint32_t& lo, uint32_t& hi) {
-        lo = hi = 0;
+        uint64_t M64 = M[0], N64 = nbm[0];
+        if constexpr (NH == 2) M64 |= (uint64_t)M[1] << 32, N64 |= (uint64_t)nbm[1] << 32;
+        const uint32_t tot = (uint32_t)__popcll(N64 & M64);
+        const int32_t nM = __popcll(M64);
+        if (rank0 + nM <= k) lo = tot;
+        else if (rank0 >= k) lo = 0;
+        else {  // lowest (k - rank0) set bits of M
+          const int32_t j = k - rank0;
+          uint32_t p = 0;
 #pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          const int32_t nM = __popc(M[h]);
-          uint32_t Mlo;
-          if (rank0 + nM <= k) Mlo = M[h];
-          else if (rank0 >= k) Mlo = 0;
-          else {  // the one lane per region holding the split: lowest (k - rank0) set bits of M
-            const int32_t j = k - rank0;
-            uint32_t p = 0;
-#pragma unroll
-            for (uint32_t st = 16; st; st >>= 1)
-              if (__popc(M[h] & lowmask(p + st)) <= j) p += st;
-            Mlo = M[h] & lowmask(p);
-          }
-          lo += (uint32_t)__popc(nbm[h] & Mlo);
-          hi += (uint32_t)__popc(nbm[h] & M[h] & ~Mlo);
-          rank0 += nM;
+          for (uint32_t st = 32 * NH / 2; st; st >>= 1)
+            if (__popcll(M64 & ((1ull << (p + st)) - 1)) <= j) p += st;
+          lo = (uint32_t)__popcll(N64 & M64 & ((1ull << p) - 1));
         }
+        hi = tot - lo;
       };
       auto put2 = [&](int key, uint32_t lo, uint32_t hi) {  // keys (key, key+1) in one reduction
         const uint32_t sum = __reduce_add_sync(FULL, lo | (hi << 16));
@@ -552,25 +564,30 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     __syncwarp();  // stage partitioned (and the input buffer fully read)
 
     // ---------------- phase E: TMA bulk stores of the aligned bodies, element stores of the edges
-#pragma unroll
-    for (int r = 0; r < LV_NREG; ++r) {
-      if (rl[r] <= 0) continue;  // warp-uniform
-      const int32_t b = rb[r], end = b + rl[r];
+    auto emit_region = [&](int32_t b, int32_t l, long long D) {  // stage [b, b+l) -> HBM [D, D+l)
+      if (l <= 0) return;  // warp-uniform
+      const int32_t end = b + l;
       const int32_t fs = (b + A - 1) / A * A, fe = end / A * A;
-      const long long go = rD[r] - b;  // HBM destination of stage position q: q + go
+      const long long go = D - b;  // HBM destination of stage position q: q + go
       if (lane == 0 && fe > fs)
         bulk_s2g(out + (go + fs), S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
       // head edge [b, min(fs, end)) and tail edge [max(fe, that), end), each < A symbols
       const int32_t hend = min(fs, end), tst = max(fe, hend);
       const int32_t q = (lane < (uint32_t)A) ? b + (int32_t)lane : tst + (int32_t)lane - A;
       if (lane < (uint32_t)(2 * A) && ((lane < (uint32_t)A) ? (q < hend) : (q < end))) out[go + q] = S.buf[ob][q];
+    };
+    if (one) {  // warp-uniform: the first segment's two runs only
+      emit_region(b1, z0, D0z);
+      emit_region(b2, o0, D0o);
+    } else {
+#pragma unroll
+      for (int r = 0; r < LV_NREG; ++r) emit_region(rb[r], rl[r], rD[r]);
     }
     if (lane == 0) bulk_commit();
     if (lane < (uint32_t)LV_NKEY && mycnt) {  // next-level ones per destination tile
       const int r = (int)(lane >> 1);
-      long long D = rD[0];
-#pragma unroll
-      for (int k = 1; k < LV_NREG; ++k) D = (r == k) ? rD[k] : D;
+      long long D = r == 1 ? D0z : D0o;
+      if (!one) D = r == 3 ? Dmz : r == 4 ? Dmo : D;
       atomicAdd(&agg_next[r == 0 ? tile : (unsigned long long)D / TILE + (lane & 1)], mycnt);
     }
     // the previous tile's output buffer: once its bulk stores have read it, load a new tile into it
