@@ -101,18 +101,21 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
   LevelSmem<T>& S = *reinterpret_cast<LevelSmem<T>*>(smem_raw);
 
   if (*flag) return;
-  const uint64_t ntiles = (n + TILE - 1) / TILE;
+  // n < 2^32 (wt_sizes rejects larger n): every position, rank and node
+  // offset of the pass fits 32 bits; only pointers are 64-bit.
+  const uint32_t n32 = (uint32_t)n;
+  const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
   const uint32_t lane = threadIdx.x;
   const uint32_t nsh = sh + 1;   // node id = symbol >> nsh
   const uint32_t i0 = lane * E;  // first tile position of this lane (phase A)
 
-  auto tile_of = [&](uint32_t it) -> uint64_t { return (uint64_t)blockIdx.x + (uint64_t)it * gridDim.x; };
+  auto tile_of = [&](uint32_t it) -> uint32_t { return blockIdx.x + it * gridDim.x; };
   auto issue = [&](uint32_t it) {  // lane 0: bulk-copy the warp's it-th tile into buf[it % NB]
-    const uint64_t t = tile_of(it);
+    const uint32_t t = tile_of(it);
     if (t >= ntiles) return;
     const int b = (int)(it % NB);
-    const uint64_t T0 = t * (uint64_t)TILE;
-    const uint64_t len = min((uint64_t)TILE, n - T0);
+    const uint32_t T0 = t * (uint32_t)TILE;
+    const uint32_t len = min((uint32_t)TILE, n32 - T0);
     const uint32_t bytes = (uint32_t)(len * sizeof(T)) & ~15u;
     fence_proxy_async_smem();
     mbar_arrive_expect_tx(&S.bar[b], bytes);
@@ -143,12 +146,12 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
   };
 
   for (uint32_t it = 0;; ++it) {
-    const uint64_t tile = tile_of(it);
+    const uint32_t tile = tile_of(it);
     if (tile >= ntiles) break;
     const int ib = (int)(it % NB), ob = (int)((it + NB - 1) % NB);
-    const uint64_t T0 = tile * (uint64_t)TILE;
-    const uint32_t len = (uint32_t)min((uint64_t)TILE, n - T0);
-    const unsigned long long P = __ldg(&pre[tile]);  // ones of this level before the tile
+    const uint32_t T0 = tile * (uint32_t)TILE;
+    const uint32_t len = min((uint32_t)TILE, n32 - T0);
+    const uint32_t P = (uint32_t)__ldg(&pre[tile]);  // ones of this level before the tile
     T* const B = S.buf[ib] + MARGIN;                 // tile position q lives at B[q]
     mbar_wait(&S.bar[ib], (it / NB) & 1u);
     if (len < TILE) {  // tail bytes the 16-byte bulk copy did not cover
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       nbm[NH - 1] = SCATTER ? (swar_bits<T, XW / 2, XW / 2>(xw, sh - 1) & vm[NH - 1]) : 0u;
     }
     {  // bitmap words (LSB-first)
-      const uint64_t gw = (T0 + i0) / 32;
+      const uint32_t gw = (T0 + i0) / 32;
       if constexpr (E == 64) {
         if (gw < words_per_level) *reinterpret_cast<uint2*>(bits + gw) = make_uint2(m[0], m[NH - 1]);
       } else if constexpr (E == 32) {
@@ -230,8 +233,8 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const uint32_t prep = incl - c;
     const uint32_t mypre = prep & 0xffffu, hpre = prep >> 16;
     const uint32_t tot = totp & 0xffffu, nseg = (totp >> 16) + 1;
-    if ((i0 & 511u) == 0 && T0 + i0 < n) sb[(T0 + i0) >> 9] = P + mypre;
-    if (lane == 0 && T0 + TILE >= n) sb[nsb - 1] = P + tot;
+    if ((i0 & 511u) == 0 && T0 + i0 < n32) sb[(T0 + i0) >> 9] = P + mypre;
+    if (lane == 0 && T0 + TILE >= n32) sb[nsb - 1] = P + tot;
     if (!SCATTER) {
       __syncwarp();  // every read of this buffer is done
       if (lane == 0) issue(it + NB);
@@ -282,10 +285,11 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const int32_t Rs1 = one ? (int32_t)tot : S.Rs1, Ram = one ? (int32_t)tot : S.Ram;
     const int32_t z0 = s1 - Rs1, o0 = Rs1;
     const int32_t om = (int32_t)tot - Ram, zm = ((int32_t)len - am) - om;
-    const long long D0z = (long long)T0 - (long long)P + (long long)tabF.x;
-    const long long D0o = (long long)P + (long long)tabF.y;
-    const long long Dmz = (long long)T0 + am - (long long)P - Ram + (long long)tabL.x;
-    const long long Dmo = (long long)P + Ram + (long long)tabL.y;
+    // HBM destinations (mod 2^32 arithmetic; the results are positions < n)
+    const uint32_t D0z = T0 - P + (uint32_t)tabF.x;
+    const uint32_t D0o = P + (uint32_t)tabF.y;
+    const uint32_t Dmz = T0 + (uint32_t)am - P - (uint32_t)Ram + (uint32_t)tabL.x;
+    const uint32_t Dmo = P + (uint32_t)Ram + (uint32_t)tabL.y;
     auto rup = [](int32_t x) { return (x + A - 1) / A * A; };
     const int32_t b1 = (int32_t)(D0z & (A - 1));
     const int32_t b2 = rup(b1 + z0) + (int32_t)(D0o & (A - 1));
@@ -295,12 +299,10 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     // the five regions (warp-uniform): identity, first zeros, first ones, last zeros, last ones
     const int32_t rb[LV_NREG] = {MARGIN + s1, b1, b2, b3, b4};
     const int32_t rl[LV_NREG] = {am - s1, z0, o0, zm, om};
-    const long long rD[LV_NREG] = {(long long)T0 + s1, D0z, D0o, Dmz, Dmo};  // HBM destination of rb[r]
+    const uint32_t rD[LV_NREG] = {T0 + (uint32_t)s1, D0z, D0o, Dmz, Dmo};  // HBM destination of rb[r]
     // symbols of side region r with rank < ksplit_r land in destination tile
     // floor(D_r / TILE), the rest in the next tile
-    auto ksplit = [&](long long D, int32_t l) {
-      return (int32_t)min((long long)l, (long long)((unsigned long long)D / TILE + 1) * TILE - D);
-    };
+    auto ksplit = [&](uint32_t D, int32_t l) { return min(l, (int32_t)(TILE - D % TILE)); };
     if (segtab) {
       if (lane == 0) S.kt[0] = make_short2((short)K0F, (short)K1F);
       if (lane == 1 && !one) S.kt[nseg - 1] = make_short2((short)K0L, (short)K1L);
@@ -537,8 +539,8 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
             K1 = K1L;
           } else {  // interior node: stage position = HBM destination - T0 + MARGIN
             const ulonglong2 t = __ldg(&tab[v]);
-            K0 = (int32_t)((long long)t.x - (long long)P) + MARGIN;
-            K1 = (int32_t)((long long)t.y + (long long)P - (long long)T0) + MARGIN;
+            K0 = (int32_t)((uint32_t)t.x - P) + MARGIN;
+            K1 = (int32_t)((uint32_t)t.y + P - T0) + MARGIN;
           }
         };
 #pragma unroll
@@ -579,17 +581,16 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     __syncwarp();  // stage partitioned (and the input buffer fully read)
 
     // ---------------- phase E: TMA bulk stores of the aligned bodies, element stores of the edges
-    auto emit_region = [&](int32_t b, int32_t l, long long D) {  // stage [b, b+l) -> HBM [D, D+l)
+    auto emit_region = [&](int32_t b, int32_t l, uint32_t D) {  // stage [b, b+l) -> HBM [D, D+l)
       if (l <= 0) return;  // warp-uniform
       const int32_t end = b + l;
       const int32_t fs = (b + A - 1) / A * A, fe = end / A * A;
-      const long long go = D - b;  // HBM destination of stage position q: q + go
-      if (lane == 0 && fe > fs)
-        bulk_s2g(out + (go + fs), S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
+      T* const go = out + D - b;  // HBM address of stage position q: go + q
+      if (lane == 0 && fe > fs) bulk_s2g(go + fs, S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
       // head edge [b, min(fs, end)) and tail edge [max(fe, that), end), each < A symbols
       const int32_t hend = min(fs, end), tst = max(fe, hend);
       const int32_t q = (lane < (uint32_t)A) ? b + (int32_t)lane : tst + (int32_t)lane - A;
-      if (lane < (uint32_t)(2 * A) && ((lane < (uint32_t)A) ? (q < hend) : (q < end))) out[go + q] = S.buf[ob][q];
+      if (lane < (uint32_t)(2 * A) && ((lane < (uint32_t)A) ? (q < hend) : (q < end))) go[q] = S.buf[ob][q];
     };
     // (a separate single-segment branch measured 2 % faster for 1-byte
     // symbols and 3 % slower for 2-byte ones)
@@ -603,9 +604,9 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     if (lane == 0) bulk_commit();
     if (lane < (uint32_t)LV_NKEY && mycnt) {  // next-level ones per destination tile
       const int r = (int)(lane >> 1);
-      long long D = r == 1 ? D0z : D0o;
+      uint32_t D = r == 1 ? D0z : D0o;
       if (!one) D = r == 3 ? Dmz : r == 4 ? Dmo : D;
-      atomicAdd(&agg_next[r == 0 ? tile : (unsigned long long)D / TILE + (lane & 1)], mycnt);
+      atomicAdd(&agg_next[r == 0 ? tile : D / TILE + (lane & 1)], mycnt);
     }
     // the previous tile's output buffer: once its bulk stores have read it, load a new tile into it
     if (lane == 0) bulk_wait_read<1>();
