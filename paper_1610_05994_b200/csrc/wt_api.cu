@@ -119,9 +119,9 @@ Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
   c.off_value = o;  // look-back values: written before their status, never read stale
   o += align_up(2 * c.status_entries * sizeof(uint64_t));
   c.off_pre = o;
-  o += align_up(c.ntiles * sizeof(uint64_t));
+  o += align_up(c.ntiles * sizeof(uint32_t));
   c.off_tab = o;
-  o += align_up(c.tab_entries * sizeof(ulonglong2));
+  o += align_up(c.tab_entries * sizeof(uint2));
   c.off_cnt = o;
   o += 2 * align_up(c.cnt_entries * sizeof(uint32_t));
   const size_t seq_bytes = align_up(n * width);
@@ -197,9 +197,9 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   unsigned long long* ones0 = reinterpret_cast<unsigned long long*>(ws + c.off_ones0);
   const wt::LookbackState status{reinterpret_cast<uint32_t*>(ws + c.off_status),
                                  reinterpret_cast<uint64_t*>(ws + c.off_value), c.status_entries};
-  ulonglong2* tab = reinterpret_cast<ulonglong2*>(ws + c.off_tab);
+  uint2* tab = reinterpret_cast<uint2*>(ws + c.off_tab);
   uint32_t* agg = reinterpret_cast<uint32_t*>(ws + c.off_agg);
-  unsigned long long* pre = reinterpret_cast<unsigned long long*>(ws + c.off_pre);
+  uint32_t* pre = reinterpret_cast<uint32_t*>(ws + c.off_pre);
   uint32_t* cnt[2] = {reinterpret_cast<uint32_t*>(ws + c.off_cnt),
                       reinterpret_cast<uint32_t*>(ws + c.off_cnt + align_up(c.cnt_entries * sizeof(uint32_t)))};
   T* buf[2] = {reinterpret_cast<T*>(ws + c.off_bufA), reinterpret_cast<T*>(ws + c.off_bufB)};
@@ -300,7 +300,7 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
       T* o = last ? nullptr : buf[l & 1];
       const uint32_t sh = L - 1 - l;
-      const ulonglong2* t = last ? nullptr : tab + ((1ull << l) - 1);
+      const uint2* t = last ? nullptr : tab + ((1ull << l) - 1);
       uint32_t* bits = out->bitmaps + (uint64_t)l * c.words;
       unsigned long long* sb = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
       uint32_t* agg_next = last ? nullptr : agg + (uint64_t)(l + 1) * c.ntiles;

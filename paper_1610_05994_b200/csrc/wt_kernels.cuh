@@ -72,11 +72,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Op op, uint64_t count, Lo
 
 // Per-tile prefixes: pre[t] = sum_{t' < t} agg[t'] (ones of the level before
 // tile t), from the per-tile ones counted by the previous pass.
-struct OpTilePrefix {
+struct OpTilePrefix {  // (n < 2^32: the prefixes fit 32 bits)
   const uint32_t* agg;
-  unsigned long long* pre;
+  uint32_t* pre;
   __device__ uint64_t load(uint64_t i) const { return agg[i]; }
-  __device__ void store(uint64_t i, uint64_t excl, uint64_t) const { pre[i] = excl; }
+  __device__ void store(uint64_t i, uint64_t excl, uint64_t) const { pre[i] = (uint32_t)excl; }
 };
 
 // Node tables of level l from the sizes of the level-(l+1) nodes
@@ -89,7 +89,7 @@ struct OpTilePrefix {
 // One scan over v of the packed pair (left | total << 32); n < 2^32.
 struct OpLevelTab {
   const uint32_t* cnt;
-  ulonglong2* tab;  // the level's slice
+  uint2* tab;  // the level's slice: {ob, Zn} (n < 2^32)
   uint64_t n;
   const unsigned long long* ones0;  // non-null for level 0
   __device__ uint64_t load(uint64_t v) const {
@@ -106,7 +106,7 @@ struct OpLevelTab {
   __device__ void store(uint64_t v, uint64_t excl, uint64_t val) const {
     const uint64_t left = val & 0xffffffffull;
     const uint64_t zn = (excl & 0xffffffffull) + left, N = excl >> 32;
-    tab[v] = make_ulonglong2(N - (zn - left), zn);
+    tab[v] = make_uint2((uint32_t)(N - (zn - left)), (uint32_t)zn);
   }
 };
 

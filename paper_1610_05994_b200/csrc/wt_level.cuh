@@ -90,8 +90,8 @@ constexpr size_t level_smem_bytes() {
 template <typename T, bool SCATTER>
 __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     k_level(const T* __restrict__ in, T* __restrict__ out, uint64_t n, uint32_t sh,
-            const ulonglong2* __restrict__ tab, uint32_t* __restrict__ bits, uint64_t words_per_level,
-            unsigned long long* __restrict__ sb, uint64_t nsb, const unsigned long long* __restrict__ pre,
+            const uint2* __restrict__ tab, uint32_t* __restrict__ bits, uint64_t words_per_level,
+            unsigned long long* __restrict__ sb, uint64_t nsb, const uint32_t* __restrict__ pre,
             uint32_t* __restrict__ agg_next, uint32_t* __restrict__ cnt_next, const int32_t* __restrict__ flag) {
   using Cfg = LvTile<T>;
   constexpr int TILE = Cfg::TILE, A = Cfg::A, E = Cfg::E, SPW = Cfg::SPW, XW = Cfg::XW, NH = Cfg::NH;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const int ib = (int)(it % NB), ob = (int)((it + NB - 1) % NB);
     const uint32_t T0 = tile * (uint32_t)TILE;
     const uint32_t len = min((uint32_t)TILE, n32 - T0);
-    const uint32_t P = (uint32_t)__ldg(&pre[tile]);  // ones of this level before the tile
+    const uint32_t P = __ldg(&pre[tile]);  // ones of this level before the tile
     T* const B = S.buf[ib] + MARGIN;                 // tile position q lives at B[q]
     mbar_wait(&S.bar[ib], (it / NB) & 1u);
     if (len < TILE) {  // tail bytes the 16-byte bulk copy did not cover
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         }
       }
     }
-    const ulonglong2 tabF = __ldg(&tab[vF]), tabL = __ldg(&tab[vL]);
+    const uint2 tabF = __ldg(&tab[vF]), tabL = __ldg(&tab[vL]);
     __syncwarp();  // own[], segment table
 
     // ---------------- constants of the tile's regions (every lane; lane r keeps region r)
@@ -286,10 +286,10 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const int32_t z0 = s1 - Rs1, o0 = Rs1;
     const int32_t om = (int32_t)tot - Ram, zm = ((int32_t)len - am) - om;
     // HBM destinations (mod 2^32 arithmetic; the results are positions < n)
-    const uint32_t D0z = T0 - P + (uint32_t)tabF.x;
-    const uint32_t D0o = P + (uint32_t)tabF.y;
-    const uint32_t Dmz = T0 + (uint32_t)am - P - (uint32_t)Ram + (uint32_t)tabL.x;
-    const uint32_t Dmo = P + (uint32_t)Ram + (uint32_t)tabL.y;
+    const uint32_t D0z = T0 - P + tabF.x;
+    const uint32_t D0o = P + tabF.y;
+    const uint32_t Dmz = T0 + (uint32_t)am - P - (uint32_t)Ram + tabL.x;
+    const uint32_t Dmo = P + (uint32_t)Ram + tabL.y;
     auto rup = [](int32_t x) { return (x + A - 1) / A * A; };
     const int32_t b1 = (int32_t)(D0z & (A - 1));
     const int32_t b2 = rup(b1 + z0) + (int32_t)(D0o & (A - 1));
@@ -538,9 +538,9 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
             K0 = K0L;
             K1 = K1L;
           } else {  // interior node: stage position = HBM destination - T0 + MARGIN
-            const ulonglong2 t = __ldg(&tab[v]);
-            K0 = (int32_t)((uint32_t)t.x - P) + MARGIN;
-            K1 = (int32_t)((uint32_t)t.y + P - T0) + MARGIN;
+            const uint2 t = __ldg(&tab[v]);
+            K0 = (int32_t)(t.x - P) + MARGIN;
+            K1 = (int32_t)(t.y + P - T0) + MARGIN;
           }
         };
 #pragma unroll
