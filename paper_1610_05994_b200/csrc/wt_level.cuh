@@ -592,16 +592,43 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       const int32_t q = (lane < (uint32_t)A) ? b + (int32_t)lane : tst + (int32_t)lane - A;
       if (lane < (uint32_t)(2 * A) && ((lane < (uint32_t)A) ? (q < hend) : (q < end))) go[q] = S.buf[ob][q];
     };
-    // (a separate single-segment branch measured 2 % faster for 1-byte
-    // symbols and 3 % slower for 2-byte ones)
-    if (sizeof(T) == 1 && one) {  // warp-uniform: the first segment's two runs only
-      emit_region(b1, z0, D0z);
-      emit_region(b2, o0, D0o);
-    } else {
+    if constexpr (sizeof(T) == 1) {  // (A = 16: one region's two edges fill the warp)
+      if (one) {  // warp-uniform: the first segment's two runs only
+        emit_region(b1, z0, D0z);
+        emit_region(b2, o0, D0o);
+      } else {
 #pragma unroll
-      for (int r = 0; r < LV_NREG; ++r) emit_region(rb[r], rl[r], rD[r]);
+        for (int r = 0; r < LV_NREG; ++r) emit_region(rb[r], rl[r], rD[r]);
+      }
+      if (lane == 0) bulk_commit();
+    } else {
+      // lane r < LV_NREG: region r's bulk store; then all regions' edge
+      // symbols (<= 2A each) as one lane-parallel list of slots
+      const uint32_t r_ = min(lane, (uint32_t)(LV_NREG - 1));
+      int32_t b = rb[0], l = rl[0];
+      uint32_t D = rD[0];
+#pragma unroll
+      for (int k = 1; k < LV_NREG; ++k)
+        if (r_ == (uint32_t)k) b = rb[k], l = rl[k], D = rD[k];
+      if (lane >= (uint32_t)LV_NREG) l = 0;
+      const int32_t end = b + l, fs = (b + A - 1) / A * A, fe = end / A * A;
+      const uint32_t Dmb = D - (uint32_t)b;  // HBM position of stage position q: Dmb + q
+      if (l > 0 && fe > fs) bulk_s2g(out + (Dmb + (uint32_t)fs), S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
+      if (lane < (uint32_t)LV_NREG) bulk_commit();
+      const int32_t hend = l > 0 ? min(fs, end) : b, tst = max(fe, hend), endv = l > 0 ? end : b;
+#pragma unroll
+      for (uint32_t base = 0; base < (uint32_t)(2 * A * LV_NREG); base += 32) {
+        const uint32_t slot = base + lane;
+        const int rs = (int)min(slot / (2 * A), (uint32_t)(LV_NREG - 1));
+        const uint32_t e = slot % (2 * A);
+        const int32_t b_ = __shfl_sync(FULL, b, rs), hend_ = __shfl_sync(FULL, hend, rs);
+        const int32_t tst_ = __shfl_sync(FULL, tst, rs), end_ = __shfl_sync(FULL, endv, rs);
+        const uint32_t Dmb_ = __shfl_sync(FULL, Dmb, rs);
+        const int32_t q = (e < (uint32_t)A) ? b_ + (int32_t)e : tst_ + (int32_t)e - A;
+        if (slot < (uint32_t)(2 * A * LV_NREG) && ((e < (uint32_t)A) ? (q < hend_) : (q < end_)))
+          out[Dmb_ + (uint32_t)q] = S.buf[ob][q];
+      }
     }
-    if (lane == 0) bulk_commit();
     if (lane < (uint32_t)LV_NKEY && mycnt) {  // next-level ones per destination tile
       const int r = (int)(lane >> 1);
       uint32_t D = r == 1 ? D0z : D0o;
@@ -609,13 +636,13 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       atomicAdd(&agg_next[r == 0 ? tile : D / TILE + (lane & 1)], mycnt);
     }
     // the previous tile's output buffer: once its bulk stores have read it, load a new tile into it
-    if (lane == 0) bulk_wait_read<1>();
+    if (sizeof(T) == 1 ? lane == 0 : lane < (uint32_t)LV_NREG) bulk_wait_read<1>();  // each lane's own groups
     __syncwarp();
     if (lane == 0 && it >= 1) issue(it + NB - 2);
   }
   if (SCATTER) {
     cc_flush();
-    if (lane == 0) bulk_wait<0>();
+    if (sizeof(T) == 1 ? lane == 0 : lane < (uint32_t)LV_NREG) bulk_wait<0>();
   }
 }
 
