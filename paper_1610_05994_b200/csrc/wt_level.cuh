@@ -411,25 +411,38 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       }
       cc_acc += lane == 0 ? (len - tot) - c01 : lane == 1 ? c01 : lane == 2 ? tot - c11 : c11;
     } else if (nvalid) {  // the lane's pieces: maximal runs of its symbols inside one node
-      uint64_t M = m[0], NB = nbm[0], V = vm[0], H = hm[0];
+      // (two node counts per 64-bit atomic: each stays < 2^32, no carry)
+      auto piece = [&](uint32_t node, uint32_t c00, uint32_t c01, uint32_t c10, uint32_t c11) {
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(cnt_next + 4u * node);
+        const unsigned long long lo = (unsigned long long)c00 | ((unsigned long long)c01 << 32);
+        const unsigned long long hi = (unsigned long long)c10 | ((unsigned long long)c11 << 32);
+        if (lo) atomicAdd(dst, lo);
+        if (hi) atomicAdd(dst + 1, hi);
+      };
       if constexpr (NH == 2) {
-        M |= (uint64_t)m[1] << 32, NB |= (uint64_t)nbm[1] << 32;
-        V |= (uint64_t)vm[1] << 32, H |= (uint64_t)hm[1] << 32;
-      }
-      uint64_t starts = (H | 1ull) & V;
-      while (starts) {
-        const int p = __ffsll((long long)starts) - 1;
-        starts &= starts - 1;
-        const int pend = starts ? __ffsll((long long)starts) - 1 : 64;
-        const uint64_t pm = V & ((pend >= 64 ? ~0ull : ((1ull << pend) - 1)) & ~((1ull << p) - 1));
-        const uint64_t z = pm & ~M, o = pm & M;
-        const uint64_t c01 = (uint64_t)__popcll(z & ~NB) | ((uint64_t)__popcll(z & NB) << 32);
-        const uint64_t c23 = (uint64_t)__popcll(o & ~NB) | ((uint64_t)__popcll(o & NB) << 32);
-        // two node counts per 64-bit atomic (each stays < 2^32: no carry)
-        unsigned long long* dst =
-            reinterpret_cast<unsigned long long*>(cnt_next + 4ull * ((uint32_t)B[i0 + p] >> nsh));
-        if (c01) atomicAdd(dst, (unsigned long long)c01);
-        if (c23) atomicAdd(dst + 1, (unsigned long long)c23);
+        const uint64_t M = m[0] | ((uint64_t)m[1] << 32), NB = nbm[0] | ((uint64_t)nbm[1] << 32);
+        const uint64_t V = vm[0] | ((uint64_t)vm[1] << 32), H = hm[0] | ((uint64_t)hm[1] << 32);
+        uint64_t starts = (H | 1ull) & V;
+        while (starts) {
+          const int p = __ffsll((long long)starts) - 1;
+          starts &= starts - 1;
+          const int pend = starts ? __ffsll((long long)starts) - 1 : 64;
+          const uint64_t pm = V & ((pend >= 64 ? ~0ull : ((1ull << pend) - 1)) & ~((1ull << p) - 1));
+          const uint64_t z = pm & ~M, o = pm & M;
+          piece((uint32_t)B[i0 + p] >> nsh, __popcll(z & ~NB), __popcll(z & NB), __popcll(o & ~NB),
+                __popcll(o & NB));
+        }
+      } else {
+        const uint32_t M = m[0], NB = nbm[0], V = vm[0];
+        uint32_t starts = (hm[0] | 1u) & V;
+        while (starts) {
+          const int p = __ffs(starts) - 1;
+          starts &= starts - 1;
+          const int pend = starts ? __ffs(starts) - 1 : 32;
+          const uint32_t pm = V & lowmask((uint32_t)pend) & ~((1u << p) - 1u);
+          const uint32_t z = pm & ~M, o = pm & M;
+          piece((uint32_t)B[i0 + p] >> nsh, __popc(z & ~NB), __popc(z & NB), __popc(o & ~NB), __popc(o & NB));
+        }
       }
     }
 #endif
