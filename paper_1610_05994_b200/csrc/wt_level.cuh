@@ -74,8 +74,8 @@ struct LevelSmem {
   uint16_t seg_a[C::MAXSEG + 1];      // segment g starts at tile position seg_a[g] (g >= 1)
   uint16_t seg_R[C::MAXSEG + 1];      // tile-local ones before seg_a[g]
   short2 kt[C::MAXSEG];               // segment g: stage offsets {K0, K1} relative to the output buffer
-  uint32_t lut[16];                   // in-word stable partition selectors (partition_lut_entry)
-  uint4 lutz[16];                     // lutz[bits].k = 1 if slot k of the partitioned word is a zero
+  uint4 lut[16];                      // in-word stable partition: {selector | nz << 16, z1, z2, z3},
+                                      // z_k = 1 if slot k of the partitioned word is a zero
   int32_t s1, am, Rs1, Ram;           // first-segment end, last-segment start, ranks there
   alignas(8) unsigned long long bar[C::NB];
 };
@@ -129,8 +129,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
   }
   if (SCATTER && lane < 16) {
     const uint32_t e = partition_lut_entry<T>(lane), nz = e >> 16;
-    S.lut[lane] = e;
-    S.lutz[lane] = make_uint4(nz > 0, nz > 1, nz > 2, nz > 3);
+    S.lut[lane] = make_uint4(e, nz > 1, nz > 2, nz > 3);
   }
   __syncwarp();
 
@@ -459,31 +458,31 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       const uint32_t hh = soff / 32, sub = soff % 32;
       const uint32_t submask = lowmask(sub), subhead = lowmask(sub + 1);
       const uint4* own = S.own[NH == 1 ? 0 : hh];
-      auto lut_of = [&](uint32_t m4) -> uint32_t { return SPW == 1 ? 0u : S.lut[m4 & ((1u << SPW) - 1u)]; };
-      auto lutz_of = [&](uint32_t m4) -> uint4 {
-        return SPW == 1 ? make_uint4(0, 0, 0, 0) : S.lutz[m4 & ((1u << SPW) - 1u)];
+      auto lut_of = [&](uint32_t m4) -> uint4 {
+        return SPW == 1 ? make_uint4(0, 0, 0, 0) : S.lut[m4 & ((1u << SPW) - 1u)];
       };
       // stores the SPW symbols of word x (tile position q0, R ones before it,
-      // bits m4, in-word partition e / zero slots z) into segment (K0, K1)
-      // (stage offsets).  Slot k of the partitioned word y goes to
+      // bits m4, in-word partition e) into segment (K0, K1) (stage offsets
+      // relative to the buffer).  Slot k of the partitioned word y goes to
       // Ao + k + z_k (Az - Ao): the slot choice is a multiply-add (FMA pipe)
       // and the symbol extraction a multiply-high, keeping the ALU pipe free.
       auto word_one_segment = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, int32_t K0, int32_t K1,
-                                  uint32_t e, uint4 z) {
+                                  uint4 e) {
         if constexpr (SPW == 1) {
           const int32_t az = sbuf + (int32_t)(q0 - R) + K0;
           st_shared<T>((uint32_t)((m4 & 1u) ? sbuf + (int32_t)R + K1 : az) * (uint32_t)sizeof(T), x);
         } else {
-          const uint32_t y = __byte_perm(x, 0u, e);
-          const int32_t nz = (int32_t)(e >> 16);
+          uint32_t y;
+          asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(x), "r"(e.x));  // selector = e.x[15:0]
+          const int32_t nz = (int32_t)(e.x >> 16);
           const uint32_t Az = (uint32_t)(sbuf + (int32_t)(q0 - R) + K0) * (uint32_t)sizeof(T);
           const uint32_t Ao = (uint32_t)(sbuf + (int32_t)R + K1 - nz) * (uint32_t)sizeof(T);
           const uint32_t d = Az - Ao;
-          st_shared<T, 0>(Ao + z.x * d, y);
-          st_shared<T, sizeof(T)>(Ao + z.y * d, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
+          st_shared<T, 0>(nz ? Az : Ao, y);
+          st_shared<T, sizeof(T)>(Ao + e.y * d, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
           if constexpr (SPW > 2) {
-            st_shared<T, 2>(Ao + z.z * d, __umulhi(y, 1u << 16));
-            st_shared<T, 3>(Ao + z.w * d, __umulhi(y, 1u << 8));
+            st_shared<T, 2>(Ao + e.z * d, __umulhi(y, 1u << 16));
+            st_shared<T, 3>(Ao + e.w * d, __umulhi(y, 1u << 8));
           }
         }
       };
@@ -492,24 +491,21 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         constexpr int BK = 4;
 #pragma unroll
         for (int k0 = 0; k0 < XW; k0 += BK) {
-          uint32_t xs[BK], Rs[BK], ms[BK], es[BK];
-          uint4 zs[BK];
+          uint32_t xs[BK], Rs[BK], ms[BK];
+          uint4 es[BK];
 #pragma unroll
           for (int k = 0; k < BK; ++k) {
             const uint32_t w = lane + 32 * (k0 + k);
             const uint2 ow = *reinterpret_cast<const uint2*>(&own[w / XW]);
             xs[k] = Win[w];
-            Rs[k] = (ow.y & 0xffffu) + (uint32_t)__popc(ow.x & submask);
+            Rs[k] = ow.y + (uint32_t)__popc(ow.x & submask);  // one segment: no head count in ow.y
             ms[k] = ow.x >> sub;
           }
 #pragma unroll
-          for (int k = 0; k < BK; ++k) {
-            es[k] = lut_of(ms[k]);
-            zs[k] = lutz_of(ms[k]);
-          }
+          for (int k = 0; k < BK; ++k) es[k] = lut_of(ms[k]);
 #pragma unroll
           for (int k = 0; k < BK; ++k)
-            word_one_segment(xs[k], (lane + 32 * (k0 + k)) * SPW, Rs[k], ms[k], K0F, K1F, es[k], zs[k]);
+            word_one_segment(xs[k], (lane + 32 * (k0 + k)) * SPW, Rs[k], ms[k], K0F, K1F, es[k]);
         }
       } else if (segtab) {  // segment table in shared memory
 #pragma unroll
@@ -526,7 +522,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           const uint32_t nv = min((uint32_t)SPW, len - q0);
           if (nv == (uint32_t)SPW && h4 == 0) {
             const short2 kk = S.kt[g];
-            word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4), lutz_of(m4));
+            word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4));
           } else {
 #pragma unroll
             for (int j = 0; j < SPW; ++j) {
@@ -570,7 +566,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           if (nv == (uint32_t)SPW && h4 == 0) {
             int32_t K0, K1;
             consts(sym_in_word<T>(x, 0) >> nsh, K0, K1);
-            word_one_segment(x, q0, R, m4, K0, K1, lut_of(m4), lutz_of(m4));
+            word_one_segment(x, q0, R, m4, K0, K1, lut_of(m4));
           } else {
 #pragma unroll
             for (int j = 0; j < SPW; ++j) {
