@@ -61,7 +61,7 @@ struct LvTile {
   static constexpr int BUF = TILE + 2 * MARGIN;  // ring buffer (symbols)
   static constexpr int NB = 4;                   // ring buffers per warp
   static constexpr int MINB = 20;                // warps (CTAs) per SM the register budget is sized for
-  static constexpr int MAXSEG = 64;              // segment table capacity (else global node tables)
+  static constexpr int MAXSEG = W == 1 ? 32 : 64;  // segment table capacity (else global node tables)
   static_assert(TILE % 512 == 0, "tiles hold whole superblocks");
   static_assert(NH == 1 || NH == 2, "mask halves");
 };
@@ -70,10 +70,11 @@ template <typename T>
 struct LevelSmem {
   using C = LvTile<T>;
   alignas(128) T buf[C::NB][C::BUF];  // ring: input tiles land at buf[b][MARGIN], outputs are staged
-  uint4 own[C::NH][32];               // per lane and mask half: {bits, ones | heads << 16 before, head bits, -}
+  uint4 own[C::NH][32];               // per lane and mask half: {bits, ones before, head bits, heads before}
   uint16_t seg_a[C::MAXSEG + 1];      // segment g starts at tile position seg_a[g] (g >= 1)
   uint16_t seg_R[C::MAXSEG + 1];      // tile-local ones before seg_a[g]
-  short2 kt[C::MAXSEG];               // segment g: stage offsets {K0, K1} relative to the output buffer
+  uint2 kt[C::MAXSEG];                // segment g: shared-memory byte addresses {Z0, O0}: a zero at q with
+                                      // R ones before it goes to Z0 + (q - R) W, a one to O0 + R W
   uint4 lut[16];                      // in-word stable partition: {selector | nz << 16, z1, z2, z3},
                                       // z_k = 1 if slot k of the partitioned word is a zero
   int32_t s1, am, Rs1, Ram;           // first-segment end, last-segment start, ranks there
@@ -206,12 +207,15 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       }
     }
     uint32_t vF = 0, vL = 0;
+    uint2 tabF = make_uint2(0, 0), tabL = make_uint2(0, 0);
     uint32_t hm[NH];
 #pragma unroll
     for (int h = 0; h < NH; ++h) hm[h] = 0;
     if (SCATTER) {
       vF = (uint32_t)B[0] >> nsh;
       vL = (uint32_t)B[len - 1] >> nsh;
+      tabF = __ldg(&tab[vF]);  // issued early: at deep levels these miss L1
+      tabL = __ldg(&tab[vL]);
       if (vF != vL) {  // warp-uniform: segment heads (positions q > 0 whose node differs from q-1's)
         uint32_t prev = lane ? ((uint32_t)B[i0 - 1] >> nsh) : vF;
 #pragma unroll
@@ -241,11 +245,12 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     }
 
     {
-      uint32_t p = prep;
+      uint32_t po = mypre, ph = hpre;
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
-        S.own[h][lane] = make_uint4(m[h], p, hm[h], 0u);
-        p += ((uint32_t)__popc(hm[h]) << 16) | (uint32_t)__popc(m[h]);
+        S.own[h][lane] = make_uint4(m[h], po, hm[h], ph);
+        po += (uint32_t)__popc(m[h]);
+        ph += (uint32_t)__popc(hm[h]);
       }
     }
     {  // segment table: start and rank of every segment g >= 1
@@ -274,7 +279,6 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         }
       }
     }
-    const uint2 tabF = __ldg(&tab[vF]), tabL = __ldg(&tab[vL]);
     __syncwarp();  // own[], segment table
 
     // ---------------- constants of the tile's regions (every lane; lane r keeps region r)
@@ -302,14 +306,18 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     // symbols of side region r with rank < ksplit_r land in destination tile
     // floor(D_r / TILE), the rest in the next tile
     auto ksplit = [&](uint32_t D, int32_t l) { return min(l, (int32_t)(TILE - D % TILE)); };
-    if (segtab) {
-      if (lane == 0) S.kt[0] = make_short2((short)K0F, (short)K1F);
-      if (lane == 1 && !one) S.kt[nseg - 1] = make_short2((short)K0L, (short)K1L);
+    // stage offsets (symbols, relative to the output buffer) -> shared-memory byte addresses
+    const int32_t sbuf = (int32_t)(smem_u32(S.buf[ob]) / (uint32_t)sizeof(T));
+    auto sa = [&](int32_t K) { return (uint32_t)(sbuf + K) * (uint32_t)sizeof(T); };
+    if (segtab && !one) {
+      if (lane == 0) S.kt[0] = make_uint2(sa(K0F), sa(K1F));
+      if (lane == 1) S.kt[nseg - 1] = make_uint2(sa(K0L), sa(K1L));
       // interior segment g (1 <= g <= nseg-2) lies wholly inside the tile: its
       // stage positions are its own positions, zeros first then ones:
       //   b = 0: q - R(q) + R(a_g) + MARGIN     b = 1: R(q) + a_{g+1} - R(a_{g+1}) + MARGIN
       for (uint32_t g = lane + 1; g + 1 < nseg; g += 32)
-        S.kt[g] = make_short2((short)(S.seg_R[g] + MARGIN), (short)(S.seg_a[g + 1] - S.seg_R[g + 1] + MARGIN));
+        S.kt[g] = make_uint2(sa((int32_t)S.seg_R[g] + MARGIN),
+                             sa((int32_t)S.seg_a[g + 1] - (int32_t)S.seg_R[g + 1] + MARGIN));
     }
 
     // ---------------- next-level ones per (region, destination tile), lane-owned symbols
@@ -450,7 +458,6 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     // ---------------- phase D: every symbol from the input buffer to its stage position
 #ifndef WT_EXP_SKIP_D
     {
-      const int32_t sbuf = (int32_t)(smem_u32(S.buf[ob]) / (uint32_t)sizeof(T));  // in symbols
       const uint32_t* Win = reinterpret_cast<const uint32_t*>(B);
       // word w = lane + 32 k is owned by phase-A lane w / XW, at symbol offset
       // (w % XW) * SPW = (lane % XW) * SPW of that lane: mask half hh, bit sub
@@ -462,21 +469,20 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         return SPW == 1 ? make_uint4(0, 0, 0, 0) : S.lut[m4 & ((1u << SPW) - 1u)];
       };
       // stores the SPW symbols of word x (tile position q0, R ones before it,
-      // bits m4, in-word partition e) into segment (K0, K1) (stage offsets
-      // relative to the buffer).  Slot k of the partitioned word y goes to
+      // bits m4, in-word partition e) into the segment with byte addresses
+      // (Z0, O0) (kt[]).  Slot k of the partitioned word y goes to
       // Ao + k + z_k (Az - Ao): the slot choice is a multiply-add (FMA pipe)
       // and the symbol extraction a multiply-high, keeping the ALU pipe free.
-      auto word_one_segment = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, int32_t K0, int32_t K1,
+      auto word_one_segment = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, uint32_t Z0, uint32_t O0,
                                   uint4 e) {
         if constexpr (SPW == 1) {
-          const int32_t az = sbuf + (int32_t)(q0 - R) + K0;
-          st_shared<T>((uint32_t)((m4 & 1u) ? sbuf + (int32_t)R + K1 : az) * (uint32_t)sizeof(T), x);
+          st_shared<T>((m4 & 1u) ? O0 + R * (uint32_t)sizeof(T) : Z0 + (q0 - R) * (uint32_t)sizeof(T), x);
         } else {
           uint32_t y;
           asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(x), "r"(e.x));  // selector = e.x[15:0]
-          const int32_t nz = (int32_t)(e.x >> 16);
-          const uint32_t Az = (uint32_t)(sbuf + (int32_t)(q0 - R) + K0) * (uint32_t)sizeof(T);
-          const uint32_t Ao = (uint32_t)(sbuf + (int32_t)R + K1 - nz) * (uint32_t)sizeof(T);
+          const uint32_t nz = e.x >> 16;
+          const uint32_t Az = Z0 + (q0 - R) * (uint32_t)sizeof(T);
+          const uint32_t Ao = O0 + (R - nz) * (uint32_t)sizeof(T);
           const uint32_t d = Az - Ao;
           st_shared<T, 0>(nz ? Az : Ao, y);
           st_shared<T, sizeof(T)>(Ao + e.y * d, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
@@ -486,7 +492,21 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           }
         }
       };
+      // the symbols of a word that spans segments (or the tile end), one by one
+      auto word_split = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, uint32_t h4, uint32_t nv, auto zo) {
+#pragma unroll
+        for (int j = 0; j < SPW; ++j) {
+          if ((uint32_t)j < nv) {
+            const uint32_t sym = sym_in_word<T>(x, j);
+            const uint2 k = zo(j, sym, h4);
+            const uint32_t Rj = R + (uint32_t)__popc(m4 & lowmask(j));
+            st_shared<T>(((m4 >> j) & 1u) ? k.y + Rj * (uint32_t)sizeof(T) : k.x + (q0 + j - Rj) * (uint32_t)sizeof(T),
+                         sym);
+          }
+        }
+      };
       if (one && len == (uint32_t)TILE) {  // warp-uniform: one segment, full tile
+        const uint32_t Z0 = sa(K0F), O0 = sa(K1F);
         // batches of BK words: the batch's shared loads first (independent), then its stores
         constexpr int BK = 4;
 #pragma unroll
@@ -498,59 +518,47 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
             const uint32_t w = lane + 32 * (k0 + k);
             const uint2 ow = *reinterpret_cast<const uint2*>(&own[w / XW]);
             xs[k] = Win[w];
-            Rs[k] = ow.y + (uint32_t)__popc(ow.x & submask);  // one segment: no head count in ow.y
+            Rs[k] = ow.y + (uint32_t)__popc(ow.x & submask);
             ms[k] = ow.x >> sub;
           }
 #pragma unroll
           for (int k = 0; k < BK; ++k) es[k] = lut_of(ms[k]);
 #pragma unroll
           for (int k = 0; k < BK; ++k)
-            word_one_segment(xs[k], (lane + 32 * (k0 + k)) * SPW, Rs[k], ms[k], K0F, K1F, es[k]);
+            word_one_segment(xs[k], (lane + 32 * (k0 + k)) * SPW, Rs[k], ms[k], Z0, O0, es[k]);
         }
-      } else if (segtab) {  // segment table in shared memory
+      } else if (one || segtab) {  // segment table in shared memory (or one segment, partial tile)
+        const uint2 kF = make_uint2(sa(K0F), sa(K1F));
+        const bool full = len == (uint32_t)TILE;
 #pragma unroll
         for (int k = 0; k < XW; ++k) {
           const uint32_t w = lane + 32 * k;
           const uint32_t q0 = w * SPW;
-          if (q0 >= len) break;
+          if (!full && q0 >= len) break;
           const uint4 ow = own[w / XW];
-          const uint32_t R = (ow.y & 0xffffu) + (uint32_t)__popc(ow.x & submask);
-          uint32_t g = (ow.y >> 16) + (uint32_t)__popc(ow.z & subhead);  // segment of the word's first symbol
+          const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
+          uint32_t g = ow.w + (uint32_t)__popc(ow.z & subhead);  // segment of the word's first symbol
           const uint32_t m4 = ow.x >> sub;
-          const uint32_t h4 = (ow.z >> sub) & ((1u << SPW) - 2u);         // heads inside the word
+          const uint32_t h4 = SPW == 1 ? 0u : (ow.z >> sub) & ((1u << SPW) - 2u);  // heads inside the word
           const uint32_t x = Win[w];
-          const uint32_t nv = min((uint32_t)SPW, len - q0);
+          const uint32_t nv = full ? (uint32_t)SPW : min((uint32_t)SPW, len - q0);
           if (nv == (uint32_t)SPW && h4 == 0) {
-            const short2 kk = S.kt[g];
+            const uint2 kk = one ? kF : S.kt[g];
             word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4));
           } else {
-#pragma unroll
-            for (int j = 0; j < SPW; ++j) {
-              if ((uint32_t)j < nv) {
-                g += (h4 >> j) & 1u;
-                const short2 kk = S.kt[g];
-                const uint32_t Rj = R + (uint32_t)__popc(m4 & lowmask(j));
-                const uint32_t b = (m4 >> j) & 1u;
-                st_shared<T>((uint32_t)(sbuf + (b ? (int32_t)Rj + kk.y : (int32_t)(q0 + j - Rj) + kk.x)) *
-                                 (uint32_t)sizeof(T),
-                             sym_in_word<T>(x, j));
-              }
-            }
+            word_split(x, q0, R, m4, h4, nv, [&](int j, uint32_t, uint32_t h) {
+              g += (h >> j) & 1u;
+              return one ? kF : S.kt[g];
+            });
           }
         }
       } else {  // too many segments for the table: node tables from global memory
-        auto consts = [&](uint32_t v, int32_t& K0, int32_t& K1) {
-          if (v == vF) {
-            K0 = K0F;
-            K1 = K1F;
-          } else if (v == vL) {
-            K0 = K0L;
-            K1 = K1L;
-          } else {  // interior node: stage position = HBM destination - T0 + MARGIN
-            const uint2 t = __ldg(&tab[v]);
-            K0 = (int32_t)(t.x - P) + MARGIN;
-            K1 = (int32_t)(t.y + P - T0) + MARGIN;
-          }
+        auto consts = [&](uint32_t v) -> uint2 {
+          if (v == vF) return make_uint2(sa(K0F), sa(K1F));
+          if (v == vL) return make_uint2(sa(K0L), sa(K1L));
+          // interior node: stage position = HBM destination - T0 + MARGIN
+          const uint2 t = __ldg(&tab[v]);
+          return make_uint2(sa((int32_t)(t.x - P) + MARGIN), sa((int32_t)(t.y + P - T0) + MARGIN));
         };
 #pragma unroll
         for (int k = 0; k < XW; ++k) {
@@ -558,29 +566,16 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           const uint32_t q0 = w * SPW;
           if (q0 >= len) break;
           const uint4 ow = own[w / XW];
-          const uint32_t R = (ow.y & 0xffffu) + (uint32_t)__popc(ow.x & submask);
+          const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
           const uint32_t m4 = ow.x >> sub;
-          const uint32_t h4 = (ow.z >> sub) & ((1u << SPW) - 2u);
+          const uint32_t h4 = SPW == 1 ? 0u : (ow.z >> sub) & ((1u << SPW) - 2u);
           const uint32_t x = Win[w];
           const uint32_t nv = min((uint32_t)SPW, len - q0);
           if (nv == (uint32_t)SPW && h4 == 0) {
-            int32_t K0, K1;
-            consts(sym_in_word<T>(x, 0) >> nsh, K0, K1);
-            word_one_segment(x, q0, R, m4, K0, K1, lut_of(m4));
+            const uint2 kk = consts(sym_in_word<T>(x, 0) >> nsh);
+            word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4));
           } else {
-#pragma unroll
-            for (int j = 0; j < SPW; ++j) {
-              if ((uint32_t)j < nv) {
-                const uint32_t sym = sym_in_word<T>(x, j);
-                int32_t K0, K1;
-                consts(sym >> nsh, K0, K1);
-                const uint32_t Rj = R + (uint32_t)__popc(m4 & lowmask(j));
-                const uint32_t b = (m4 >> j) & 1u;
-                st_shared<T>((uint32_t)(sbuf + (b ? (int32_t)Rj + K1 : (int32_t)(q0 + j - Rj) + K0)) *
-                                 (uint32_t)sizeof(T),
-                             sym);
-              }
-            }
+            word_split(x, q0, R, m4, h4, nv, [&](int, uint32_t sym, uint32_t) { return consts(sym >> nsh); });
           }
         }
       }
