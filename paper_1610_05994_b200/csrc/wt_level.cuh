@@ -244,269 +244,110 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       continue;
     }
 
-    {
-      uint32_t po = mypre, ph = hpre;
-#pragma unroll
-      for (int h = 0; h < NH; ++h) {
-        S.own[h][lane] = make_uint4(m[h], po, hm[h], ph);
-        po += (uint32_t)__popc(m[h]);
-        ph += (uint32_t)__popc(hm[h]);
-      }
-    }
-    {  // segment table: start and rank of every segment g >= 1
-      uint32_t g = hpre + 1;
-#pragma unroll
-      for (int h = 0; h < NH; ++h) {
-        uint32_t hh = hm[h];
-        while (hh) {
-          const uint32_t k = 32 * h + (uint32_t)(__ffs(hh) - 1);
-          hh &= hh - 1;
-          uint32_t Rk = mypre + (uint32_t)__popc(m[h] & lowmask(k % 32));
-          if (h == 1) Rk += (uint32_t)__popc(m[0]);
-          if (g <= (uint32_t)Cfg::MAXSEG) {
-            S.seg_a[g] = (uint16_t)(i0 + k);
-            S.seg_R[g] = (uint16_t)Rk;
-          }
-          if (g == 1) {
-            S.s1 = (int32_t)(i0 + k);
-            S.Rs1 = (int32_t)Rk;
-          }
-          if (g == nseg - 1) {
-            S.am = (int32_t)(i0 + k);
-            S.Ram = (int32_t)Rk;
-          }
-          ++g;
-        }
-      }
-    }
-    __syncwarp();  // own[], segment table
-
-    // ---------------- constants of the tile's regions (every lane; lane r keeps region r)
-    const bool segtab = nseg <= (uint32_t)Cfg::MAXSEG;  // warp-uniform
-    const bool one = (nseg == 1);
-    const int32_t s1 = one ? (int32_t)len : S.s1, am = one ? (int32_t)len : S.am;
-    const int32_t Rs1 = one ? (int32_t)tot : S.Rs1, Ram = one ? (int32_t)tot : S.Ram;
-    const int32_t z0 = s1 - Rs1, o0 = Rs1;
-    const int32_t om = (int32_t)tot - Ram, zm = ((int32_t)len - am) - om;
-    // HBM destinations (mod 2^32 arithmetic; the results are positions < n)
-    const uint32_t D0z = T0 - P + tabF.x;
-    const uint32_t D0o = P + tabF.y;
-    const uint32_t Dmz = T0 + (uint32_t)am - P - (uint32_t)Ram + tabL.x;
-    const uint32_t Dmo = P + (uint32_t)Ram + tabL.y;
-    auto rup = [](int32_t x) { return (x + A - 1) / A * A; };
-    const int32_t b1 = (int32_t)(D0z & (A - 1));
-    const int32_t b2 = rup(b1 + z0) + (int32_t)(D0o & (A - 1));
-    const int32_t b3 = rup(MARGIN + am) + (int32_t)(Dmz & (A - 1));
-    const int32_t b4 = rup(b3 + zm) + (int32_t)(Dmo & (A - 1));
-    const int32_t K0F = b1, K1F = b2, K0L = b3 - am + Ram, K1L = b4 - Ram;
-    // the five regions (warp-uniform): identity, first zeros, first ones, last zeros, last ones
-    const int32_t rb[LV_NREG] = {MARGIN + s1, b1, b2, b3, b4};
-    const int32_t rl[LV_NREG] = {am - s1, z0, o0, zm, om};
-    const uint32_t rD[LV_NREG] = {T0 + (uint32_t)s1, D0z, D0o, Dmz, Dmo};  // HBM destination of rb[r]
-    // symbols of side region r with rank < ksplit_r land in destination tile
-    // floor(D_r / TILE), the rest in the next tile
-    auto ksplit = [&](uint32_t D, int32_t l) { return min(l, (int32_t)(TILE - D % TILE)); };
     // stage offsets (symbols, relative to the output buffer) -> shared-memory byte addresses
     const int32_t sbuf = (int32_t)(smem_u32(S.buf[ob]) / (uint32_t)sizeof(T));
     auto sa = [&](int32_t K) { return (uint32_t)(sbuf + K) * (uint32_t)sizeof(T); };
-    if (segtab && !one) {
-      if (lane == 0) S.kt[0] = make_uint2(sa(K0F), sa(K1F));
-      if (lane == 1) S.kt[nseg - 1] = make_uint2(sa(K0L), sa(K1L));
-      // interior segment g (1 <= g <= nseg-2) lies wholly inside the tile: its
-      // stage positions are its own positions, zeros first then ones:
-      //   b = 0: q - R(q) + R(a_g) + MARGIN     b = 1: R(q) + a_{g+1} - R(a_{g+1}) + MARGIN
-      for (uint32_t g = lane + 1; g + 1 < nseg; g += 32)
-        S.kt[g] = make_uint2(sa((int32_t)S.seg_R[g] + MARGIN),
-                             sa((int32_t)S.seg_a[g + 1] - (int32_t)S.seg_R[g + 1] + MARGIN));
-    }
-
-    // ---------------- next-level ones per (region, destination tile), lane-owned symbols
-    uint32_t mycnt = 0;  // lane k < LV_NKEY: count of key k = 2 r + half
-#ifndef WT_EXP_SKIP_COUNT
-    {
-      // count of nbm bits among the set bits of M, split at rank k (the set
-      // bits of M have ranks rank0, rank0+1, ... in position order).  Only
-      // the lane holding rank k searches for its k-th set bit.
-      auto split = [&](const uint32_t(&M)[NH], int32_t rank0, int32_t k, uint32_t& lo, uint32_t& hi) {
-        if constexpr (NH == 2) {
-          const uint64_t M64 = M[0] | ((uint64_t)M[1] << 32), N64 = nbm[0] | ((uint64_t)nbm[1] << 32);
-          const uint32_t tot = (uint32_t)__popcll(N64 & M64);
-          const int32_t nM = __popcll(M64);
-          if (rank0 + nM <= k) lo = tot;
-          else if (rank0 >= k) lo = 0;
-          else {  // lowest (k - rank0) set bits of M
-            const int32_t j = k - rank0;
-            uint32_t p = 0;
-#pragma unroll
-            for (uint32_t st = 32; st; st >>= 1)
-              if (__popcll(M64 & ((1ull << (p + st)) - 1)) <= j) p += st;
-            lo = (uint32_t)__popcll(N64 & M64 & ((1ull << p) - 1));
-          }
-          hi = tot - lo;
-        } else {
-          const uint32_t tot = (uint32_t)__popc(nbm[0] & M[0]);
-          const int32_t nM = __popc(M[0]);
-          if (rank0 + nM <= k) lo = tot;
-          else if (rank0 >= k) lo = 0;
-          else {
-            const int32_t j = k - rank0;
-            uint32_t p = 0;
-#pragma unroll
-            for (uint32_t st = 16; st; st >>= 1)
-              if (__popc(M[0] & ((1u << (p + st)) - 1)) <= j) p += st;
-            lo = (uint32_t)__popc(nbm[0] & M[0] & ((1u << p) - 1));
-          }
-          hi = tot - lo;
-        }
-      };
-      auto put2 = [&](int key, uint32_t lo, uint32_t hi) {  // keys (key, key+1) in one reduction
-        const uint32_t sum = __reduce_add_sync(FULL, lo | (hi << 16));
-        if (lane == (uint32_t)key) mycnt = sum & 0xffffu;
-        if (lane == (uint32_t)key + 1) mycnt = sum >> 16;
-      };
-      uint32_t M[NH], lo, hi;
-      if (one) {  // warp-uniform: one segment, only the first-segment runs
-#pragma unroll
-        for (int h = 0; h < NH; ++h) M[h] = vm[h] & ~m[h];
-        split(M, (int32_t)(i0 - mypre), ksplit(D0z, z0), lo, hi);
-        put2(2, lo, hi);
-        split(m, (int32_t)mypre, ksplit(D0o, o0), lo, hi);
-        put2(4, lo, hi);
+    // symbols of a side region with rank < ksplit land in destination tile
+    // floor(D / TILE), the rest in the next tile
+    auto ksplit = [&](uint32_t D, int32_t l) { return min(l, (int32_t)(TILE - D % TILE)); };
+    // ---------------- phase D helpers
+    const uint32_t* Win = reinterpret_cast<const uint32_t*>(B);
+    // word w = lane + 32 k is owned by phase-A lane w / XW, at symbol offset
+    // (w % XW) * SPW = (lane % XW) * SPW of that lane: mask half hh, bit sub
+    const uint32_t soff = (lane % (uint32_t)XW) * SPW;
+    const uint32_t hh = soff / 32, sub = soff % 32;
+    const uint32_t submask = lowmask(sub), subhead = lowmask(sub + 1);
+    const uint4* own = S.own[NH == 1 ? 0 : hh];
+    auto lut_of = [&](uint32_t m4) -> uint4 {
+      return SPW == 1 ? make_uint4(0, 0, 0, 0) : S.lut[m4 & ((1u << SPW) - 1u)];
+    };
+    // stores the SPW symbols of word x (tile position q0, R ones before it,
+    // bits m4, in-word partition e) into the segment with byte addresses
+    // (Z0, O0) (kt[]).  Slot k of the partitioned word y goes to
+    // Ao + k + z_k (Az - Ao): the slot choice is a multiply-add (FMA pipe)
+    // and the symbol extraction a multiply-high, keeping the ALU pipe free.
+    auto word_one_segment = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, uint32_t Z0, uint32_t O0,
+                                uint4 e) {
+      if constexpr (SPW == 1) {
+        st_shared<T>((m4 & 1u) ? O0 + R * (uint32_t)sizeof(T) : Z0 + (q0 - R) * (uint32_t)sizeof(T), x);
       } else {
-        uint32_t fm[NH], lm[NH];
+        uint32_t y;
+        asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(x), "r"(e.x));  // selector = e.x[15:0]
+        const uint32_t nz = e.x >> 16;
+        const uint32_t Az = Z0 + (q0 - R) * (uint32_t)sizeof(T);
+        const uint32_t Ao = O0 + (R - nz) * (uint32_t)sizeof(T);
+        const uint32_t d = Az - Ao;
+        st_shared<T, 0>(nz ? Az : Ao, y);
+        st_shared<T, sizeof(T)>(Ao + e.y * d, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
+        if constexpr (SPW > 2) {
+          st_shared<T, 2>(Ao + e.z * d, __umulhi(y, 1u << 16));
+          st_shared<T, 3>(Ao + e.w * d, __umulhi(y, 1u << 8));
+        }
+      }
+    };
+    // the symbols of a word that spans segments (or the tile end), one by one
+    auto word_split = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, uint32_t h4, uint32_t nv, auto zo) {
+#pragma unroll
+      for (int j = 0; j < SPW; ++j) {
+        if ((uint32_t)j < nv) {
+          const uint32_t sym = sym_in_word<T>(x, j);
+          const uint2 k = zo(j, sym, h4);
+          const uint32_t Rj = R + (uint32_t)__popc(m4 & lowmask(j));
+          st_shared<T>(((m4 >> j) & 1u) ? k.y + Rj * (uint32_t)sizeof(T) : k.x + (q0 + j - Rj) * (uint32_t)sizeof(T),
+                       sym);
+        }
+      }
+    };
+
+    if (nseg == 1) {
+      // ================= one segment: the whole tile lies in node vF.  Zeros
+      // go to D0z.., ones to D0o..; staged at b1 / b2 (congruent mod 16 B)
+      {
+        uint32_t po = mypre;
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
-          fm[h] = lowmask((uint32_t)min(max(s1 - (int32_t)i0 - 32 * h, 0), 32)) & vm[h];
-          lm[h] = vm[h] & ~lowmask((uint32_t)min(max(am - (int32_t)i0 - 32 * h, 0), 32));
+          *reinterpret_cast<uint2*>(&S.own[h][lane]) = make_uint2(m[h], po);
+          po += (uint32_t)__popc(m[h]);
         }
-        uint32_t c0 = 0;
-#pragma unroll
-        for (int h = 0; h < NH; ++h) c0 += (uint32_t)__popc(nbm[h] & vm[h] & ~fm[h] & ~lm[h]);
-        put2(0, c0, 0u);
-#pragma unroll
-        for (int h = 0; h < NH; ++h) M[h] = fm[h] & ~m[h];
-        split(M, (int32_t)(i0 - mypre), ksplit(D0z, z0), lo, hi);
-        put2(2, lo, hi);
-#pragma unroll
-        for (int h = 0; h < NH; ++h) M[h] = fm[h] & m[h];
-        split(M, (int32_t)mypre, ksplit(D0o, o0), lo, hi);
-        put2(4, lo, hi);
-        const int32_t qs = max((int32_t)i0, am);
-        const int32_t Rq = ((int32_t)i0 < am) ? Ram : (int32_t)mypre;  // tile-local ones before qs
-#pragma unroll
-        for (int h = 0; h < NH; ++h) M[h] = lm[h] & ~m[h];
-        split(M, (qs - am) - (Rq - Ram), ksplit(Dmz, zm), lo, hi);
-        put2(6, lo, hi);
-#pragma unroll
-        for (int h = 0; h < NH; ++h) M[h] = lm[h] & m[h];
-        split(M, Rq - Ram, ksplit(Dmo, om), lo, hi);
-        put2(8, lo, hi);
       }
-    }
-#endif
-    // ---------------- progressive counting: level-(l+2) node sizes, i.e. the
-    // symbols of each level-l node by their (level-l, level-(l+1)) bit pair
+      const uint32_t z0 = len - tot, o0 = tot;
+      const uint32_t D0z = T0 - P + tabF.x, D0o = P + tabF.y;  // (mod 2^32; positions < n)
+      const uint32_t b1 = D0z & (A - 1);
+      const uint32_t b2 = ((b1 + z0 + A - 1) & ~(uint32_t)(A - 1)) + (D0o & (A - 1));
+      const uint32_t Z0 = sa((int32_t)b1), O0 = sa((int32_t)b2);
+      // next level's ones among the zeros / the ones, and the part of each
+      // run below its destination tile boundary (ranks < kz / ko): lanes
+      // wholly below count here, the one lane straddling the boundary counts
+      // its part in the stage after phase D (window below)
+      const uint32_t kz = (uint32_t)ksplit(D0z, (int32_t)z0), ko = (uint32_t)ksplit(D0o, (int32_t)o0);
+      uint32_t nol = 0, tbz = 0, tbo = 0;
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        nol += (uint32_t)__popc(m[h]);
+        tbz += (uint32_t)__popc(nbm[h] & ~m[h]);
+        tbo += (uint32_t)__popc(nbm[h] & m[h]);
+      }
+      const uint32_t nzl = nvalid - nol, rz = i0 - mypre, ro = mypre;
+      const uint32_t redz = __reduce_add_sync(FULL, ((rz + nzl <= kz) ? tbz : 0u) | (tbz << 16));
+      const uint32_t redo = __reduce_add_sync(FULL, ((ro + nol <= ko) ? tbo : 0u) | (tbo << 16));
+      const uint32_t c01 = redz >> 16, c11 = redo >> 16;
+      uint32_t Lz = redz & 0xffffu, Lo = redo & 0xffffu;
+      const uint32_t splz = __ballot_sync(FULL, rz < kz && rz + nzl > kz);
+      const uint32_t splo = __ballot_sync(FULL, ro < ko && ro + nol > ko);
+      const uint32_t sz0 = __shfl_sync(FULL, rz, (__ffs(splz) - 1) & 31);
+      const uint32_t so0 = __shfl_sync(FULL, ro, (__ffs(splo) - 1) & 31);
 #ifndef WT_EXP_SKIP_PCOUNT
-    if (one) {  // warp-uniform: all symbols in node vF.  The (b, nb) pair counts
-      // follow from the next-level ones already reduced above (keys 2..5: nb
-      // ones among the zeros / the ones, split by destination tile)
-      const uint32_t c01 = __shfl_sync(FULL, mycnt, 2) + __shfl_sync(FULL, mycnt, 3);
-      const uint32_t c11 = __shfl_sync(FULL, mycnt, 4) + __shfl_sync(FULL, mycnt, 5);
+      // progressive counting: the (b, nb) pair counts of node vF are the run
+      // sizes and their next-level ones
       if (vF != cc_node) {
         cc_flush();
         cc_node = vF;
       }
-      cc_acc += lane == 0 ? (len - tot) - c01 : lane == 1 ? c01 : lane == 2 ? tot - c11 : c11;
-    } else if (nvalid) {  // the lane's pieces: maximal runs of its symbols inside one node
-      // (two node counts per 64-bit atomic: each stays < 2^32, no carry)
-      auto piece = [&](uint32_t node, uint32_t c00, uint32_t c01, uint32_t c10, uint32_t c11) {
-        unsigned long long* dst = reinterpret_cast<unsigned long long*>(cnt_next + 4u * node);
-        const unsigned long long lo = (unsigned long long)c00 | ((unsigned long long)c01 << 32);
-        const unsigned long long hi = (unsigned long long)c10 | ((unsigned long long)c11 << 32);
-        if (lo) atomicAdd(dst, lo);
-        if (hi) atomicAdd(dst + 1, hi);
-      };
-      if constexpr (NH == 2) {
-        const uint64_t M = m[0] | ((uint64_t)m[1] << 32), NB = nbm[0] | ((uint64_t)nbm[1] << 32);
-        const uint64_t V = vm[0] | ((uint64_t)vm[1] << 32), H = hm[0] | ((uint64_t)hm[1] << 32);
-        uint64_t starts = (H | 1ull) & V;
-        while (starts) {
-          const int p = __ffsll((long long)starts) - 1;
-          starts &= starts - 1;
-          const int pend = starts ? __ffsll((long long)starts) - 1 : 64;
-          const uint64_t pm = V & ((pend >= 64 ? ~0ull : ((1ull << pend) - 1)) & ~((1ull << p) - 1));
-          const uint64_t z = pm & ~M, o = pm & M;
-          piece((uint32_t)B[i0 + p] >> nsh, __popcll(z & ~NB), __popcll(z & NB), __popcll(o & ~NB),
-                __popcll(o & NB));
-        }
-      } else {
-        const uint32_t M = m[0], NB = nbm[0], V = vm[0];
-        uint32_t starts = (hm[0] | 1u) & V;
-        while (starts) {
-          const int p = __ffs(starts) - 1;
-          starts &= starts - 1;
-          const int pend = starts ? __ffs(starts) - 1 : 32;
-          const uint32_t pm = V & lowmask((uint32_t)pend) & ~((1u << p) - 1u);
-          const uint32_t z = pm & ~M, o = pm & M;
-          piece((uint32_t)B[i0 + p] >> nsh, __popc(z & ~NB), __popc(z & NB), __popc(o & ~NB), __popc(o & NB));
-        }
-      }
-    }
+      cc_acc += lane == 0 ? z0 - c01 : lane == 1 ? c01 : lane == 2 ? o0 - c11 : lane == 3 ? c11 : 0u;
 #endif
-    if (segtab && !one) __syncwarp();  // kt[]
-
-    // ---------------- phase D: every symbol from the input buffer to its stage position
+      __syncwarp();  // own[]
 #ifndef WT_EXP_SKIP_D
-    {
-      const uint32_t* Win = reinterpret_cast<const uint32_t*>(B);
-      // word w = lane + 32 k is owned by phase-A lane w / XW, at symbol offset
-      // (w % XW) * SPW = (lane % XW) * SPW of that lane: mask half hh, bit sub
-      const uint32_t soff = (lane % (uint32_t)XW) * SPW;
-      const uint32_t hh = soff / 32, sub = soff % 32;
-      const uint32_t submask = lowmask(sub), subhead = lowmask(sub + 1);
-      const uint4* own = S.own[NH == 1 ? 0 : hh];
-      auto lut_of = [&](uint32_t m4) -> uint4 {
-        return SPW == 1 ? make_uint4(0, 0, 0, 0) : S.lut[m4 & ((1u << SPW) - 1u)];
-      };
-      // stores the SPW symbols of word x (tile position q0, R ones before it,
-      // bits m4, in-word partition e) into the segment with byte addresses
-      // (Z0, O0) (kt[]).  Slot k of the partitioned word y goes to
-      // Ao + k + z_k (Az - Ao): the slot choice is a multiply-add (FMA pipe)
-      // and the symbol extraction a multiply-high, keeping the ALU pipe free.
-      auto word_one_segment = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, uint32_t Z0, uint32_t O0,
-                                  uint4 e) {
-        if constexpr (SPW == 1) {
-          st_shared<T>((m4 & 1u) ? O0 + R * (uint32_t)sizeof(T) : Z0 + (q0 - R) * (uint32_t)sizeof(T), x);
-        } else {
-          uint32_t y;
-          asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(x), "r"(e.x));  // selector = e.x[15:0]
-          const uint32_t nz = e.x >> 16;
-          const uint32_t Az = Z0 + (q0 - R) * (uint32_t)sizeof(T);
-          const uint32_t Ao = O0 + (R - nz) * (uint32_t)sizeof(T);
-          const uint32_t d = Az - Ao;
-          st_shared<T, 0>(nz ? Az : Ao, y);
-          st_shared<T, sizeof(T)>(Ao + e.y * d, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
-          if constexpr (SPW > 2) {
-            st_shared<T, 2>(Ao + e.z * d, __umulhi(y, 1u << 16));
-            st_shared<T, 3>(Ao + e.w * d, __umulhi(y, 1u << 8));
-          }
-        }
-      };
-      // the symbols of a word that spans segments (or the tile end), one by one
-      auto word_split = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, uint32_t h4, uint32_t nv, auto zo) {
-#pragma unroll
-        for (int j = 0; j < SPW; ++j) {
-          if ((uint32_t)j < nv) {
-            const uint32_t sym = sym_in_word<T>(x, j);
-            const uint2 k = zo(j, sym, h4);
-            const uint32_t Rj = R + (uint32_t)__popc(m4 & lowmask(j));
-            st_shared<T>(((m4 >> j) & 1u) ? k.y + Rj * (uint32_t)sizeof(T) : k.x + (q0 + j - Rj) * (uint32_t)sizeof(T),
-                         sym);
-          }
-        }
-      };
-      if (one && len == (uint32_t)TILE) {  // warp-uniform: one segment, full tile
-        const uint32_t Z0 = sa(K0F), O0 = sa(K1F);
+      if (len == (uint32_t)TILE) {  // warp-uniform: full tile
         // batches of BK words: the batch's shared loads first (independent), then its stores
         constexpr int BK = 4;
 #pragma unroll
@@ -527,126 +368,398 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           for (int k = 0; k < BK; ++k)
             word_one_segment(xs[k], (lane + 32 * (k0 + k)) * SPW, Rs[k], ms[k], Z0, O0, es[k]);
         }
-      } else if (one || segtab) {  // segment table in shared memory (or one segment, partial tile)
-        const uint2 kF = make_uint2(sa(K0F), sa(K1F));
-        const bool full = len == (uint32_t)TILE;
-#pragma unroll
-        for (int k = 0; k < XW; ++k) {
-          const uint32_t w = lane + 32 * k;
-          const uint32_t q0 = w * SPW;
-          if (!full && q0 >= len) break;
-          const uint4 ow = own[w / XW];
-          const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
-          uint32_t g = ow.w + (uint32_t)__popc(ow.z & subhead);  // segment of the word's first symbol
-          const uint32_t m4 = ow.x >> sub;
-          const uint32_t h4 = SPW == 1 ? 0u : (ow.z >> sub) & ((1u << SPW) - 2u);  // heads inside the word
-          const uint32_t x = Win[w];
-          const uint32_t nv = full ? (uint32_t)SPW : min((uint32_t)SPW, len - q0);
-          if (nv == (uint32_t)SPW && h4 == 0) {
-            const uint2 kk = one ? kF : S.kt[g];
-            word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4));
-          } else {
-            word_split(x, q0, R, m4, h4, nv, [&](int j, uint32_t, uint32_t h) {
-              g += (h >> j) & 1u;
-              return one ? kF : S.kt[g];
-            });
-          }
-        }
-      } else {  // too many segments for the table: node tables from global memory
-        auto consts = [&](uint32_t v) -> uint2 {
-          if (v == vF) return make_uint2(sa(K0F), sa(K1F));
-          if (v == vL) return make_uint2(sa(K0L), sa(K1L));
-          // interior node: stage position = HBM destination - T0 + MARGIN
-          const uint2 t = __ldg(&tab[v]);
-          return make_uint2(sa((int32_t)(t.x - P) + MARGIN), sa((int32_t)(t.y + P - T0) + MARGIN));
-        };
+      } else {  // the last, partial tile
+        const uint2 kF = make_uint2(Z0, O0);
 #pragma unroll
         for (int k = 0; k < XW; ++k) {
           const uint32_t w = lane + 32 * k;
           const uint32_t q0 = w * SPW;
           if (q0 >= len) break;
-          const uint4 ow = own[w / XW];
+          const uint2 ow = *reinterpret_cast<const uint2*>(&own[w / XW]);
           const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
           const uint32_t m4 = ow.x >> sub;
-          const uint32_t h4 = SPW == 1 ? 0u : (ow.z >> sub) & ((1u << SPW) - 2u);
           const uint32_t x = Win[w];
           const uint32_t nv = min((uint32_t)SPW, len - q0);
-          if (nv == (uint32_t)SPW && h4 == 0) {
-            const uint2 kk = consts(sym_in_word<T>(x, 0) >> nsh);
-            word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4));
-          } else {
-            word_split(x, q0, R, m4, h4, nv, [&](int, uint32_t sym, uint32_t) { return consts(sym >> nsh); });
+          if (nv == (uint32_t)SPW) word_one_segment(x, q0, R, m4, Z0, O0, lut_of(m4));
+          else word_split(x, q0, R, m4, 0u, nv, [&](int, uint32_t, uint32_t) { return kF; });
+        }
+      }
+#endif
+      fence_proxy_async_smem();
+      __syncwarp();  // stage written (and the input buffer fully read)
+      // the straddling lane's symbols below the boundary: stage positions
+      // [bst + r0, bst + k), fewer than E, their next-level bits counted here
+      auto window = [&](uint32_t bst, uint32_t r0, uint32_t k) {
+        const int32_t lo = (int32_t)(bst + r0), hi = (int32_t)(bst + k);
+        uint32_t c = 0;
+#pragma unroll
+        for (int j = 0; j < (E + 31) / 32; ++j) {
+          const int32_t q = hi - E + 32 * j + (int32_t)lane;
+          const bool in = q >= lo && q < hi;
+          const uint32_t sym = in ? (uint32_t)S.buf[ob][q] : 0u;
+          c += (uint32_t)__popc(__ballot_sync(FULL, (sym >> (sh - 1)) & 1u));
+        }
+        return c;
+      };
+      if (splz) Lz += window(b1, sz0, kz);
+      if (splo) Lo += window(b2, so0, ko);
+      // ---------------- phase E: lanes 0 / 1 bulk-store the two runs' aligned
+      // bodies, the warp stores their edge symbols
+      {
+        const bool r2 = lane == 1;
+        const uint32_t b = r2 ? b2 : b1, l = r2 ? o0 : z0, D = r2 ? D0o : D0z;
+        const uint32_t fs = (b + A - 1) & ~(uint32_t)(A - 1), fe = (b + l) & ~(uint32_t)(A - 1);
+        if (lane < 2 && fe > fs) bulk_s2g(out + (D - b + fs), S.buf[ob] + fs, (fe - fs) * (uint32_t)sizeof(T));
+        if (lane < (uint32_t)LV_NREG) bulk_commit();
+#pragma unroll
+        for (uint32_t base = 0; base < (uint32_t)(4 * A); base += 32) {
+          const uint32_t slot = base + lane, e = slot % (2 * A);
+          const bool s2 = slot >= (uint32_t)(2 * A);
+          const uint32_t bb = s2 ? b2 : b1, end = bb + (s2 ? o0 : z0), DD = s2 ? D0o : D0z;
+          const uint32_t hend = min((bb + A - 1) & ~(uint32_t)(A - 1), end);
+          const uint32_t tst = max(end & ~(uint32_t)(A - 1), hend);
+          const uint32_t q = e < (uint32_t)A ? bb + e : tst + e - A;
+          if (slot < (uint32_t)(4 * A) && (e < (uint32_t)A ? q < hend : q < end)) out[DD - bb + q] = S.buf[ob][q];
+        }
+      }
+      if (lane < 4) {  // next-level ones per destination tile
+        const uint32_t v = lane == 0 ? Lz : lane == 1 ? c01 - Lz : lane == 2 ? Lo : c11 - Lo;
+        if (v) atomicAdd(&agg_next[(lane < 2 ? D0z : D0o) / TILE + (lane & 1)], v);
+      }
+    } else {
+      // ================= several segments
+
+      {
+        uint32_t po = mypre, ph = hpre;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          S.own[h][lane] = make_uint4(m[h], po, hm[h], ph);
+          po += (uint32_t)__popc(m[h]);
+          ph += (uint32_t)__popc(hm[h]);
+        }
+      }
+      {  // segment table: start and rank of every segment g >= 1
+        uint32_t g = hpre + 1;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          uint32_t hh = hm[h];
+          while (hh) {
+            const uint32_t k = 32 * h + (uint32_t)(__ffs(hh) - 1);
+            hh &= hh - 1;
+            uint32_t Rk = mypre + (uint32_t)__popc(m[h] & lowmask(k % 32));
+            if (h == 1) Rk += (uint32_t)__popc(m[0]);
+            if (g <= (uint32_t)Cfg::MAXSEG) {
+              S.seg_a[g] = (uint16_t)(i0 + k);
+              S.seg_R[g] = (uint16_t)Rk;
+            }
+            if (g == 1) {
+              S.s1 = (int32_t)(i0 + k);
+              S.Rs1 = (int32_t)Rk;
+            }
+            if (g == nseg - 1) {
+              S.am = (int32_t)(i0 + k);
+              S.Ram = (int32_t)Rk;
+            }
+            ++g;
           }
         }
       }
-    }
-#endif
-    fence_proxy_async_smem();
-    __syncwarp();  // stage partitioned (and the input buffer fully read)
+      __syncwarp();  // own[], segment table
 
-    // ---------------- phase E: TMA bulk stores of the aligned bodies, element stores of the edges
-    auto emit_region = [&](int32_t b, int32_t l, uint32_t D) {  // stage [b, b+l) -> HBM [D, D+l)
-      if (l <= 0) return;  // warp-uniform
-      const int32_t end = b + l;
-      const int32_t fs = (b + A - 1) / A * A, fe = end / A * A;
-      T* const go = out + D - b;  // HBM address of stage position q: go + q
-      if (lane == 0 && fe > fs) bulk_s2g(go + fs, S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
-      // head edge [b, min(fs, end)) and tail edge [max(fe, that), end), each < A symbols
-      const int32_t hend = min(fs, end), tst = max(fe, hend);
-      const int32_t q = (lane < (uint32_t)A) ? b + (int32_t)lane : tst + (int32_t)lane - A;
-      if (lane < (uint32_t)(2 * A) && ((lane < (uint32_t)A) ? (q < hend) : (q < end))) go[q] = S.buf[ob][q];
-    };
-    if constexpr (sizeof(T) == 1) {  // (A = 16: one region's two edges fill the warp)
-      if (one) {  // warp-uniform: the first segment's two runs only
-        emit_region(b1, z0, D0z);
-        emit_region(b2, o0, D0o);
+      // ---------------- constants of the tile's regions (every lane; lane r keeps region r)
+      const bool segtab = nseg <= (uint32_t)Cfg::MAXSEG;  // warp-uniform
+      constexpr bool one = false;  // (this branch: nseg > 1)
+      const int32_t s1 = one ? (int32_t)len : S.s1, am = one ? (int32_t)len : S.am;
+      const int32_t Rs1 = one ? (int32_t)tot : S.Rs1, Ram = one ? (int32_t)tot : S.Ram;
+      const int32_t z0 = s1 - Rs1, o0 = Rs1;
+      const int32_t om = (int32_t)tot - Ram, zm = ((int32_t)len - am) - om;
+      // HBM destinations (mod 2^32 arithmetic; the results are positions < n)
+      const uint32_t D0z = T0 - P + tabF.x;
+      const uint32_t D0o = P + tabF.y;
+      const uint32_t Dmz = T0 + (uint32_t)am - P - (uint32_t)Ram + tabL.x;
+      const uint32_t Dmo = P + (uint32_t)Ram + tabL.y;
+      auto rup = [](int32_t x) { return (x + A - 1) / A * A; };
+      const int32_t b1 = (int32_t)(D0z & (A - 1));
+      const int32_t b2 = rup(b1 + z0) + (int32_t)(D0o & (A - 1));
+      const int32_t b3 = rup(MARGIN + am) + (int32_t)(Dmz & (A - 1));
+      const int32_t b4 = rup(b3 + zm) + (int32_t)(Dmo & (A - 1));
+      const int32_t K0F = b1, K1F = b2, K0L = b3 - am + Ram, K1L = b4 - Ram;
+      // the five regions (warp-uniform): identity, first zeros, first ones, last zeros, last ones
+      const int32_t rb[LV_NREG] = {MARGIN + s1, b1, b2, b3, b4};
+      const int32_t rl[LV_NREG] = {am - s1, z0, o0, zm, om};
+      const uint32_t rD[LV_NREG] = {T0 + (uint32_t)s1, D0z, D0o, Dmz, Dmo};  // HBM destination of rb[r]
+      // symbols of side region r with rank < ksplit_r land in destination tile
+      // floor(D_r / TILE), the rest in the next tile
+      if (segtab && !one) {
+        if (lane == 0) S.kt[0] = make_uint2(sa(K0F), sa(K1F));
+        if (lane == 1) S.kt[nseg - 1] = make_uint2(sa(K0L), sa(K1L));
+        // interior segment g (1 <= g <= nseg-2) lies wholly inside the tile: its
+        // stage positions are its own positions, zeros first then ones:
+        //   b = 0: q - R(q) + R(a_g) + MARGIN     b = 1: R(q) + a_{g+1} - R(a_{g+1}) + MARGIN
+        for (uint32_t g = lane + 1; g + 1 < nseg; g += 32)
+          S.kt[g] = make_uint2(sa((int32_t)S.seg_R[g] + MARGIN),
+                               sa((int32_t)S.seg_a[g + 1] - (int32_t)S.seg_R[g + 1] + MARGIN));
+      }
+
+      // ---------------- next-level ones per (region, destination tile), lane-owned symbols
+      uint32_t mycnt = 0;  // lane k < LV_NKEY: count of key k = 2 r + half
+#ifndef WT_EXP_SKIP_COUNT
+      {
+        // count of nbm bits among the set bits of M, split at rank k (the set
+        // bits of M have ranks rank0, rank0+1, ... in position order).  Only
+        // the lane holding rank k searches for its k-th set bit.
+        auto split = [&](const uint32_t(&M)[NH], int32_t rank0, int32_t k, uint32_t& lo, uint32_t& hi) {
+          if constexpr (NH == 2) {
+            const uint64_t M64 = M[0] | ((uint64_t)M[1] << 32), N64 = nbm[0] | ((uint64_t)nbm[1] << 32);
+            const uint32_t tot = (uint32_t)__popcll(N64 & M64);
+            const int32_t nM = __popcll(M64);
+            if (rank0 + nM <= k) lo = tot;
+            else if (rank0 >= k) lo = 0;
+            else {  // lowest (k - rank0) set bits of M
+              const int32_t j = k - rank0;
+              uint32_t p = 0;
+#pragma unroll
+              for (uint32_t st = 32; st; st >>= 1)
+                if (__popcll(M64 & ((1ull << (p + st)) - 1)) <= j) p += st;
+              lo = (uint32_t)__popcll(N64 & M64 & ((1ull << p) - 1));
+            }
+            hi = tot - lo;
+          } else {
+            const uint32_t tot = (uint32_t)__popc(nbm[0] & M[0]);
+            const int32_t nM = __popc(M[0]);
+            if (rank0 + nM <= k) lo = tot;
+            else if (rank0 >= k) lo = 0;
+            else {
+              const int32_t j = k - rank0;
+              uint32_t p = 0;
+#pragma unroll
+              for (uint32_t st = 16; st; st >>= 1)
+                if (__popc(M[0] & ((1u << (p + st)) - 1)) <= j) p += st;
+              lo = (uint32_t)__popc(nbm[0] & M[0] & ((1u << p) - 1));
+            }
+            hi = tot - lo;
+          }
+        };
+        auto put2 = [&](int key, uint32_t lo, uint32_t hi) {  // keys (key, key+1) in one reduction
+          const uint32_t sum = __reduce_add_sync(FULL, lo | (hi << 16));
+          if (lane == (uint32_t)key) mycnt = sum & 0xffffu;
+          if (lane == (uint32_t)key + 1) mycnt = sum >> 16;
+        };
+        uint32_t M[NH], lo, hi;
+        if (one) {  // warp-uniform: one segment, only the first-segment runs
+#pragma unroll
+          for (int h = 0; h < NH; ++h) M[h] = vm[h] & ~m[h];
+          split(M, (int32_t)(i0 - mypre), ksplit(D0z, z0), lo, hi);
+          put2(2, lo, hi);
+          split(m, (int32_t)mypre, ksplit(D0o, o0), lo, hi);
+          put2(4, lo, hi);
+        } else {
+          uint32_t fm[NH], lm[NH];
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            fm[h] = lowmask((uint32_t)min(max(s1 - (int32_t)i0 - 32 * h, 0), 32)) & vm[h];
+            lm[h] = vm[h] & ~lowmask((uint32_t)min(max(am - (int32_t)i0 - 32 * h, 0), 32));
+          }
+          uint32_t c0 = 0;
+#pragma unroll
+          for (int h = 0; h < NH; ++h) c0 += (uint32_t)__popc(nbm[h] & vm[h] & ~fm[h] & ~lm[h]);
+          put2(0, c0, 0u);
+#pragma unroll
+          for (int h = 0; h < NH; ++h) M[h] = fm[h] & ~m[h];
+          split(M, (int32_t)(i0 - mypre), ksplit(D0z, z0), lo, hi);
+          put2(2, lo, hi);
+#pragma unroll
+          for (int h = 0; h < NH; ++h) M[h] = fm[h] & m[h];
+          split(M, (int32_t)mypre, ksplit(D0o, o0), lo, hi);
+          put2(4, lo, hi);
+          const int32_t qs = max((int32_t)i0, am);
+          const int32_t Rq = ((int32_t)i0 < am) ? Ram : (int32_t)mypre;  // tile-local ones before qs
+#pragma unroll
+          for (int h = 0; h < NH; ++h) M[h] = lm[h] & ~m[h];
+          split(M, (qs - am) - (Rq - Ram), ksplit(Dmz, zm), lo, hi);
+          put2(6, lo, hi);
+#pragma unroll
+          for (int h = 0; h < NH; ++h) M[h] = lm[h] & m[h];
+          split(M, Rq - Ram, ksplit(Dmo, om), lo, hi);
+          put2(8, lo, hi);
+        }
+      }
+#endif
+      // ---------------- progressive counting: level-(l+2) node sizes, i.e. the
+      // symbols of each level-l node by their (level-l, level-(l+1)) bit pair
+#ifndef WT_EXP_SKIP_PCOUNT
+      if (one) {  // warp-uniform: all symbols in node vF.  The (b, nb) pair counts
+        // follow from the next-level ones already reduced above (keys 2..5: nb
+        // ones among the zeros / the ones, split by destination tile)
+        const uint32_t c01 = __shfl_sync(FULL, mycnt, 2) + __shfl_sync(FULL, mycnt, 3);
+        const uint32_t c11 = __shfl_sync(FULL, mycnt, 4) + __shfl_sync(FULL, mycnt, 5);
+        if (vF != cc_node) {
+          cc_flush();
+          cc_node = vF;
+        }
+        cc_acc += lane == 0 ? (len - tot) - c01 : lane == 1 ? c01 : lane == 2 ? tot - c11 : c11;
+      } else if (nvalid) {  // the lane's pieces: maximal runs of its symbols inside one node
+        // (two node counts per 64-bit atomic: each stays < 2^32, no carry)
+        auto piece = [&](uint32_t node, uint32_t c00, uint32_t c01, uint32_t c10, uint32_t c11) {
+          unsigned long long* dst = reinterpret_cast<unsigned long long*>(cnt_next + 4u * node);
+          const unsigned long long lo = (unsigned long long)c00 | ((unsigned long long)c01 << 32);
+          const unsigned long long hi = (unsigned long long)c10 | ((unsigned long long)c11 << 32);
+          if (lo) atomicAdd(dst, lo);
+          if (hi) atomicAdd(dst + 1, hi);
+        };
+        if constexpr (NH == 2) {
+          const uint64_t M = m[0] | ((uint64_t)m[1] << 32), NB = nbm[0] | ((uint64_t)nbm[1] << 32);
+          const uint64_t V = vm[0] | ((uint64_t)vm[1] << 32), H = hm[0] | ((uint64_t)hm[1] << 32);
+          uint64_t starts = (H | 1ull) & V;
+          while (starts) {
+            const int p = __ffsll((long long)starts) - 1;
+            starts &= starts - 1;
+            const int pend = starts ? __ffsll((long long)starts) - 1 : 64;
+            const uint64_t pm = V & ((pend >= 64 ? ~0ull : ((1ull << pend) - 1)) & ~((1ull << p) - 1));
+            const uint64_t z = pm & ~M, o = pm & M;
+            piece((uint32_t)B[i0 + p] >> nsh, __popcll(z & ~NB), __popcll(z & NB), __popcll(o & ~NB),
+                  __popcll(o & NB));
+          }
+        } else {
+          const uint32_t M = m[0], NB = nbm[0], V = vm[0];
+          uint32_t starts = (hm[0] | 1u) & V;
+          while (starts) {
+            const int p = __ffs(starts) - 1;
+            starts &= starts - 1;
+            const int pend = starts ? __ffs(starts) - 1 : 32;
+            const uint32_t pm = V & lowmask((uint32_t)pend) & ~((1u << p) - 1u);
+            const uint32_t z = pm & ~M, o = pm & M;
+            piece((uint32_t)B[i0 + p] >> nsh, __popc(z & ~NB), __popc(z & NB), __popc(o & ~NB), __popc(o & NB));
+          }
+        }
+      }
+#endif
+      if (segtab && !one) __syncwarp();  // kt[]
+
+      // ---------------- phase D: every symbol from the input buffer to its stage position
+#ifndef WT_EXP_SKIP_D
+      {
+        if (segtab) {  // segment table in shared memory (or one segment, partial tile)
+          const uint2 kF = make_uint2(sa(K0F), sa(K1F));
+          const bool full = len == (uint32_t)TILE;
+#pragma unroll
+          for (int k = 0; k < XW; ++k) {
+            const uint32_t w = lane + 32 * k;
+            const uint32_t q0 = w * SPW;
+            if (!full && q0 >= len) break;
+            const uint4 ow = own[w / XW];
+            const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
+            uint32_t g = ow.w + (uint32_t)__popc(ow.z & subhead);  // segment of the word's first symbol
+            const uint32_t m4 = ow.x >> sub;
+            const uint32_t h4 = SPW == 1 ? 0u : (ow.z >> sub) & ((1u << SPW) - 2u);  // heads inside the word
+            const uint32_t x = Win[w];
+            const uint32_t nv = full ? (uint32_t)SPW : min((uint32_t)SPW, len - q0);
+            if (nv == (uint32_t)SPW && h4 == 0) {
+              const uint2 kk = one ? kF : S.kt[g];
+              word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4));
+            } else {
+              word_split(x, q0, R, m4, h4, nv, [&](int j, uint32_t, uint32_t h) {
+                g += (h >> j) & 1u;
+                return one ? kF : S.kt[g];
+              });
+            }
+          }
+        } else {  // too many segments for the table: node tables from global memory
+          auto consts = [&](uint32_t v) -> uint2 {
+            if (v == vF) return make_uint2(sa(K0F), sa(K1F));
+            if (v == vL) return make_uint2(sa(K0L), sa(K1L));
+            // interior node: stage position = HBM destination - T0 + MARGIN
+            const uint2 t = __ldg(&tab[v]);
+            return make_uint2(sa((int32_t)(t.x - P) + MARGIN), sa((int32_t)(t.y + P - T0) + MARGIN));
+          };
+#pragma unroll
+          for (int k = 0; k < XW; ++k) {
+            const uint32_t w = lane + 32 * k;
+            const uint32_t q0 = w * SPW;
+            if (q0 >= len) break;
+            const uint4 ow = own[w / XW];
+            const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
+            const uint32_t m4 = ow.x >> sub;
+            const uint32_t h4 = SPW == 1 ? 0u : (ow.z >> sub) & ((1u << SPW) - 2u);
+            const uint32_t x = Win[w];
+            const uint32_t nv = min((uint32_t)SPW, len - q0);
+            if (nv == (uint32_t)SPW && h4 == 0) {
+              const uint2 kk = consts(sym_in_word<T>(x, 0) >> nsh);
+              word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4));
+            } else {
+              word_split(x, q0, R, m4, h4, nv, [&](int, uint32_t sym, uint32_t) { return consts(sym >> nsh); });
+            }
+          }
+        }
+      }
+#endif
+      fence_proxy_async_smem();
+      __syncwarp();  // stage partitioned (and the input buffer fully read)
+
+      // ---------------- phase E: TMA bulk stores of the aligned bodies, element stores of the edges
+      auto emit_region = [&](int32_t b, int32_t l, uint32_t D) {  // stage [b, b+l) -> HBM [D, D+l)
+        if (l <= 0) return;  // warp-uniform
+        const int32_t end = b + l;
+        const int32_t fs = (b + A - 1) / A * A, fe = end / A * A;
+        T* const go = out + D - b;  // HBM address of stage position q: go + q
+        if (lane == 0 && fe > fs) bulk_s2g(go + fs, S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
+        // head edge [b, min(fs, end)) and tail edge [max(fe, that), end), each < A symbols
+        const int32_t hend = min(fs, end), tst = max(fe, hend);
+        const int32_t q = (lane < (uint32_t)A) ? b + (int32_t)lane : tst + (int32_t)lane - A;
+        if (lane < (uint32_t)(2 * A) && ((lane < (uint32_t)A) ? (q < hend) : (q < end))) go[q] = S.buf[ob][q];
+      };
+      if constexpr (sizeof(T) == 1) {  // (A = 16: one region's two edges fill the warp)
+        if (one) {  // warp-uniform: the first segment's two runs only
+          emit_region(b1, z0, D0z);
+          emit_region(b2, o0, D0o);
+        } else {
+#pragma unroll
+          for (int r = 0; r < LV_NREG; ++r) emit_region(rb[r], rl[r], rD[r]);
+        }
+        if (lane < (uint32_t)LV_NREG) bulk_commit();  // lanes 1.. commit empty groups (uniform wait below)
       } else {
+        // lane r < LV_NREG: region r's bulk store; then all regions' edge
+        // symbols (<= 2A each) as one lane-parallel list of slots
+        const uint32_t r_ = min(lane, (uint32_t)(LV_NREG - 1));
+        int32_t b = rb[0], l = rl[0];
+        uint32_t D = rD[0];
 #pragma unroll
-        for (int r = 0; r < LV_NREG; ++r) emit_region(rb[r], rl[r], rD[r]);
+        for (int k = 1; k < LV_NREG; ++k)
+          if (r_ == (uint32_t)k) b = rb[k], l = rl[k], D = rD[k];
+        if (lane >= (uint32_t)LV_NREG) l = 0;
+        const int32_t end = b + l, fs = (b + A - 1) / A * A, fe = end / A * A;
+        const uint32_t Dmb = D - (uint32_t)b;  // HBM position of stage position q: Dmb + q
+        if (l > 0 && fe > fs) bulk_s2g(out + (Dmb + (uint32_t)fs), S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
+        if (lane < (uint32_t)LV_NREG) bulk_commit();
+        const int32_t hend = l > 0 ? min(fs, end) : b, tst = max(fe, hend), endv = l > 0 ? end : b;
+#pragma unroll
+        for (uint32_t base = 0; base < (uint32_t)(2 * A * LV_NREG); base += 32) {
+          const uint32_t slot = base + lane;
+          const int rs = (int)min(slot / (2 * A), (uint32_t)(LV_NREG - 1));
+          const uint32_t e = slot % (2 * A);
+          const int32_t b_ = __shfl_sync(FULL, b, rs), hend_ = __shfl_sync(FULL, hend, rs);
+          const int32_t tst_ = __shfl_sync(FULL, tst, rs), end_ = __shfl_sync(FULL, endv, rs);
+          const uint32_t Dmb_ = __shfl_sync(FULL, Dmb, rs);
+          const int32_t q = (e < (uint32_t)A) ? b_ + (int32_t)e : tst_ + (int32_t)e - A;
+          if (slot < (uint32_t)(2 * A * LV_NREG) && ((e < (uint32_t)A) ? (q < hend_) : (q < end_)))
+            out[Dmb_ + (uint32_t)q] = S.buf[ob][q];
+        }
       }
-      if (lane == 0) bulk_commit();
-    } else {
-      // lane r < LV_NREG: region r's bulk store; then all regions' edge
-      // symbols (<= 2A each) as one lane-parallel list of slots
-      const uint32_t r_ = min(lane, (uint32_t)(LV_NREG - 1));
-      int32_t b = rb[0], l = rl[0];
-      uint32_t D = rD[0];
-#pragma unroll
-      for (int k = 1; k < LV_NREG; ++k)
-        if (r_ == (uint32_t)k) b = rb[k], l = rl[k], D = rD[k];
-      if (lane >= (uint32_t)LV_NREG) l = 0;
-      const int32_t end = b + l, fs = (b + A - 1) / A * A, fe = end / A * A;
-      const uint32_t Dmb = D - (uint32_t)b;  // HBM position of stage position q: Dmb + q
-      if (l > 0 && fe > fs) bulk_s2g(out + (Dmb + (uint32_t)fs), S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
-      if (lane < (uint32_t)LV_NREG) bulk_commit();
-      const int32_t hend = l > 0 ? min(fs, end) : b, tst = max(fe, hend), endv = l > 0 ? end : b;
-#pragma unroll
-      for (uint32_t base = 0; base < (uint32_t)(2 * A * LV_NREG); base += 32) {
-        const uint32_t slot = base + lane;
-        const int rs = (int)min(slot / (2 * A), (uint32_t)(LV_NREG - 1));
-        const uint32_t e = slot % (2 * A);
-        const int32_t b_ = __shfl_sync(FULL, b, rs), hend_ = __shfl_sync(FULL, hend, rs);
-        const int32_t tst_ = __shfl_sync(FULL, tst, rs), end_ = __shfl_sync(FULL, endv, rs);
-        const uint32_t Dmb_ = __shfl_sync(FULL, Dmb, rs);
-        const int32_t q = (e < (uint32_t)A) ? b_ + (int32_t)e : tst_ + (int32_t)e - A;
-        if (slot < (uint32_t)(2 * A * LV_NREG) && ((e < (uint32_t)A) ? (q < hend_) : (q < end_)))
-          out[Dmb_ + (uint32_t)q] = S.buf[ob][q];
+      if (lane < (uint32_t)LV_NKEY && mycnt) {  // next-level ones per destination tile
+        const int r = (int)(lane >> 1);
+        uint32_t D = r == 1 ? D0z : D0o;
+        if (!one) D = r == 3 ? Dmz : r == 4 ? Dmo : D;
+        atomicAdd(&agg_next[r == 0 ? tile : D / TILE + (lane & 1)], mycnt);
       }
-    }
-    if (lane < (uint32_t)LV_NKEY && mycnt) {  // next-level ones per destination tile
-      const int r = (int)(lane >> 1);
-      uint32_t D = r == 1 ? D0z : D0o;
-      if (!one) D = r == 3 ? Dmz : r == 4 ? Dmo : D;
-      atomicAdd(&agg_next[r == 0 ? tile : D / TILE + (lane & 1)], mycnt);
     }
     // the previous tile's output buffer: once its bulk stores have read it, load a new tile into it
-    if (sizeof(T) == 1 ? lane == 0 : lane < (uint32_t)LV_NREG) bulk_wait_read<1>();  // each lane's own groups
+    if (lane < (uint32_t)LV_NREG) bulk_wait_read<1>();  // each lane's own groups
     __syncwarp();
     if (lane == 0 && it >= 1) issue(it + NB - 2);
   }
   if (SCATTER) {
     cc_flush();
-    if (sizeof(T) == 1 ? lane == 0 : lane < (uint32_t)LV_NREG) bulk_wait<0>();
+    if (lane < (uint32_t)LV_NREG) bulk_wait<0>();
   }
 }
 
