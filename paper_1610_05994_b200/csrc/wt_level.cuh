@@ -639,29 +639,63 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       // ---------------- phase D: every symbol from the input buffer to its stage position
 #ifndef WT_EXP_SKIP_D
       {
-        if (segtab) {  // segment table in shared memory (or one segment, partial tile)
-          const uint2 kF = make_uint2(sa(K0F), sa(K1F));
-          const bool full = len == (uint32_t)TILE;
-#pragma unroll
-          for (int k = 0; k < XW; ++k) {
+        if (segtab) {  // segment table in shared memory
+          const uint32_t kt_base = smem_u32(S.kt);
+          // word w = lane + 32 k: segment g of its first symbol, stage by kt[g]
+          auto seg_word = [&](int k, bool check) {
             const uint32_t w = lane + 32 * k;
             const uint32_t q0 = w * SPW;
-            if (!full && q0 >= len) break;
             const uint4 ow = own[w / XW];
             const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
             uint32_t g = ow.w + (uint32_t)__popc(ow.z & subhead);  // segment of the word's first symbol
             const uint32_t m4 = ow.x >> sub;
-            const uint32_t h4 = SPW == 1 ? 0u : (ow.z >> sub) & ((1u << SPW) - 2u);  // heads inside the word
             const uint32_t x = Win[w];
-            const uint32_t nv = full ? (uint32_t)SPW : min((uint32_t)SPW, len - q0);
-            if (nv == (uint32_t)SPW && h4 == 0) {
-              const uint2 kk = one ? kF : S.kt[g];
-              word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4));
+            if constexpr (SPW == 1) {
+              const uint2 kk = ld_shared_u2(kt_base + 8u * g);
+              word_one_segment(x, q0, R, m4, kk.x, kk.y, make_uint4(0, 0, 0, 0));
             } else {
-              word_split(x, q0, R, m4, h4, nv, [&](int j, uint32_t, uint32_t h) {
-                g += (h >> j) & 1u;
-                return one ? kF : S.kt[g];
-              });
+              const uint32_t h4 = (ow.z >> sub) & ((1u << SPW) - 2u);  // heads inside the word
+              const uint32_t nv = check ? min((uint32_t)SPW, len - q0) : (uint32_t)SPW;
+              if (nv == (uint32_t)SPW && h4 == 0) {
+                const uint2 kk = ld_shared_u2(kt_base + 8u * g);
+                word_one_segment(x, q0, R, m4, kk.x, kk.y, lut_of(m4));
+              } else {
+                word_split(x, q0, R, m4, h4, nv, [&](int j, uint32_t, uint32_t h) {
+                  g += (h >> j) & 1u;
+                  return ld_shared_u2(kt_base + 8u * g);
+                });
+              }
+            }
+          };
+          if (SPW == 1 && len == (uint32_t)TILE) {  // warp-uniform; batches of BK words, loads first
+            constexpr int BK = 4;
+#pragma unroll
+            for (int k0 = 0; k0 < XW; k0 += BK) {
+              uint32_t xs[BK], Rs[BK], gs[BK], bs[BK];
+              uint2 ks[BK];
+#pragma unroll
+              for (int k = 0; k < BK; ++k) {
+                const uint32_t w = lane + 32 * (k0 + k);
+                const uint4 ow = own[w / XW];
+                xs[k] = Win[w];
+                Rs[k] = ow.y + (uint32_t)__popc(ow.x & submask);
+                gs[k] = ow.w + (uint32_t)__popc(ow.z & subhead);
+                bs[k] = (ow.x >> sub) & 1u;
+              }
+#pragma unroll
+              for (int k = 0; k < BK; ++k) ks[k] = ld_shared_u2(kt_base + 8u * gs[k]);
+#pragma unroll
+              for (int k = 0; k < BK; ++k)
+                word_one_segment(xs[k], lane + 32 * (k0 + k), Rs[k], bs[k], ks[k].x, ks[k].y, make_uint4(0, 0, 0, 0));
+            }
+          } else if (len == (uint32_t)TILE) {
+#pragma unroll
+            for (int k = 0; k < XW; ++k) seg_word(k, false);
+          } else {
+#pragma unroll
+            for (int k = 0; k < XW; ++k) {
+              if ((lane + 32 * k) * SPW >= len) break;
+              seg_word(k, true);
             }
           }
         } else {  // too many segments for the table: node tables from global memory

@@ -142,6 +142,12 @@ __device__ __forceinline__ uint32_t sym_in_word(uint32_t x, int j) {
   return x;
 }
 
+__device__ __forceinline__ uint2 ld_shared_u2(uint32_t a) {  // shared byte address a (8-byte aligned)
+  uint2 v;
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t lowmask(uint32_t k) { return k >= 32 ? 0xffffffffu : ((1u << k) - 1u); }
 
 }  // namespace wt
