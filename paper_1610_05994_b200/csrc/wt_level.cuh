@@ -70,13 +70,14 @@ template <typename T>
 struct LevelSmem {
   using C = LvTile<T>;
   alignas(128) T buf[C::NB][C::BUF];  // ring: input tiles land at buf[b][MARGIN], outputs are staged
-  uint4 own[C::NH][32];               // per lane and mask half: {bits, ones before, head bits, heads before}
+  uint4 own[32 * C::NH];              // lane l, mask half h at [NH l + h] (the NH entries of a lane adjacent:
+                                      // phase D's loads of a word round then hit distinct banks):
+                                      // {bits, ones before, head bits, heads before}
   uint16_t seg_a[C::MAXSEG + 1];      // segment g starts at tile position seg_a[g] (g >= 1)
   uint16_t seg_R[C::MAXSEG + 1];      // tile-local ones before seg_a[g]
   uint2 kt[C::MAXSEG];                // segment g: shared-memory byte addresses {Z0, O0}: a zero at q with
                                       // R ones before it goes to Z0 + (q - R) W, a one to O0 + R W
-  uint4 lut[16];                      // in-word stable partition: {selector | nz << 16, z1, z2, z3},
-                                      // z_k = 1 if slot k of the partitioned word is a zero
+  uint32_t lut[16];                   // in-word stable partition: selector | nz << 16 (nz zeros first)
   int32_t s1, am, Rs1, Ram;           // first-segment end, last-segment start, ranks there
   alignas(8) unsigned long long bar[C::NB];
 };
@@ -129,8 +130,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     for (int b = 0; b < (SCATTER ? NB - 1 : NB); ++b) issue((uint32_t)b);
   }
   if (SCATTER && lane < 16) {
-    const uint32_t e = partition_lut_entry<T>(lane), nz = e >> 16;
-    S.lut[lane] = make_uint4(e, nz > 1, nz > 2, nz > 3);
+    S.lut[lane] = partition_lut_entry<T>(lane);
   }
   __syncwarp();
 
@@ -257,31 +257,29 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const uint32_t soff = (lane % (uint32_t)XW) * SPW;
     const uint32_t hh = soff / 32, sub = soff % 32;
     const uint32_t submask = lowmask(sub), subhead = lowmask(sub + 1);
-    const uint4* own = S.own[NH == 1 ? 0 : hh];
-    auto lut_of = [&](uint32_t m4) -> uint4 {
-      return SPW == 1 ? make_uint4(0, 0, 0, 0) : S.lut[m4 & ((1u << SPW) - 1u)];
-    };
+    const uint4* own = S.own + (NH == 1 ? 0 : hh);  // own[NH * owner]
+    // (4-byte entries: the 16 entries span 16 banks, one wavefront per word round)
+    auto lut_of = [&](uint32_t m4) -> uint32_t { return SPW == 1 ? 0u : S.lut[m4 & ((1u << SPW) - 1u)]; };
     // stores the SPW symbols of word x (tile position q0, R ones before it,
     // bits m4, in-word partition e) into the segment with byte addresses
-    // (Z0, O0) (kt[]).  Slot k of the partitioned word y goes to
-    // Ao + k + z_k (Az - Ao): the slot choice is a multiply-add (FMA pipe)
-    // and the symbol extraction a multiply-high, keeping the ALU pipe free.
+    // (Z0, O0) (kt[]).  Slot k of the partitioned word y is a zero iff
+    // k < nz: it goes to Az + k, else to Ao + k; the symbol extraction is a
+    // multiply-high (FMA pipe).
     auto word_one_segment = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, uint32_t Z0, uint32_t O0,
-                                uint4 e) {
+                                uint32_t e) {
       if constexpr (SPW == 1) {
         st_shared<T>((m4 & 1u) ? O0 + R * (uint32_t)sizeof(T) : Z0 + (q0 - R) * (uint32_t)sizeof(T), x);
       } else {
         uint32_t y;
-        asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(x), "r"(e.x));  // selector = e.x[15:0]
-        const uint32_t nz = e.x >> 16;
+        asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(x), "r"(e));  // selector = e[15:0]
+        const uint32_t nz = e >> 16;
         const uint32_t Az = Z0 + (q0 - R) * (uint32_t)sizeof(T);
         const uint32_t Ao = O0 + (R - nz) * (uint32_t)sizeof(T);
-        const uint32_t d = Az - Ao;
-        st_shared<T, 0>(nz ? Az : Ao, y);
-        st_shared<T, sizeof(T)>(Ao + e.y * d, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
+        st_shared<T, 0>(e >= (1u << 16) ? Az : Ao, y);
+        st_shared<T, sizeof(T)>(e >= (2u << 16) ? Az : Ao, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
         if constexpr (SPW > 2) {
-          st_shared<T, 2>(Ao + e.z * d, __umulhi(y, 1u << 16));
-          st_shared<T, 3>(Ao + e.w * d, __umulhi(y, 1u << 8));
+          st_shared<T, 2>(e >= (3u << 16) ? Az : Ao, __umulhi(y, 1u << 16));
+          st_shared<T, 3>(e >= (4u << 16) ? Az : Ao, __umulhi(y, 1u << 8));
         }
       }
     };
@@ -306,7 +304,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         uint32_t po = mypre;
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
-          *reinterpret_cast<uint2*>(&S.own[h][lane]) = make_uint2(m[h], po);
+          *reinterpret_cast<uint2*>(&S.own[NH * lane + h]) = make_uint2(m[h], po);
           po += (uint32_t)__popc(m[h]);
         }
       }
@@ -353,11 +351,11 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
 #pragma unroll
         for (int k0 = 0; k0 < XW; k0 += BK) {
           uint32_t xs[BK], Rs[BK], ms[BK];
-          uint4 es[BK];
+          uint32_t es[BK];
 #pragma unroll
           for (int k = 0; k < BK; ++k) {
             const uint32_t w = lane + 32 * (k0 + k);
-            const uint2 ow = *reinterpret_cast<const uint2*>(&own[w / XW]);
+            const uint2 ow = *reinterpret_cast<const uint2*>(&own[NH * (w / XW)]);
             xs[k] = Win[w];
             Rs[k] = ow.y + (uint32_t)__popc(ow.x & submask);
             ms[k] = ow.x >> sub;
@@ -375,7 +373,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           const uint32_t w = lane + 32 * k;
           const uint32_t q0 = w * SPW;
           if (q0 >= len) break;
-          const uint2 ow = *reinterpret_cast<const uint2*>(&own[w / XW]);
+          const uint2 ow = *reinterpret_cast<const uint2*>(&own[NH * (w / XW)]);
           const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
           const uint32_t m4 = ow.x >> sub;
           const uint32_t x = Win[w];
@@ -433,7 +431,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         uint32_t po = mypre, ph = hpre;
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
-          S.own[h][lane] = make_uint4(m[h], po, hm[h], ph);
+          S.own[NH * lane + h] = make_uint4(m[h], po, hm[h], ph);
           po += (uint32_t)__popc(m[h]);
           ph += (uint32_t)__popc(hm[h]);
         }
@@ -645,14 +643,14 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           auto seg_word = [&](int k, bool check) {
             const uint32_t w = lane + 32 * k;
             const uint32_t q0 = w * SPW;
-            const uint4 ow = own[w / XW];
+            const uint4 ow = own[NH * (w / XW)];
             const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
             uint32_t g = ow.w + (uint32_t)__popc(ow.z & subhead);  // segment of the word's first symbol
             const uint32_t m4 = ow.x >> sub;
             const uint32_t x = Win[w];
             if constexpr (SPW == 1) {
               const uint2 kk = ld_shared_u2(kt_base + 8u * g);
-              word_one_segment(x, q0, R, m4, kk.x, kk.y, make_uint4(0, 0, 0, 0));
+              word_one_segment(x, q0, R, m4, kk.x, kk.y, 0u);
             } else {
               const uint32_t h4 = (ow.z >> sub) & ((1u << SPW) - 2u);  // heads inside the word
               const uint32_t nv = check ? min((uint32_t)SPW, len - q0) : (uint32_t)SPW;
@@ -676,7 +674,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
 #pragma unroll
               for (int k = 0; k < BK; ++k) {
                 const uint32_t w = lane + 32 * (k0 + k);
-                const uint4 ow = own[w / XW];
+                const uint4 ow = own[NH * (w / XW)];
                 xs[k] = Win[w];
                 Rs[k] = ow.y + (uint32_t)__popc(ow.x & submask);
                 gs[k] = ow.w + (uint32_t)__popc(ow.z & subhead);
@@ -686,7 +684,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
               for (int k = 0; k < BK; ++k) ks[k] = ld_shared_u2(kt_base + 8u * gs[k]);
 #pragma unroll
               for (int k = 0; k < BK; ++k)
-                word_one_segment(xs[k], lane + 32 * (k0 + k), Rs[k], bs[k], ks[k].x, ks[k].y, make_uint4(0, 0, 0, 0));
+                word_one_segment(xs[k], lane + 32 * (k0 + k), Rs[k], bs[k], ks[k].x, ks[k].y, 0u);
             }
           } else if (len == (uint32_t)TILE) {
 #pragma unroll
@@ -711,7 +709,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
             const uint32_t w = lane + 32 * k;
             const uint32_t q0 = w * SPW;
             if (q0 >= len) break;
-            const uint4 ow = own[w / XW];
+            const uint4 ow = own[NH * (w / XW)];
             const uint32_t R = ow.y + (uint32_t)__popc(ow.x & submask);
             const uint32_t m4 = ow.x >> sub;
             const uint32_t h4 = SPW == 1 ? 0u : (ow.z >> sub) & ((1u << SPW) - 2u);
