@@ -77,7 +77,8 @@ struct LevelSmem {
   uint16_t seg_R[C::MAXSEG + 1];      // tile-local ones before seg_a[g]
   uint2 kt[C::MAXSEG];                // segment g: shared-memory byte addresses {Z0, O0}: a zero at q with
                                       // R ones before it goes to Z0 + (q - R) W, a one to O0 + R W
-  uint32_t lut[16];                   // in-word stable partition: selector | nz << 16 (nz zeros first)
+  uint2 lut[16];                      // in-word stable partition: {selector | nz << 16 (nz zeros first),
+                                      // nz > 1}; 8-byte entries: one wavefront per word round
   int32_t s1, am, Rs1, Ram;           // first-segment end, last-segment start, ranks there
   alignas(8) unsigned long long bar[C::NB];
 };
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     for (int b = 0; b < (SCATTER ? NB - 1 : NB); ++b) issue((uint32_t)b);
   }
   if (SCATTER && lane < 16) {
-    S.lut[lane] = partition_lut_entry<T>(lane);
+    S.lut[lane] = make_uint2(partition_lut_entry<T>(lane), (partition_lut_entry<T>(lane) >> 16) > 1);
   }
   __syncwarp();
 
@@ -259,24 +260,32 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const uint32_t submask = lowmask(sub), subhead = lowmask(sub + 1);
     const uint4* own = S.own + (NH == 1 ? 0 : hh);  // own[NH * owner]
     // (4-byte entries: the 16 entries span 16 banks, one wavefront per word round)
-    auto lut_of = [&](uint32_t m4) -> uint32_t { return SPW == 1 ? 0u : S.lut[m4 & ((1u << SPW) - 1u)]; };
+    auto lut_of = [&](uint32_t m4) -> uint2 {
+      if constexpr (SPW == 1) return make_uint2(0, 0);
+      else if constexpr (SPW == 4) return make_uint2(S.lut[m4 & 15u].x, 0u);  // (u8: .y unused, 4-byte loads)
+      else return S.lut[m4 & ((1u << SPW) - 1u)];
+    };
     // stores the SPW symbols of word x (tile position q0, R ones before it,
     // bits m4, in-word partition e) into the segment with byte addresses
     // (Z0, O0) (kt[]).  Slot k of the partitioned word y is a zero iff
     // k < nz: it goes to Az + k, else to Ao + k; the symbol extraction is a
     // multiply-high (FMA pipe).
     auto word_one_segment = [&](uint32_t x, uint32_t q0, uint32_t R, uint32_t m4, uint32_t Z0, uint32_t O0,
-                                uint32_t e) {
+                                uint2 e2) {
       if constexpr (SPW == 1) {
         st_shared<T>((m4 & 1u) ? O0 + R * (uint32_t)sizeof(T) : Z0 + (q0 - R) * (uint32_t)sizeof(T), x);
       } else {
+        const uint32_t e = e2.x;
         uint32_t y;
         asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(x), "r"(e));  // selector = e[15:0]
         const uint32_t nz = e >> 16;
         const uint32_t Az = Z0 + (q0 - R) * (uint32_t)sizeof(T);
         const uint32_t Ao = O0 + (R - nz) * (uint32_t)sizeof(T);
         st_shared<T, 0>(e >= (1u << 16) ? Az : Ao, y);
-        st_shared<T, sizeof(T)>(e >= (2u << 16) ? Az : Ao, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
+        if constexpr (SPW == 2)  // (u16: slot 1 by a multiply-add, FMA pipe)
+          st_shared<T, sizeof(T)>(Ao + e2.y * (Az - Ao), __umulhi(y, 1u << (32 - 8 * sizeof(T))));
+        else
+          st_shared<T, sizeof(T)>(e >= (2u << 16) ? Az : Ao, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
         if constexpr (SPW > 2) {
           st_shared<T, 2>(e >= (3u << 16) ? Az : Ao, __umulhi(y, 1u << 16));
           st_shared<T, 3>(e >= (4u << 16) ? Az : Ao, __umulhi(y, 1u << 8));
@@ -351,7 +360,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
 #pragma unroll
         for (int k0 = 0; k0 < XW; k0 += BK) {
           uint32_t xs[BK], Rs[BK], ms[BK];
-          uint32_t es[BK];
+          uint2 es[BK];
 #pragma unroll
           for (int k = 0; k < BK; ++k) {
             const uint32_t w = lane + 32 * (k0 + k);
@@ -650,7 +659,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
             const uint32_t x = Win[w];
             if constexpr (SPW == 1) {
               const uint2 kk = ld_shared_u2(kt_base + 8u * g);
-              word_one_segment(x, q0, R, m4, kk.x, kk.y, 0u);
+              word_one_segment(x, q0, R, m4, kk.x, kk.y, make_uint2(0, 0));
             } else {
               const uint32_t h4 = (ow.z >> sub) & ((1u << SPW) - 2u);  // heads inside the word
               const uint32_t nv = check ? min((uint32_t)SPW, len - q0) : (uint32_t)SPW;
@@ -684,7 +693,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
               for (int k = 0; k < BK; ++k) ks[k] = ld_shared_u2(kt_base + 8u * gs[k]);
 #pragma unroll
               for (int k = 0; k < BK; ++k)
-                word_one_segment(xs[k], lane + 32 * (k0 + k), Rs[k], bs[k], ks[k].x, ks[k].y, 0u);
+                word_one_segment(xs[k], lane + 32 * (k0 + k), Rs[k], bs[k], ks[k].x, ks[k].y, make_uint2(0, 0));
             }
           } else if (len == (uint32_t)TILE) {
 #pragma unroll
