@@ -162,18 +162,37 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     }
 
     // ---------------- phase A: the lane's 64 bytes -> E bits, bitmap word(s)
+    // The lane's four 16-byte chunks are read in a lane-rotated order (slot
+    // v holds chunk (v + rot) & 3): lanes 64 bytes apart would otherwise hit
+    // the same banks 4-way.  Masks are built in slot order and rotated back.
+    constexpr int CS = E / 4;  // symbols per chunk
+    const uint32_t rot = SCATTER ? (lane >> 1) & 3u : 0u;  // (last level: not smem-bound, no rotation)
     uint32_t xw[XW];
     {
       const uint4* src = reinterpret_cast<const uint4*>(B + i0);
 #pragma unroll
       for (int v = 0; v < XW / 4; ++v) {
-        const uint4 q = src[v];
+        const uint4 q = src[(v + rot) & 3u];
         xw[4 * v] = q.x, xw[4 * v + 1] = q.y, xw[4 * v + 2] = q.z, xw[4 * v + 3] = q.w;
       }
     }
+    // slot-order bits (bit CS v + j = symbol j of slot v) -> position order
+    auto unrot = [&](uint32_t (&x)[NH]) {
+      if constexpr (NH == 2) {  // 64 bits: rotate left by 16 rot
+        uint32_t lo = (rot & 2u) ? x[1] : x[0], hi = (rot & 2u) ? x[0] : x[1];
+        const uint32_t s16 = (rot & 1u) * 16u;
+        x[0] = __funnelshift_l(hi, lo, s16);
+        x[1] = __funnelshift_l(lo, hi, s16);
+      } else if constexpr (E == 32) {
+        x[0] = __funnelshift_l(x[0], x[0], 8u * rot);
+      } else {  // E == 16: a 16-bit field
+        x[0] = ((x[0] * 0x10001u) >> (16u - 4u * rot)) & 0xffffu;
+      }
+    };
     const uint32_t nvalid = (i0 >= len) ? 0u : min((uint32_t)E, len - i0);
     uint32_t m[NH], nbm[NH], vm[NH];
     vm[0] = lowmask(min(nvalid, 32u)) & EM;
+    if constexpr (NH == 2) vm[NH - 1] = lowmask(nvalid > 32 ? nvalid - 32 : 0u);
     if constexpr (sizeof(T) == 4) {
       // one funnel rotation per symbol serves both masks: rotr(x, sh - k)
       // puts bit sh at k and bit sh-1 at k-1 (mod 32); nbm is accumulated
@@ -185,17 +204,20 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         mm |= r & (1u << k);
         if (SCATTER) nn |= r & (1u << ((k + 31) & 31));
       }
-      m[0] = mm & vm[0];
-      nbm[0] = SCATTER ? (__funnelshift_l(nn, nn, 1) & vm[0]) : 0u;  // next level's bits
+      m[0] = mm;
+      nbm[0] = SCATTER ? __funnelshift_l(nn, nn, 1) & 0xffffu : 0u;  // next level's bits
     } else {
-      m[0] = swar_bits<T, XW / NH, 0>(xw, sh) & vm[0];
-      nbm[0] = SCATTER ? (swar_bits<T, XW / NH, 0>(xw, sh - 1) & vm[0]) : 0u;  // next level's bits
+      m[0] = swar_bits<T, XW / NH, 0>(xw, sh);
+      nbm[0] = SCATTER ? swar_bits<T, XW / NH, 0>(xw, sh - 1) : 0u;  // next level's bits
+      if constexpr (NH == 2) {
+        m[NH - 1] = swar_bits<T, XW / 2, XW / 2>(xw, sh);
+        nbm[NH - 1] = SCATTER ? swar_bits<T, XW / 2, XW / 2>(xw, sh - 1) : 0u;
+      }
     }
-    if constexpr (NH == 2) {
-      vm[NH - 1] = lowmask(nvalid > 32 ? nvalid - 32 : 0u);
-      m[NH - 1] = swar_bits<T, XW / 2, XW / 2>(xw, sh) & vm[NH - 1];
-      nbm[NH - 1] = SCATTER ? (swar_bits<T, XW / 2, XW / 2>(xw, sh - 1) & vm[NH - 1]) : 0u;
-    }
+    unrot(m);
+    if (SCATTER) unrot(nbm);
+#pragma unroll
+    for (int h = 0; h < NH; ++h) m[h] &= vm[h], nbm[h] &= vm[h];
     {  // bitmap words (LSB-first)
       const uint32_t gw = (T0 + i0) / 32;
       if constexpr (E == 64) {
@@ -218,13 +240,21 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       tabF = __ldg(&tab[vF]);  // issued early: at deep levels these miss L1
       tabL = __ldg(&tab[vL]);
       if (vF != vL) {  // warp-uniform: segment heads (positions q > 0 whose node differs from q-1's)
-        uint32_t prev = lane ? ((uint32_t)B[i0 - 1] >> nsh) : vF;
+        // in slot order: the first symbol of slot v follows the last symbol of
+        // slot v - 1, or the previous lane's last symbol when it is chunk 0
+        const uint32_t pl = lane ? ((uint32_t)B[i0 - 1] >> nsh) : vF;
 #pragma unroll
-        for (int q = 0; q < E; ++q) {
-          const uint32_t nd = sym_of<T>(xw, q) >> nsh;
-          hm[q / 32] |= (nd != prev ? 1u : 0u) << (q % 32);
-          prev = nd;
+        for (int v = 0; v < 4; ++v) {
+          uint32_t prev = (v == (int)((4u - rot) & 3u)) ? pl : (sym_of<T>(xw, ((v + 3) & 3) * CS + CS - 1) >> nsh);
+#pragma unroll
+          for (int j = 0; j < CS; ++j) {
+            const int q = v * CS + j;
+            const uint32_t nd = sym_of<T>(xw, q) >> nsh;
+            hm[q / 32] |= (nd != prev ? 1u : 0u) << (q % 32);
+            prev = nd;
+          }
         }
+        unrot(hm);
 #pragma unroll
         for (int h = 0; h < NH; ++h) hm[h] &= vm[h];
       }
