@@ -307,11 +307,13 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       uint32_t* cn = last ? nullptr : cnt[l & 1];
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
       if (last)
-        wt::k_level<T, false><<<grid_last, wt::LV_THREADS, lsmem, stream>>>(in, o, n, sh, t, bits, c.words, sb,
-                                                                           c.nsb, pre, agg_next, cn, flag);
+        wt::k_level<T, false><<<grid_last, wt::LV_THREADS, lsmem, stream>>>(
+            in, o, (uint32_t)n, (uint32_t)c.ntiles, sh, t, bits, (uint32_t)c.words, sb, (uint32_t)c.nsb, pre,
+            agg_next, cn, flag);
       else
-        wt::k_level<T, true><<<grid_sc, wt::LV_THREADS, lsmem, stream>>>(in, o, n, sh, t, bits, c.words, sb, c.nsb,
-                                                                         pre, agg_next, cn, flag);
+        wt::k_level<T, true><<<grid_sc, wt::LV_THREADS, lsmem, stream>>>(
+            in, o, (uint32_t)n, (uint32_t)c.ntiles, sh, t, bits, (uint32_t)c.words, sb, (uint32_t)c.nsb, pre,
+            agg_next, cn, flag);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_level");
       if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
     }

@@ -92,9 +92,9 @@ constexpr size_t level_smem_bytes() {
 // blockDim.x == 32 (one warp per CTA).
 template <typename T, bool SCATTER>
 __global__ void __launch_bounds__(32, LvTile<T>::MINB)
-    k_level(const T* __restrict__ in, T* __restrict__ out, uint64_t n, uint32_t sh,
-            const uint2* __restrict__ tab, uint32_t* __restrict__ bits, uint64_t words_per_level,
-            unsigned long long* __restrict__ sb, uint64_t nsb, const uint32_t* __restrict__ pre,
+    k_level(const T* __restrict__ in, T* __restrict__ out, uint32_t n32, uint32_t ntiles, uint32_t sh,
+            const uint2* __restrict__ tab, uint32_t* __restrict__ bits, uint32_t words_per_level,
+            unsigned long long* __restrict__ sb, uint32_t nsb, const uint32_t* __restrict__ pre,
             uint32_t* __restrict__ agg_next, uint32_t* __restrict__ cnt_next, const int32_t* __restrict__ flag) {
   using Cfg = LvTile<T>;
   constexpr int TILE = Cfg::TILE, A = Cfg::A, E = Cfg::E, SPW = Cfg::SPW, XW = Cfg::XW, NH = Cfg::NH;
@@ -106,8 +106,6 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
   if (*flag) return;
   // n < 2^32 (wt_sizes rejects larger n): every position, rank and node
   // offset of the pass fits 32 bits; only pointers are 64-bit.
-  const uint32_t n32 = (uint32_t)n;
-  const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
   const uint32_t lane = threadIdx.x;
   const uint32_t nsh = sh + 1;   // node id = symbol >> nsh
   const uint32_t i0 = lane * E;  // first tile position of this lane (phase A)
@@ -288,6 +286,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const uint32_t soff = (lane % (uint32_t)XW) * SPW;
     const uint32_t hh = soff / 32, sub = soff % 32;
     const uint32_t submask = lowmask(sub), subhead = lowmask(sub + 1);
+    const uint32_t lutrot = (sub - 3u) & 31u;  // rotr by this puts bits [sub, sub + 4) at [3, 7)
     const uint4* own = S.own + (NH == 1 ? 0 : hh);  // own[NH * owner]
     // (4-byte entries: the 16 entries span 16 banks, one wavefront per word round)
     auto lut_of = [&](uint32_t m4) -> uint2 {
@@ -380,7 +379,10 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         cc_flush();
         cc_node = vF;
       }
-      cc_acc += lane == 0 ? z0 - c01 : lane == 1 ? c01 : lane == 2 ? o0 - c11 : lane == 3 ? c11 : 0u;
+      {  // lane k < 4 adds count k = {00, 01, 10, 11}; lanes >= 4 hold don't-cares (cc_flush reads lanes 0..3)
+        const uint32_t cx = (lane & 2u) ? c11 : c01;
+        cc_acc += (lane & 1u) ? cx : ((lane & 2u) ? o0 : z0) - cx;
+      }
 #endif
       __syncwarp();  // own[]
 #ifndef WT_EXP_SKIP_D
@@ -397,10 +399,17 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
             const uint2 ow = *reinterpret_cast<const uint2*>(&own[NH * (w / XW)]);
             xs[k] = Win[w];
             Rs[k] = ow.y + (uint32_t)__popc(ow.x & submask);
-            ms[k] = ow.x >> sub;
+            ms[k] = SPW == 4 ? ow.x : ow.x >> sub;
           }
 #pragma unroll
-          for (int k = 0; k < BK; ++k) es[k] = lut_of(ms[k]);
+          for (int k = 0; k < BK; ++k) {
+            if constexpr (SPW == 4) {  // (u8) entry byte offset m4 * 8 by one funnel rotation of the bits
+              const uint32_t o8 = __funnelshift_r(ms[k], ms[k], lutrot) & 0x78u;
+              es[k] = make_uint2(*reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(S.lut) + o8), 0u);
+            } else {
+              es[k] = lut_of(ms[k]);
+            }
+          }
 #pragma unroll
           for (int k = 0; k < BK; ++k)
             word_one_segment(xs[k], (lane + 32 * (k0 + k)) * SPW, Rs[k], ms[k], Z0, O0, es[k]);
