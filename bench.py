@@ -55,8 +55,12 @@ def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
     bitmap = 4 * 16 * ((n + 511) // 512)
     if kind == "level":      # read T_l, write T_{l+1}, bitmap words, superblocks
         return 2 * n * w + bitmap + 8 * nsb
-    if kind == "last_level":  # read T_{L-1}, bitmap words, superblocks
+    if kind == "last_level":  # read T_{L-1}, bitmap words, superblocks (L = 1 only)
         return n * w + bitmap + 8 * nsb
+    if kind == "pair":        # level L-2 fused with L-1: read T_{L-2}, both bitmaps, superblocks of L-2
+        return n * w + 2 * bitmap + 8 * nsb
+    if kind == "sb_scan":     # superblocks of level L-1 from its bitmap
+        return bitmap + 8 * nsb
     if kind == "prologue":    # read S once (range check, level-0 tile ones)
         return n * w
     if kind == "scan":        # node_offsets: read 2^L uint32 leaf counts, write 2^L + 1 uint64
@@ -66,8 +70,8 @@ def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
         return 12 * ((n + tile - 1) // tile)
     if kind == "tables":      # level l: read 2^(l+1) uint32 counts, write 2^l {ob, Zn}; average per launch
         return sum(4 * (2 << l) + 16 * (1 << l) for l in range(max(L - 1, 0))) // max(L - 1, 1)
-    if kind == "memset":      # zero 2^(l+2) uint32 counts before pass l; average per launch
-        return sum(4 * (4 << l) for l in range(max(L - 1, 0))) // max(L - 1, 1)
+    if kind == "memset":      # zero 2^(l+2) uint32 counts before pass l, and B_{L-1}; average per launch
+        return (sum(4 * (4 << l) for l in range(max(L - 1, 0))) + bitmap) // L
     return 0
 
 

@@ -54,7 +54,7 @@ int num_sms() {
 
 // opt in to > 48 KiB dynamic shared memory once per level-kernel instantiation
 // and size the persistent grid: every resident CTA slot of every SM.
-template <typename T, bool SC>
+template <typename T, int SC>
 cudaError_t level_kernel_setup(int* blocks_per_sm) {
   static int bps = 0;
   static cudaError_t once = [] {
@@ -103,7 +103,8 @@ Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
   c.tab_entries = c.L >= 2 ? (1ull << (c.L - 1)) - 1 : 0;
   c.cnt_entries = c.L >= 2 ? (1ull << c.L) : 0;
   const uint64_t pre_tiles = (c.ntiles + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
-  c.status_entries = std::max<uint64_t>(1, std::max(pre_tiles, scan_tiles));
+  const uint64_t sb_tiles = (c.nsb + wt::SCAN_TILE - 1) / wt::SCAN_TILE;  // last level's superblock scan
+  c.status_entries = std::max<uint64_t>(1, std::max(std::max(pre_tiles, scan_tiles), sb_tiles));
   size_t o = 0;
   c.off_flag = o;
   o += ALIGN;
@@ -180,7 +181,9 @@ struct Launcher {
   }
 };
 
-enum Kind : uint32_t { K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7 };
+enum Kind : uint32_t {
+  K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7, K_PAIR = 8, K_SBSCAN = 9
+};
 
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
 template <typename T>
@@ -263,20 +266,25 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   constexpr uint64_t TILE = wt::LvTile<T>::TILE;
   const uint64_t ntiles = (n + TILE - 1) / TILE;
   const size_t lsmem = wt::level_smem_bytes<T>();
-  int bps_sc = 1, bps_last = 1;
+  int bps_sc = 1, bps_last = 1, bps_pair = 1;
   if (!dry) {
-    if ((e = level_kernel_setup<T, true>(&bps_sc)) != cudaSuccess) return fail_cuda(e, "k_level setup");
-    if ((e = level_kernel_setup<T, false>(&bps_last)) != cudaSuccess) return fail_cuda(e, "k_level setup");
+    if ((e = level_kernel_setup<T, 1>(&bps_sc)) != cudaSuccess) return fail_cuda(e, "k_level setup");
+    if ((e = level_kernel_setup<T, 0>(&bps_last)) != cudaSuccess) return fail_cuda(e, "k_level setup");
+    if ((e = level_kernel_setup<T, 2>(&bps_pair)) != cudaSuccess) return fail_cuda(e, "k_level setup");
   }
   const uint32_t grid_sc = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_sc * (uint64_t)num_sms());
   const uint32_t grid_last = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_last * (uint64_t)num_sms());
+  const uint32_t grid_pair = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_pair * (uint64_t)num_sms());
 #ifdef WT_EXP_LEVELS  // experiment builds: only the first level passes (timing studies)
   const uint32_t Lrun = std::min<uint32_t>(L, WT_EXP_LEVELS);
 #else
   const uint32_t Lrun = L;
 #endif
-  for (uint32_t l = 0; l < Lrun; ++l) {
+  // L >= 2: passes 0..L-3 write T_{l+1}; pass L-2 is fused with level L-1
+  // (writes B_{L-1} directly, no T_{L-1}); L = 1: the single last-level pass
+  for (uint32_t l = 0; l < Lrun && (L == 1 || l + 1 < L); ++l) {
     const bool last = (l + 1 == L);
+    const bool pair = (l + 2 == L);
     if (!last && l >= 1) {  // node tables of level l from the level-(l+1) node sizes counted by pass l-1
       note(K_TABLES);
       wt::OpLevelTab op{dry ? nullptr : cnt[(l - 1) & 1], tab + ((1ull << l) - 1), n, nullptr};
@@ -291,27 +299,41 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
         if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
       }
     }
+    uint32_t* const lastbits = dry ? nullptr : out->bitmaps + (uint64_t)(L - 1) * c.words;
+    if (pair) {  // B_{L-1} is OR-ed together by the fused pass: zero it first
+      note(K_MEMSET);
+      if (!dry) {
+        if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+        if ((e = cudaMemsetAsync(lastbits, 0, c.words * sizeof(uint32_t), stream)) != cudaSuccess)
+          return fail_cuda(e, "memset last bitmap");
+        if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      }
+    }
     // pre_l = exclusive scan of agg_l (ones of level l per tile)
     note(K_TSCAN);
     if ((st = scan(wt::OpTilePrefix{agg + (uint64_t)l * c.ntiles, pre}, c.ntiles, "k_scan(tile prefix)")) != WT_OK)
       return st;
-    note(last ? K_LAST : K_LEVEL);
+    note(last ? K_LAST : pair ? K_PAIR : K_LEVEL);
     if (!dry) {
       const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
-      T* o = last ? nullptr : buf[l & 1];
+      T* o = last ? nullptr : pair ? reinterpret_cast<T*>(lastbits) : buf[l & 1];
       const uint32_t sh = L - 1 - l;
       const uint2* t = last ? nullptr : tab + ((1ull << l) - 1);
       uint32_t* bits = out->bitmaps + (uint64_t)l * c.words;
       unsigned long long* sb = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
-      uint32_t* agg_next = last ? nullptr : agg + (uint64_t)(l + 1) * c.ntiles;
+      uint32_t* agg_next = (last || pair) ? nullptr : agg + (uint64_t)(l + 1) * c.ntiles;
       uint32_t* cn = last ? nullptr : cnt[l & 1];
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
       if (last)
-        wt::k_level<T, false><<<grid_last, wt::LV_THREADS, lsmem, stream>>>(
+        wt::k_level<T, 0><<<grid_last, wt::LV_THREADS, lsmem, stream>>>(
+            in, o, (uint32_t)n, (uint32_t)c.ntiles, sh, t, bits, (uint32_t)c.words, sb, (uint32_t)c.nsb, pre,
+            agg_next, cn, flag);
+      else if (pair)
+        wt::k_level<T, 2><<<grid_pair, wt::LV_THREADS, lsmem, stream>>>(
             in, o, (uint32_t)n, (uint32_t)c.ntiles, sh, t, bits, (uint32_t)c.words, sb, (uint32_t)c.nsb, pre,
             agg_next, cn, flag);
       else
-        wt::k_level<T, true><<<grid_sc, wt::LV_THREADS, lsmem, stream>>>(
+        wt::k_level<T, 1><<<grid_sc, wt::LV_THREADS, lsmem, stream>>>(
             in, o, (uint32_t)n, (uint32_t)c.ntiles, sh, t, bits, (uint32_t)c.words, sb, (uint32_t)c.nsb, pre,
             agg_next, cn, flag);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_level");
@@ -321,6 +343,12 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       note(K_SCAN);
       if ((st = scan(wt::OpLeafC{dry ? nullptr : cnt[l & 1], C, 1ull << L, n, nullptr}, 1ull << L, "k_scan(C)")) !=
           WT_OK)
+        return st;
+      // superblocks of level L-1 from the bitmap the fused pass wrote
+      note(K_SBSCAN);
+      unsigned long long* sbl =
+          dry ? nullptr : reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)(L - 1) * c.nsb;
+      if ((st = scan(wt::OpBlockPop{lastbits, sbl, c.nsb - 1}, c.nsb - 1, "k_scan(last-level superblocks)")) != WT_OK)
         return st;
     }
   }

@@ -129,6 +129,29 @@ struct OpLeafC {
   }
 };
 
+// Superblocks of a level from its finished bitmap (the last level, whose
+// bits the fused pass L-2 wrote in place): SB[t] = ones in the 512-bit blocks
+// before t, SB[nblocks] = the level's total (reading R7 of DESIGN.md).
+struct OpBlockPop {
+  const uint32_t* bits;
+  unsigned long long* sb;
+  uint64_t nblocks;
+  __device__ uint64_t load(uint64_t i) const {
+    const uint4* p = reinterpret_cast<const uint4*>(bits + 16 * i);
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint4 q = p[k];
+      c += (uint32_t)(__popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w));
+    }
+    return c;
+  }
+  __device__ void store(uint64_t i, uint64_t excl, uint64_t val) const {
+    sb[i] = excl;
+    if (i + 1 == nblocks) sb[nblocks] = excl + val;
+  }
+};
+
 }  // namespace wt
 
 

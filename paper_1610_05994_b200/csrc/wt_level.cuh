@@ -90,12 +90,18 @@ constexpr size_t level_smem_bytes() {
 
 // ------------------------------------------------------------ the kernel
 // blockDim.x == 32 (one warp per CTA).
-template <typename T, bool SCATTER>
+// MODE 0: level L-1 (bitmap and superblocks only); MODE 1: level l < L-2,
+// also T_{l+1} to `out`; MODE 2: level L-2 fused with level L-1: instead of
+// T_{L-1} it writes B_{L-1} (the last level's bits of T_{L-1}, in T_{L-1}
+// order) to `out` reinterpreted as uint32 words, which must be zero on entry
+// (words shared with other tiles are OR-ed); no next-level tile counts.
+template <typename T, int MODE>
 __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     k_level(const T* __restrict__ in, T* __restrict__ out, uint32_t n32, uint32_t ntiles, uint32_t sh,
             const uint2* __restrict__ tab, uint32_t* __restrict__ bits, uint32_t words_per_level,
             unsigned long long* __restrict__ sb, uint32_t nsb, const uint32_t* __restrict__ pre,
             uint32_t* __restrict__ agg_next, uint32_t* __restrict__ cnt_next, const int32_t* __restrict__ flag) {
+  constexpr bool SCATTER = MODE != 0, BITS = MODE == 2;
   using Cfg = LvTile<T>;
   constexpr int TILE = Cfg::TILE, A = Cfg::A, E = Cfg::E, SPW = Cfg::SPW, XW = Cfg::XW, NH = Cfg::NH;
   constexpr int MARGIN = Cfg::MARGIN, NB = Cfg::NB;
@@ -164,7 +170,9 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     // v holds chunk (v + rot) & 3): lanes 64 bytes apart would otherwise hit
     // the same banks 4-way.  Masks are built in slot order and rotated back.
     constexpr int CS = E / 4;  // symbols per chunk
-    const uint32_t rot = SCATTER ? (lane >> 1) & 3u : 0u;  // (last level: not smem-bound, no rotation)
+    // (not for the last level, which is not smem-bound, nor for MODE 2, whose
+    // one-segment tiles compact the bits from xw[] in position order)
+    const uint32_t rot = (MODE == 1) ? (lane >> 1) & 3u : 0u;
     uint32_t xw[XW];
     {
       const uint4* src = reinterpret_cast<const uint4*>(B + i0);
@@ -335,7 +343,163 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       }
     };
 
-    if (nseg == 1) {
+    // MODE 2: the staged symbols of region [b, b + l) (congruent to HBM
+    // position D mod 16 bytes) -> their last-level bits (bit 0) at bit
+    // positions [D, D + l) of B_{L-1}.  Global word gw covers stage
+    // positions [32 gw - D + b, +32), a 16-byte-aligned window; whole words
+    // are stored, words shared with other regions or tiles are OR-ed.
+    auto emit_bits = [&](int nreg, const int32_t* rb_, const int32_t* rl_, const uint32_t* rD_) {
+      uint32_t* const nbits = reinterpret_cast<uint32_t*>(out);
+      uint32_t wb[LV_NREG], cum[LV_NREG + 1];
+      cum[0] = 0;
+#pragma unroll
+      for (int r = 0; r < LV_NREG; ++r) {
+        const bool live = r < nreg && rl_[r] > 0;
+        wb[r] = rD_[r] / 32u;
+        cum[r + 1] = cum[r] + (live ? (rD_[r] + (uint32_t)rl_[r] - 1u) / 32u - wb[r] + 1u : 0u);
+      }
+      for (uint32_t s0 = 0; s0 < cum[LV_NREG]; s0 += 32) {  // warp-uniform trip count
+        const uint32_t s = s0 + lane;
+        int r = 0;
+#pragma unroll
+        for (int k = 1; k < LV_NREG; ++k) r += s >= cum[k] ? 1 : 0;
+        int32_t b = rb_[0], l = rl_[0];
+        uint32_t D = rD_[0], w0 = wb[0], c0 = cum[0];
+#pragma unroll
+        for (int k = 1; k < LV_NREG; ++k)
+          if (r == k) b = rb_[k], l = rl_[k], D = rD_[k], w0 = wb[k], c0 = cum[k];
+        const uint32_t gw = w0 + (s - c0);
+        const int32_t p = (int32_t)(32u * gw - D) + b;  // stage position of bit 0 of word gw
+        uint32_t word = 0;
+        if (s < cum[LV_NREG]) {
+          constexpr int CH = 32 * (int)sizeof(T) / 16;  // 16-byte chunks per 32 symbols
+          constexpr int PC = 16 / (int)sizeof(T);       // symbols per chunk
+          uint32_t xv[4 * CH];
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const int32_t pc = p + PC * c;
+            uint4 q = make_uint4(0, 0, 0, 0);
+            if (pc + PC > b && pc < b + l) q = *reinterpret_cast<const uint4*>(S.buf[ob] + pc);  // (pc >= 0)
+            xv[4 * c] = q.x, xv[4 * c + 1] = q.y, xv[4 * c + 2] = q.z, xv[4 * c + 3] = q.w;
+          }
+          word = swar_bits<T, 4 * CH, 0>(xv, 0u);
+          const int32_t lo = max(b - p, 0), hi = min(b + l - p, 32);  // valid bits [lo, hi)
+          const uint32_t msk = lowmask((uint32_t)hi) & ~lowmask((uint32_t)lo);
+          word &= msk;
+          if (msk == 0xffffffffu) nbits[gw] = word;
+          else if (word) atomicOr(&nbits[gw], word);
+        }
+      }
+    };
+    if (BITS && nseg == 1) {
+      // ================= MODE 2, one segment (node vF): no symbol moves at
+      // all.  The last-level bits (bit 0) of the tile's zeros, in order, form
+      // the bit run [D0z, D0z + z0) of B_{L-1}, those of its ones the run
+      // [D0o, D0o + o0).  Each lane compacts the bits of its E symbols (the
+      // in-word partition PRMT of phase D, then a multiply gathers bit 0 of
+      // the partitioned symbols), ORs its two strings into a bit stage in the
+      // free output buffer, and the warp stores the runs' words (whole words
+      // plain, the two boundary words of each run OR-ed: other tiles share them).
+      const uint32_t z0 = len - tot, o0 = tot;
+      const uint32_t D0z = T0 - P + tabF.x, D0o = P + tabF.y;
+      uint32_t nol = 0, tbz = 0, tbo = 0;
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        nol += (uint32_t)__popc(m[h]);
+        tbz += (uint32_t)__popc(nbm[h] & ~m[h]);
+        tbo += (uint32_t)__popc(nbm[h] & m[h]);
+      }
+      const uint32_t nzl = nvalid - nol, rz = i0 - mypre, ro = mypre;
+      const uint32_t red = __reduce_add_sync(FULL, tbz | (tbo << 16));
+      const uint32_t c01 = red & 0xffffu, c11 = red >> 16;
+#ifndef WT_EXP_SKIP_PCOUNT
+      if (vF != cc_node) {
+        cc_flush();
+        cc_node = vF;
+      }
+      {
+        const uint32_t cx = (lane & 2u) ? c11 : c01;
+        cc_acc += (lane & 1u) ? cx : ((lane & 2u) ? o0 : z0) - cx;
+      }
+#endif
+      // compaction: strings of the zeros' / ones' bits, 32 symbols per half
+      constexpr int HW = (XW + NH - 1) / NH;  // words per half
+      uint32_t Zh[NH], Oh[NH], nzh[NH];
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        uint32_t Zs = 0, Os = 0, zp = 0, op = 0;
+#pragma unroll
+        for (int kk = 0; kk < HW; ++kk) {
+          const int k = h * HW + kk;
+          if constexpr (SPW == 1) {
+            const uint32_t b = (m[h] >> kk) & 1u, g = xw[k] & 1u;
+            Zs |= (b ? 0u : g) << zp;
+            Os |= (b ? g : 0u) << op;
+            zp += 1u - b;
+            op += b;
+          } else {
+            const uint32_t m4 = (m[h] >> (SPW * kk)) & ((1u << SPW) - 1u);
+            const uint32_t e = S.lut[m4].x, nz = e >> 16;
+            uint32_t y;
+            asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(xw[k]), "r"(e));
+            uint32_t g;  // bit 0 of the partitioned symbols, slot j at bit j
+            if constexpr (SPW == 4) g = ((y & 0x01010101u) * 0x10204080u) >> 28;
+            else g = (y & 1u) | ((y >> 15) & 2u);
+            Zs |= (g & ((1u << nz) - 1u)) << zp;
+            Os |= (g >> nz) << op;
+            zp += nz;
+            op += SPW - nz;
+          }
+        }
+        Zh[h] = Zs, Oh[h] = Os, nzh[h] = zp;
+      }
+      // 64-bit strings (low, high).  Positions past the tile end (m = 0)
+      // count as zeros after every valid zero: the zero string is cut to nzl
+      uint32_t Z[2], O[2];
+      if constexpr (NH == 2) {
+        Z[0] = Zh[0] | __funnelshift_lc(0u, Zh[1], nzh[0]);
+        Z[1] = __funnelshift_lc(Zh[1], 0u, nzh[0]);
+        const uint32_t noh0 = (uint32_t)__popc(m[0]);
+        O[0] = Oh[0] | __funnelshift_lc(0u, Oh[1], noh0);
+        O[1] = __funnelshift_lc(Oh[1], 0u, noh0);
+      } else {
+        Z[0] = Zh[0], Z[1] = 0, O[0] = Oh[0], O[1] = 0;
+      }
+      Z[0] &= lowmask(nzl);
+      Z[1] &= lowmask(nzl > 32u ? nzl - 32u : 0u);
+      // bit stage in the output buffer: zero-run words [0, WZ), one-run words [WZ, 2 WZ)
+      constexpr uint32_t WZ = TILE / 32 + 2;
+      uint32_t* const st = reinterpret_cast<uint32_t*>(S.buf[ob]);
+      for (uint32_t j = lane; j < 2 * WZ; j += 32) st[j] = 0;
+      __syncwarp();
+      auto put = [&](uint32_t base, uint32_t pos, const uint32_t (&v)[2], uint32_t nb) {  // nb bits of v at bit pos
+        if (nb == 0) return;
+        const uint32_t j = pos >> 5, off = pos & 31u;
+        const uint32_t w0 = v[0] << off;
+        const uint32_t w1 = __funnelshift_lc(v[0], v[1], off);
+        const uint32_t w2 = __funnelshift_lc(v[1], 0u, off);
+        if (w0) atomicOr(&st[base + j], w0);
+        if (w1) atomicOr(&st[base + j + 1], w1);
+        if (w2) atomicOr(&st[base + j + 2], w2);
+      };
+      put(0, (D0z & 31u) + rz, Z, nzl);
+      put(WZ, (D0o & 31u) + ro, O, nol);
+      __syncwarp();
+      uint32_t* const nbits = reinterpret_cast<uint32_t*>(out);
+      auto emit_run = [&](uint32_t base, uint32_t D, uint32_t l) {
+        if (l == 0) return;
+        const uint32_t nw = ((D & 31u) + l + 31u) / 32u;
+        const bool head_full = (D & 31u) == 0, tail_full = ((D + l) & 31u) == 0;
+        for (uint32_t j = lane; j < nw; j += 32) {
+          const uint32_t wv = st[base + j];
+          const bool full = (j > 0 || head_full) && (j + 1 < nw || tail_full);
+          if (full) nbits[D / 32u + j] = wv;
+          else if (wv) atomicOr(&nbits[D / 32u + j], wv);
+        }
+      };
+      emit_run(0, D0z, z0);
+      emit_run(WZ, D0o, o0);
+    } else if (nseg == 1) {
       // ================= one segment: the whole tile lies in node vF.  Zeros
       // go to D0z.., ones to D0o..; staged at b1 / b2 (congruent mod 16 B)
       {
@@ -447,6 +611,11 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         }
         return c;
       };
+      if constexpr (BITS) {  // the two runs' last-level bits
+        const int32_t rb2[2] = {(int32_t)b1, (int32_t)b2}, rl2[2] = {(int32_t)z0, (int32_t)o0};
+        const uint32_t rD2[2] = {D0z, D0o};
+        emit_bits(2, rb2, rl2, rD2);
+      } else {
       if (splz) Lz += window(b1, sz0, kz);
       if (splo) Lo += window(b2, so0, ko);
       // ---------------- phase E: lanes 0 / 1 bulk-store the two runs' aligned
@@ -472,6 +641,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         const uint32_t v = lane == 0 ? Lz : lane == 1 ? c01 - Lz : lane == 2 ? Lo : c11 - Lo;
         if (v) atomicAdd(&agg_next[(lane < 2 ? D0z : D0o) / TILE + (lane & 1)], v);
       }
+      }  // !BITS
     } else {
       // ================= several segments
 
@@ -550,7 +720,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       // ---------------- next-level ones per (region, destination tile), lane-owned symbols
       uint32_t mycnt = 0;  // lane k < LV_NKEY: count of key k = 2 r + half
 #ifndef WT_EXP_SKIP_COUNT
-      {
+      if constexpr (!BITS) {
         // count of nbm bits among the set bits of M, split at rank k (the set
         // bits of M have ranks rank0, rank0+1, ... in position order).  Only
         // the lane holding rank k searches for its k-th set bit.
@@ -775,7 +945,9 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
 #endif
       fence_proxy_async_smem();
       __syncwarp();  // stage partitioned (and the input buffer fully read)
-
+      if constexpr (BITS) {
+        emit_bits(LV_NREG, rb, rl, rD);
+      } else {
       // ---------------- phase E: TMA bulk stores of the aligned bodies, element stores of the edges
       auto emit_region = [&](int32_t b, int32_t l, uint32_t D) {  // stage [b, b+l) -> HBM [D, D+l)
         if (l <= 0) return;  // warp-uniform
@@ -831,6 +1003,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         if (!one) D = r == 3 ? Dmz : r == 4 ? Dmo : D;
         atomicAdd(&agg_next[r == 0 ? tile : D / TILE + (lane & 1)], mycnt);
       }
+      }  // !BITS
     }
     // the previous tile's output buffer: once its bulk stores have read it, load a new tile into it
     if (lane < (uint32_t)LV_NREG) bulk_wait_read<1>();  // each lane's own groups

@@ -84,9 +84,12 @@ def test_build_validates_before_touching_the_device(wt):
 def test_launch_plan(wt):
     lv = ["tables", "memset", "tile_scan", "level"]
     last = ["tile_scan", "last_level"]
-    assert wt.launch_plan(1 << 20, 256, 1) == (["prologue", "tables", "memset", "tile_scan", "level"] + lv * 6
-                                               + ["scan"] + last)
-    assert wt.launch_plan(1 << 20, 4, 1) == ["prologue", "tables", "memset", "tile_scan", "level", "scan"] + last
+    # pass L-2 is fused with level L-1: it writes B_{L-1} (zeroed first), then C and the last superblocks
+    pair = ["memset", "memset", "tile_scan", "pair", "scan", "sb_scan"]
+    assert wt.launch_plan(1 << 20, 256, 1) == (["prologue", "tables", "memset", "tile_scan", "level"] + lv * 5
+                                               + ["tables"] + pair)
+    assert wt.launch_plan(1 << 20, 4, 1) == ["prologue", "tables"] + pair
+    assert wt.launch_plan(1 << 20, 8, 1) == ["prologue", "tables", "memset", "tile_scan", "level", "tables"] + pair
     assert wt.launch_plan(100, 2, 1) == ["prologue", "scan"] + last
     assert wt.launch_plan(100, 1, 1) == ["prologue", "scan"]
     assert wt.launch_plan(0, 16, 1) == []

@@ -21,13 +21,16 @@ def kind_of(name: str) -> str:
     if "k_prologue" in name:
         return "prologue"
     if "k_level" in name:
-        return "level" if ", 1>(" in name else "last_level"
+        return {", 1>(": "level", ", 2>(": "pair"}.get(next((k for k in (", 1>(", ", 2>(") if k in name), ""),
+                                                          "last_level")
     if "OpTilePrefix" in name:
         return "tile_scan"
     if "OpLevelTab" in name:
         return "tables"
     if "OpLeafC" in name:
         return "scan"
+    if "OpBlockPop" in name:
+        return "sb_scan"
     return "other(" + re.sub(r"\(.*", "", name)[:40] + ")"
 
 
@@ -103,9 +106,13 @@ def main():
             lines.append("  " + json.dumps(r))
         lvl = [r for r in fc if "k_level" in r["kernel"]]
         if lvl:
-            traffic = lvl[0]["dram_read"] + lvl[0]["dram_write"]
+            traffic = {}
+            for r in lvl:
+                kd = "pair" if ", 2>" in r["kernel"] else "level" if ", 1>" in r["kernel"] else "last_level"
+                traffic.setdefault(kd, r["dram_read"] + r["dram_write"])
+            traffic["_source"] = f"profiles/{tag}/ncu_summary_cfg{cfg}.txt"
             with open(os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cfg}.json"), "w") as f:
-                json.dump({"level": traffic, "_source": f"profiles/{tag}/ncu_summary_cfg{cfg}.txt"}, f)
+                json.dump(traffic, f)
     with open(os.path.join(outdir, f"ncu_summary_cfg{cfg}.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
     print("\n".join(lines))

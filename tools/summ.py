@@ -7,4 +7,4 @@ for c in sys.argv[1:]:
         print("   %-11s n=%2d ms=%.3f share=%.2f GBps=%.0f" % (k, v["launches_per_step"], v["ms_per_step"], v["share"], v["algorithmic_GBps"]))
     if "-v" in sys.argv[0:1]:
         pass
-    pl = d["per_launch_ms"]; print("   per launch:", " ".join("%s:%.3f" % (p[:2], x) for p, x in zip(d["plan"], pl) if p in ("level", "last_level", "hist")))
+    pl = d["per_launch_ms"]; print("   per launch:", " ".join("%s:%.3f" % (p[:2], x) for p, x in zip(d["plan"], pl) if p in ("level", "last_level", "pair", "hist")))
