@@ -213,11 +213,12 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       m[0] = mm;
       nbm[0] = SCATTER ? __funnelshift_l(nn, nn, 1) & 0xffffu : 0u;  // next level's bits
     } else {
+      // (MODE 2: the next level's bits only on multi-segment tiles, below)
       m[0] = swar_bits<T, XW / NH, 0>(xw, sh);
-      nbm[0] = SCATTER ? swar_bits<T, XW / NH, 0>(xw, sh - 1) : 0u;  // next level's bits
+      nbm[0] = MODE == 1 ? swar_bits<T, XW / NH, 0>(xw, sh - 1) : 0u;  // next level's bits
       if constexpr (NH == 2) {
         m[NH - 1] = swar_bits<T, XW / 2, XW / 2>(xw, sh);
-        nbm[NH - 1] = SCATTER ? swar_bits<T, XW / 2, XW / 2>(xw, sh - 1) : 0u;
+        nbm[NH - 1] = MODE == 1 ? swar_bits<T, XW / 2, XW / 2>(xw, sh - 1) : 0u;
       }
     }
     unrot(m);
@@ -402,26 +403,10 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       // plain, the two boundary words of each run OR-ed: other tiles share them).
       const uint32_t z0 = len - tot, o0 = tot;
       const uint32_t D0z = T0 - P + tabF.x, D0o = P + tabF.y;
-      uint32_t nol = 0, tbz = 0, tbo = 0;
+      uint32_t nol = 0;
 #pragma unroll
-      for (int h = 0; h < NH; ++h) {
-        nol += (uint32_t)__popc(m[h]);
-        tbz += (uint32_t)__popc(nbm[h] & ~m[h]);
-        tbo += (uint32_t)__popc(nbm[h] & m[h]);
-      }
+      for (int h = 0; h < NH; ++h) nol += (uint32_t)__popc(m[h]);
       const uint32_t nzl = nvalid - nol, rz = i0 - mypre, ro = mypre;
-      const uint32_t red = __reduce_add_sync(FULL, tbz | (tbo << 16));
-      const uint32_t c01 = red & 0xffffu, c11 = red >> 16;
-#ifndef WT_EXP_SKIP_PCOUNT
-      if (vF != cc_node) {
-        cc_flush();
-        cc_node = vF;
-      }
-      {
-        const uint32_t cx = (lane & 2u) ? c11 : c01;
-        cc_acc += (lane & 1u) ? cx : ((lane & 2u) ? o0 : z0) - cx;
-      }
-#endif
       // compaction: strings of the zeros' / ones' bits, 32 symbols per half
       constexpr int HW = (XW + NH - 1) / NH;  // words per half
       uint32_t Zh[NH], Oh[NH], nzh[NH];
@@ -467,10 +452,24 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       }
       Z[0] &= lowmask(nzl);
       Z[1] &= lowmask(nzl > 32u ? nzl - 32u : 0u);
+      // progressive counting: (b, nb) pair counts of node vF from the strings
+      const uint32_t red = __reduce_add_sync(
+          FULL, (uint32_t)(__popc(Z[0]) + __popc(Z[1])) | ((uint32_t)(__popc(O[0]) + __popc(O[1])) << 16));
+      const uint32_t c01 = red & 0xffffu, c11 = red >> 16;
+#ifndef WT_EXP_SKIP_PCOUNT
+      if (vF != cc_node) {
+        cc_flush();
+        cc_node = vF;
+      }
+      {
+        const uint32_t cx = (lane & 2u) ? c11 : c01;
+        cc_acc += (lane & 1u) ? cx : ((lane & 2u) ? o0 : z0) - cx;
+      }
+#endif
       // bit stage in the output buffer: zero-run words [0, WZ), one-run words [WZ, 2 WZ)
-      constexpr uint32_t WZ = TILE / 32 + 2;
+      constexpr uint32_t WZ = (TILE / 32 + 2 + 3) & ~3u;  // (a multiple of 4 words: 16-byte zeroing)
       uint32_t* const st = reinterpret_cast<uint32_t*>(S.buf[ob]);
-      for (uint32_t j = lane; j < 2 * WZ; j += 32) st[j] = 0;
+      for (uint32_t j = lane; j < 2 * WZ / 4; j += 32) reinterpret_cast<uint4*>(st)[j] = make_uint4(0, 0, 0, 0);
       __syncwarp();
       auto put = [&](uint32_t base, uint32_t pos, const uint32_t (&v)[2], uint32_t nb) {  // nb bits of v at bit pos
         if (nb == 0) return;
@@ -486,19 +485,18 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       put(WZ, (D0o & 31u) + ro, O, nol);
       __syncwarp();
       uint32_t* const nbits = reinterpret_cast<uint32_t*>(out);
-      auto emit_run = [&](uint32_t base, uint32_t D, uint32_t l) {
-        if (l == 0) return;
-        const uint32_t nw = ((D & 31u) + l + 31u) / 32u;
-        const bool head_full = (D & 31u) == 0, tail_full = ((D + l) & 31u) == 0;
-        for (uint32_t j = lane; j < nw; j += 32) {
-          const uint32_t wv = st[base + j];
-          const bool full = (j > 0 || head_full) && (j + 1 < nw || tail_full);
-          if (full) nbits[D / 32u + j] = wv;
-          else if (wv) atomicOr(&nbits[D / 32u + j], wv);
-        }
-      };
-      emit_run(0, D0z, z0);
-      emit_run(WZ, D0o, o0);
+      // the two runs' words as one lane-parallel list: zero-run words [0, nwz), then one-run words
+      const uint32_t nwz = z0 ? ((D0z & 31u) + z0 + 31u) / 32u : 0u;
+      const uint32_t nwo = o0 ? ((D0o & 31u) + o0 + 31u) / 32u : 0u;
+      for (uint32_t s = lane; s < nwz + nwo; s += 32) {
+        const bool one_run = s >= nwz;
+        const uint32_t j = one_run ? s - nwz : s, nw = one_run ? nwo : nwz;
+        const uint32_t D = one_run ? D0o : D0z, l = one_run ? o0 : z0;
+        const uint32_t wv = st[(one_run ? WZ : 0u) + j];
+        const bool full = (j > 0 || (D & 31u) == 0) && (j + 1 < nw || ((D + l) & 31u) == 0);
+        if (full) nbits[D / 32u + j] = wv;
+        else if (wv) atomicOr(&nbits[D / 32u + j], wv);
+      }
     } else if (nseg == 1) {
       // ================= one segment: the whole tile lies in node vF.  Zeros
       // go to D0z.., ones to D0o..; staged at b1 / b2 (congruent mod 16 B)
@@ -644,6 +642,10 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       }  // !BITS
     } else {
       // ================= several segments
+      if constexpr (MODE == 2 && sizeof(T) != 4) {  // the next level's bits (phase A skipped them)
+        nbm[0] = swar_bits<T, XW / NH, 0>(xw, sh - 1) & vm[0];
+        if constexpr (NH == 2) nbm[NH - 1] = swar_bits<T, XW / 2, XW / 2>(xw, sh - 1) & vm[NH - 1];
+      }
 
       {
         uint32_t po = mypre, ph = hpre;
