@@ -173,7 +173,7 @@ wt_status wt_select(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uin
  * only when L = 1), 6 tile-prefix scan, 7 memset (a node-count buffer, or the
  * last level's bitmap before pass 8), 8 level pass L-2 fused with level L-1
  * (a5 with k = 2: writes B_{L-2} and B_{L-1}, no T_{L-1}), 9 superblock scan
- * of level L-1 over its bitmap. */
+ * of level L-1 over its per-block ones, 10 per-block ones of level L-1. */
 uint32_t wt_launch_plan(uint64_t n, uint64_t sigma, uint32_t width, uint32_t* kinds, uint32_t cap);
 
 /* Debug aid: byte offsets inside the workspace of wt_build_async(n, sigma,

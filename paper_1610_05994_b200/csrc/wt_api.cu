@@ -87,7 +87,7 @@ struct Carve {
   uint64_t words = 0, nsb = 0, c_len = 0, ntiles = 0;
   uint64_t status_entries = 0, tab_entries = 0, cnt_entries = 0;
   size_t off_flag = 0, off_counters = 0, off_ones0 = 0, off_status = 0, off_value = 0, off_agg = 0, ctrl_bytes = 0;
-  size_t off_pre = 0, off_tab = 0, off_cnt = 0, off_bufA = 0, off_bufB = 0, total = 0;
+  size_t off_pre = 0, off_tab = 0, off_cnt = 0, off_blk = 0, off_bufA = 0, off_bufB = 0, total = 0;
   // host-API extras (after total)
   size_t off_seq = 0, off_bits = 0, off_sb = 0, off_c = 0, host_total = 0;
 };
@@ -125,11 +125,14 @@ Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
   o += align_up(c.tab_entries * sizeof(uint2));
   c.off_cnt = o;
   o += 2 * align_up(c.cnt_entries * sizeof(uint32_t));
+  c.off_blk = o;  // ones per 512-bit block of the last level (its superblock scan)
+  if (c.L >= 2) o += align_up((c.nsb - 1) * sizeof(uint32_t));
   const size_t seq_bytes = align_up(n * width);
+  // T_1 .. T_{L-2} (the fused pass L-2 writes no T_{L-1})
   c.off_bufA = o;
-  if (c.L >= 2) o += seq_bytes;  // T_1, T_3, ...
+  if (c.L >= 3) o += seq_bytes;  // T_1, T_3, ...
   c.off_bufB = o;
-  if (c.L >= 3) o += seq_bytes;  // T_2, T_4, ...
+  if (c.L >= 4) o += seq_bytes;  // T_2, T_4, ...
   c.total = o;
   c.off_seq = o;
   o += seq_bytes;
@@ -182,7 +185,8 @@ struct Launcher {
 };
 
 enum Kind : uint32_t {
-  K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7, K_PAIR = 8, K_SBSCAN = 9
+  K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7, K_PAIR = 8, K_SBSCAN = 9,
+  K_BLKPOP = 10
 };
 
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
@@ -345,10 +349,21 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
           WT_OK)
         return st;
       // superblocks of level L-1 from the bitmap the fused pass wrote
+      uint32_t* blk = reinterpret_cast<uint32_t*>(ws + c.off_blk);
+      note(K_BLKPOP);
+      if (!dry) {
+        if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+        const uint64_t nbk = c.nsb - 1, warps = (nbk + 31) / 32;
+        const uint32_t g = (uint32_t)std::max<uint64_t>(
+            1, std::min<uint64_t>((warps + wt::BP_THREADS / 32 - 1) / (wt::BP_THREADS / 32), 16ull * num_sms()));
+        wt::k_block_pop<<<g, wt::BP_THREADS, 0, stream>>>(lastbits, blk, nbk, flag);
+        if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_block_pop");
+        if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      }
       note(K_SBSCAN);
       unsigned long long* sbl =
           dry ? nullptr : reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)(L - 1) * c.nsb;
-      if ((st = scan(wt::OpBlockPop{lastbits, sbl, c.nsb - 1}, c.nsb - 1, "k_scan(last-level superblocks)")) != WT_OK)
+      if ((st = scan(wt::OpBlockPop{blk, sbl, c.nsb - 1}, c.nsb - 1, "k_scan(last-level superblocks)")) != WT_OK)
         return st;
     }
   }

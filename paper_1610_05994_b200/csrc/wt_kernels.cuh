@@ -132,20 +132,43 @@ struct OpLeafC {
 // Superblocks of a level from its finished bitmap (the last level, whose
 // bits the fused pass L-2 wrote in place): SB[t] = ones in the 512-bit blocks
 // before t, SB[nblocks] = the level's total (reading R7 of DESIGN.md).
+// Two steps: k_block_pop writes the per-block ones (coalesced: a warp reads 32
+// blocks = 2 KiB as consecutive 16-byte chunks), then a scan of the counts.
+constexpr int BP_THREADS = 256;
+__global__ void __launch_bounds__(BP_THREADS) k_block_pop(const uint32_t* __restrict__ bits, uint32_t* __restrict__ cnt,
+                                                          uint64_t nblocks, const int32_t* __restrict__ flag) {
+  if (*flag) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (BP_THREADS / 32);
+  const uint4* src = reinterpret_cast<const uint4*>(bits);
+  for (uint64_t wb = (uint64_t)blockIdx.x * (BP_THREADS / 32) + (threadIdx.x >> 5); wb * 32 < nblocks; wb += nw) {
+    uint32_t c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // chunk lane + 32 k of the warp's 128 = block 8 k + lane / 4
+      const uint64_t ch = wb * 128 + lane + 32 * k;
+      c[k] = 0;
+      if (ch < 4 * nblocks) {
+        const uint4 q = ldg_nc_v4(src + ch);
+        c[k] = (uint32_t)(__popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w));
+      }
+      c[k] += __shfl_xor_sync(FULL, c[k], 1);
+      c[k] += __shfl_xor_sync(FULL, c[k], 2);
+    }
+    if ((lane & 3) == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t b = wb * 32 + 8 * k + lane / 4;
+        if (b < nblocks) cnt[b] = c[k];
+      }
+    }
+  }
+}
+
 struct OpBlockPop {
-  const uint32_t* bits;
+  const uint32_t* cnt;  // ones per 512-bit block (k_block_pop)
   unsigned long long* sb;
   uint64_t nblocks;
-  __device__ uint64_t load(uint64_t i) const {
-    const uint4* p = reinterpret_cast<const uint4*>(bits + 16 * i);
-    uint32_t c = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint4 q = p[k];
-      c += (uint32_t)(__popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w));
-    }
-    return c;
-  }
+  __device__ uint64_t load(uint64_t i) const { return cnt[i]; }
   __device__ void store(uint64_t i, uint64_t excl, uint64_t val) const {
     sb[i] = excl;
     if (i + 1 == nblocks) sb[nblocks] = excl + val;

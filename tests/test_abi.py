@@ -48,9 +48,11 @@ def test_sizes(wt):
     s = wt.sizes(1 << 28, 1 << 24, 4)
     assert s.levels == 24 and s.words_per_level == (1 << 28) // 32 and s.sb_per_level == (1 << 19) + 1
     assert s.bitmap_bytes == 24 * (1 << 23) * 4 and s.superblock_bytes == 24 * ((1 << 19) + 1) * 8
-    # two ping-pong permuted copies of the sequence at most, plus node tables,
-    # two 2^L uint32 node-count buffers and per-tile counts
+    # two ping-pong permuted copies of the sequence at most (T_1..T_{L-2}), plus
+    # node tables, two 2^L uint32 node-count buffers, per-tile and per-block counts
     assert 2 * (1 << 30) <= s.workspace_bytes < 2 * (1 << 30) + 450 * (1 << 20)
+    assert wt.sizes(1 << 20, 4, 1).workspace_bytes < 1 << 20   # L=2: the fused pass writes no permuted copy
+    assert wt.sizes(1 << 20, 8, 1).workspace_bytes > 1 << 20   # L=3: T_1
     assert s.host_workspace_bytes > s.workspace_bytes + (1 << 30)
     assert wt.sizes(5, 1, 1).levels == 0
     assert wt.sizes(5, 2, 1).workspace_bytes < 1 << 20   # L=1: no permuted copy
@@ -85,7 +87,7 @@ def test_launch_plan(wt):
     lv = ["tables", "memset", "tile_scan", "level"]
     last = ["tile_scan", "last_level"]
     # pass L-2 is fused with level L-1: it writes B_{L-1} (zeroed first), then C and the last superblocks
-    pair = ["memset", "memset", "tile_scan", "pair", "scan", "sb_scan"]
+    pair = ["memset", "memset", "tile_scan", "pair", "scan", "block_pop", "sb_scan"]
     assert wt.launch_plan(1 << 20, 256, 1) == (["prologue", "tables", "memset", "tile_scan", "level"] + lv * 5
                                                + ["tables"] + pair)
     assert wt.launch_plan(1 << 20, 4, 1) == ["prologue", "tables"] + pair

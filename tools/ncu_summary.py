@@ -31,6 +31,8 @@ def kind_of(name: str) -> str:
         return "scan"
     if "OpBlockPop" in name:
         return "sb_scan"
+    if "k_block_pop" in name:
+        return "block_pop"
     return "other(" + re.sub(r"\(.*", "", name)[:40] + ")"
 
 
