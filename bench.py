@@ -67,13 +67,15 @@ def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
         return n * w
     if kind == "scan":        # node_offsets: read 2^L uint32 leaf counts, write 2^L + 1 uint64
         return 4 * (1 << L) + 8 * ((1 << L) + 1)
-    if kind == "tile_scan":
+    if kind in ("prep", "tile_scan"):  # tile prefixes (read agg, write pre), node tables, zeroed counts; avg per launch
         tile = {1: 2048, 2: 1024, 4: 512}[w]
-        return 12 * ((n + tile - 1) // tile)
-    if kind == "tables":      # level l: read 2^(l+1) uint32 counts, write 2^l {ob, Zn}; average per launch
-        return sum(4 * (2 << l) + 16 * (1 << l) for l in range(max(L - 1, 0))) // max(L - 1, 1)
-    if kind == "memset":      # zero 2^(l+2) uint32 counts before pass l, and B_{L-1}; average per launch
-        return (sum(4 * (4 << l) for l in range(max(L - 1, 0))) + bitmap) // L
+        tiles = (n + tile - 1) // tile
+        levels = max(L - 1, 1)
+        tables = sum(4 * (2 << l) + 8 * (1 << l) for l in range(max(L - 1, 0)))
+        zero = sum(16 * (1 << l) for l in range(max(L - 1, 0))) + (bitmap if L >= 2 else 0)
+        return 8 * tiles + (tables + zero) // levels
+    if kind == "final_scan":  # last-level superblocks from the block counts, C from the leaf counts
+        return 4 * (nsb - 1) + 8 * nsb + 4 * (1 << L) + 8 * ((1 << L) + 1)
     return 0
 
 

@@ -87,6 +87,7 @@ struct Carve {
   uint64_t words = 0, nsb = 0, c_len = 0, ntiles = 0;
   uint64_t status_entries = 0, tab_entries = 0, cnt_entries = 0;
   size_t off_flag = 0, off_counters = 0, off_ones0 = 0, off_status = 0, off_value = 0, off_agg = 0, ctrl_bytes = 0;
+  size_t off_status2 = 0, off_value2 = 0;  // a second look-back state (two scans per k_prep launch)
   size_t off_pre = 0, off_tab = 0, off_cnt = 0, off_blk = 0, off_bufA = 0, off_bufB = 0, total = 0;
   // host-API extras (after total)
   size_t off_seq = 0, off_bits = 0, off_sb = 0, off_c = 0, host_total = 0;
@@ -114,10 +115,14 @@ Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
   o += ALIGN;
   c.off_status = o;
   o += align_up(c.status_entries * sizeof(uint32_t));
+  c.off_status2 = o;
+  o += align_up(c.status_entries * sizeof(uint32_t));
   c.off_agg = o;
   o += align_up((size_t)c.L * c.ntiles * sizeof(uint32_t));
   c.ctrl_bytes = o;
   c.off_value = o;  // look-back values: written before their status, never read stale
+  o += align_up(2 * c.status_entries * sizeof(uint64_t));
+  c.off_value2 = o;
   o += align_up(2 * c.status_entries * sizeof(uint64_t));
   c.off_pre = o;
   o += align_up(c.ntiles * sizeof(uint32_t));
@@ -186,7 +191,7 @@ struct Launcher {
 
 enum Kind : uint32_t {
   K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7, K_PAIR = 8, K_SBSCAN = 9,
-  K_BLKPOP = 10
+  K_BLKPOP = 10, K_PREP = 11, K_FINAL = 12
 };
 
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
@@ -204,6 +209,8 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   unsigned long long* ones0 = reinterpret_cast<unsigned long long*>(ws + c.off_ones0);
   const wt::LookbackState status{reinterpret_cast<uint32_t*>(ws + c.off_status),
                                  reinterpret_cast<uint64_t*>(ws + c.off_value), c.status_entries};
+  const wt::LookbackState status2{reinterpret_cast<uint32_t*>(ws + c.off_status2),
+                                  reinterpret_cast<uint64_t*>(ws + c.off_value2), c.status_entries};
   uint2* tab = reinterpret_cast<uint2*>(ws + c.off_tab);
   uint32_t* agg = reinterpret_cast<uint32_t*>(ws + c.off_agg);
   uint32_t* pre = reinterpret_cast<uint32_t*>(ws + c.off_pre);
@@ -255,15 +262,33 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_prologue");
     if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
   }
+  // one k_prep launch: scan A (look-back state 1), scan B (state 2), zero fills
+  auto prep = [&](uint32_t kind, auto opA, uint64_t na, auto opB, uint64_t nb, wt::ZeroFill z,
+                  const char* what) -> wt_status {
+    note(kind);
+    if (!dry) {
+      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      const uint64_t ga = (na + wt::SCAN_TILE - 1) / wt::SCAN_TILE, gb = (nb + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
+      const uint64_t zu = z.n0 + z.n1;
+      const uint64_t gz = zu ? std::min<uint64_t>((zu + 4 * wt::SCAN_THREADS - 1) / (4 * wt::SCAN_THREADS),
+                                                  2ull * num_sms())
+                             : (ga + gb ? 0 : 1);
+      wt::k_prep<decltype(opA), decltype(opB)><<<(uint32_t)(ga + gb + gz), wt::SCAN_THREADS, 0, stream>>>(
+          opA, na, status, counters + counter, epoch, opB, nb, status2, counters + counter + 1, epoch + 1, z, flag);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, what);
+      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    }
+    epoch += 2;
+    counter += 2;
+    return WT_OK;
+  };
+  const wt::ZeroFill nozero{nullptr, 0, nullptr, 0};
+
   if (L == 0) {  // sigma = 1: C = [0, n]
     note(K_SCAN);
     if ((st = scan(wt::OpLeafC{nullptr, C, 1, n, nullptr}, 1, "k_scan(C)")) != WT_OK) return st;
-  } else if (L == 1) {
-    note(K_SCAN);
-    if ((st = scan(wt::OpLeafC{nullptr, C, 2, n, ones0}, 2, "k_scan(C)")) != WT_OK) return st;
-  } else {
-    note(K_TABLES);
-    if ((st = scan(wt::OpLevelTab{nullptr, tab, n, ones0}, 1, "k_scan(level-0 table)")) != WT_OK) return st;
+    if (count) *count = nk;
+    return WT_OK;
   }
 
   // a3 / a4: one pass per level
@@ -279,93 +304,84 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   const uint32_t grid_sc = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_sc * (uint64_t)num_sms());
   const uint32_t grid_last = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_last * (uint64_t)num_sms());
   const uint32_t grid_pair = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_pair * (uint64_t)num_sms());
+  auto level = [&](uint32_t l, int mode) -> wt_status {
+    note(mode == 0 ? K_LAST : mode == 2 ? K_PAIR : K_LEVEL);
+    if (dry) return WT_OK;
+    const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
+    T* o = mode == 0 ? nullptr : mode == 2 ? reinterpret_cast<T*>(out->bitmaps + (uint64_t)(L - 1) * c.words)
+                                           : buf[l & 1];
+    const uint32_t sh = L - 1 - l;
+    const uint2* t = mode == 0 ? nullptr : tab + ((1ull << l) - 1);
+    uint32_t* bits = out->bitmaps + (uint64_t)l * c.words;
+    unsigned long long* sb = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
+    uint32_t* agg_next = mode == 1 ? agg + (uint64_t)(l + 1) * c.ntiles : nullptr;
+    uint32_t* cn = mode == 0 ? nullptr : cnt[l & 1];
+    if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    const uint32_t n32 = (uint32_t)n, nt32 = (uint32_t)c.ntiles, w32 = (uint32_t)c.words, nsb32 = (uint32_t)c.nsb;
+    if (mode == 0)
+      wt::k_level<T, 0><<<grid_last, wt::LV_THREADS, lsmem, stream>>>(in, o, n32, nt32, sh, t, bits, w32, sb, nsb32,
+                                                                      pre, agg_next, cn, flag);
+    else if (mode == 2)
+      wt::k_level<T, 2><<<grid_pair, wt::LV_THREADS, lsmem, stream>>>(in, o, n32, nt32, sh, t, bits, w32, sb, nsb32,
+                                                                      pre, agg_next, cn, flag);
+    else
+      wt::k_level<T, 1><<<grid_sc, wt::LV_THREADS, lsmem, stream>>>(in, o, n32, nt32, sh, t, bits, w32, sb, nsb32,
+                                                                    pre, agg_next, cn, flag);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_level");
+    if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    return WT_OK;
+  };
+
+  if (L == 1) {  // C from ones0, the tile prefixes of level 0, the single (last) level
+    if ((st = prep(K_PREP, wt::OpTilePrefix{agg, pre}, c.ntiles, wt::OpLeafC{nullptr, C, 2, n, ones0}, 2, nozero,
+                   "k_prep")) != WT_OK)
+      return st;
+    if ((st = level(0, 0)) != WT_OK) return st;
+    if (count) *count = nk;
+    return WT_OK;
+  }
 #ifdef WT_EXP_LEVELS  // experiment builds: only the first level passes (timing studies)
-  const uint32_t Lrun = std::min<uint32_t>(L, WT_EXP_LEVELS);
+  const uint32_t Lrun = std::min<uint32_t>(L - 1, WT_EXP_LEVELS);
 #else
-  const uint32_t Lrun = L;
+  const uint32_t Lrun = L - 1;
 #endif
   // L >= 2: passes 0..L-3 write T_{l+1}; pass L-2 is fused with level L-1
-  // (writes B_{L-1} directly, no T_{L-1}); L = 1: the single last-level pass
-  for (uint32_t l = 0; l < Lrun && (L == 1 || l + 1 < L); ++l) {
-    const bool last = (l + 1 == L);
+  // (writes B_{L-1} directly, no T_{L-1})
+  uint32_t* const lastbits = dry ? nullptr : out->bitmaps + (uint64_t)(L - 1) * c.words;
+  for (uint32_t l = 0; l < Lrun; ++l) {
     const bool pair = (l + 2 == L);
-    if (!last && l >= 1) {  // node tables of level l from the level-(l+1) node sizes counted by pass l-1
-      note(K_TABLES);
-      wt::OpLevelTab op{dry ? nullptr : cnt[(l - 1) & 1], tab + ((1ull << l) - 1), n, nullptr};
-      if ((st = scan(op, 1ull << l, "k_scan(level table)")) != WT_OK) return st;
-    }
-    if (!last) {  // pass l counts the level-(l+2) node sizes into cnt[l % 2]
-      note(K_MEMSET);
-      if (!dry) {
-        if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-        if ((e = cudaMemsetAsync(cnt[l & 1], 0, (4ull << l) * sizeof(uint32_t), stream)) != cudaSuccess)
-          return fail_cuda(e, "memset counts");
-        if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      }
-    }
-    uint32_t* const lastbits = dry ? nullptr : out->bitmaps + (uint64_t)(L - 1) * c.words;
-    if (pair) {  // B_{L-1} is OR-ed together by the fused pass: zero it first
-      note(K_MEMSET);
-      if (!dry) {
-        if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-        if ((e = cudaMemsetAsync(lastbits, 0, c.words * sizeof(uint32_t), stream)) != cudaSuccess)
-          return fail_cuda(e, "memset last bitmap");
-        if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      }
-    }
-    // pre_l = exclusive scan of agg_l (ones of level l per tile)
-    note(K_TSCAN);
-    if ((st = scan(wt::OpTilePrefix{agg + (uint64_t)l * c.ntiles, pre}, c.ntiles, "k_scan(tile prefix)")) != WT_OK)
+    // pre_l (scan of agg_l), the node tables of level l (from the level-(l+1)
+    // node sizes counted by pass l-1, or from ones0 for l = 0), and zero the
+    // node-count buffer pass l fills (and B_{L-1}, OR-ed by the fused pass)
+    wt::OpLevelTab tb = (l == 0) ? wt::OpLevelTab{nullptr, tab, n, ones0}
+                                 : wt::OpLevelTab{dry ? nullptr : cnt[(l - 1) & 1], tab + ((1ull << l) - 1), n, nullptr};
+    wt::ZeroFill z{dry ? nullptr : reinterpret_cast<uint4*>(cnt[l & 1]), 1ull << l,
+                   pair && !dry ? reinterpret_cast<uint4*>(lastbits) : nullptr, pair ? c.words / 4 : 0};
+    if ((st = prep(K_PREP, wt::OpTilePrefix{agg + (uint64_t)l * c.ntiles, pre}, c.ntiles, tb, 1ull << l, z,
+                   "k_prep")) != WT_OK)
       return st;
-    note(last ? K_LAST : pair ? K_PAIR : K_LEVEL);
+    if ((st = level(l, pair ? 2 : 1)) != WT_OK) return st;
+  }
+  if (Lrun == L - 1) {
+    // superblocks of level L-1 from the bitmap the fused pass wrote, and C
+    // (exclusive scan of the leaf counts pass L-2 made)
+    uint32_t* blk = reinterpret_cast<uint32_t*>(ws + c.off_blk);
+    note(K_BLKPOP);
     if (!dry) {
-      const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
-      T* o = last ? nullptr : pair ? reinterpret_cast<T*>(lastbits) : buf[l & 1];
-      const uint32_t sh = L - 1 - l;
-      const uint2* t = last ? nullptr : tab + ((1ull << l) - 1);
-      uint32_t* bits = out->bitmaps + (uint64_t)l * c.words;
-      unsigned long long* sb = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
-      uint32_t* agg_next = (last || pair) ? nullptr : agg + (uint64_t)(l + 1) * c.ntiles;
-      uint32_t* cn = last ? nullptr : cnt[l & 1];
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      if (last)
-        wt::k_level<T, 0><<<grid_last, wt::LV_THREADS, lsmem, stream>>>(
-            in, o, (uint32_t)n, (uint32_t)c.ntiles, sh, t, bits, (uint32_t)c.words, sb, (uint32_t)c.nsb, pre,
-            agg_next, cn, flag);
-      else if (pair)
-        wt::k_level<T, 2><<<grid_pair, wt::LV_THREADS, lsmem, stream>>>(
-            in, o, (uint32_t)n, (uint32_t)c.ntiles, sh, t, bits, (uint32_t)c.words, sb, (uint32_t)c.nsb, pre,
-            agg_next, cn, flag);
-      else
-        wt::k_level<T, 1><<<grid_sc, wt::LV_THREADS, lsmem, stream>>>(
-            in, o, (uint32_t)n, (uint32_t)c.ntiles, sh, t, bits, (uint32_t)c.words, sb, (uint32_t)c.nsb, pre,
-            agg_next, cn, flag);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_level");
+      const uint64_t nbk = c.nsb - 1, warps = (nbk + 31) / 32;
+      const uint32_t g = (uint32_t)std::max<uint64_t>(
+          1, std::min<uint64_t>((warps + wt::BP_THREADS / 32 - 1) / (wt::BP_THREADS / 32), 16ull * num_sms()));
+      wt::k_block_pop<<<g, wt::BP_THREADS, 0, stream>>>(lastbits, blk, nbk, flag);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_block_pop");
       if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
     }
-    if (l + 2 == L) {  // pass L-2 counted the leaves: C = exclusive scan of the leaf counts
-      note(K_SCAN);
-      if ((st = scan(wt::OpLeafC{dry ? nullptr : cnt[l & 1], C, 1ull << L, n, nullptr}, 1ull << L, "k_scan(C)")) !=
-          WT_OK)
-        return st;
-      // superblocks of level L-1 from the bitmap the fused pass wrote
-      uint32_t* blk = reinterpret_cast<uint32_t*>(ws + c.off_blk);
-      note(K_BLKPOP);
-      if (!dry) {
-        if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-        const uint64_t nbk = c.nsb - 1, warps = (nbk + 31) / 32;
-        const uint32_t g = (uint32_t)std::max<uint64_t>(
-            1, std::min<uint64_t>((warps + wt::BP_THREADS / 32 - 1) / (wt::BP_THREADS / 32), 16ull * num_sms()));
-        wt::k_block_pop<<<g, wt::BP_THREADS, 0, stream>>>(lastbits, blk, nbk, flag);
-        if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_block_pop");
-        if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      }
-      note(K_SBSCAN);
-      unsigned long long* sbl =
-          dry ? nullptr : reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)(L - 1) * c.nsb;
-      if ((st = scan(wt::OpBlockPop{blk, sbl, c.nsb - 1}, c.nsb - 1, "k_scan(last-level superblocks)")) != WT_OK)
-        return st;
-    }
+    unsigned long long* sbl =
+        dry ? nullptr : reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)(L - 1) * c.nsb;
+    if ((st = prep(K_FINAL, wt::OpBlockPop{blk, sbl, c.nsb - 1}, c.nsb - 1,
+                   wt::OpLeafC{dry ? nullptr : cnt[(L - 2) & 1], C, 1ull << L, n, nullptr}, 1ull << L, nozero,
+                   "k_prep(final)")) != WT_OK)
+      return st;
   }
   if (count) *count = nk;
   return WT_OK;

@@ -29,15 +29,14 @@ constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
 // Exclusive scan of uint64 values over [0, count) with a decoupled look-back.
-// Op supplies load(i) and store(i, exclusive, value).
+// Op supplies load(i) and store(i, exclusive, value).  One CTA scans one tile
+// of SCAN_TILE values; tile ids come from an atomic ticket (forward progress).
 template <class Op>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan(Op op, uint64_t count, LookbackState status,
-                                                       uint32_t* tile_counter, uint32_t epoch,
-                                                       const int32_t* __restrict__ flag) {
+__device__ __forceinline__ void scan_tile(const Op& op, uint64_t count, const LookbackState& status,
+                                          uint32_t* tile_counter, uint32_t epoch) {
   __shared__ uint64_t s_warp[SCAN_THREADS / 32];
   __shared__ uint64_t s_P;
   __shared__ uint32_t s_tile;
-  if (*flag) return;
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
   __syncthreads();
   const uint64_t tile = s_tile;
@@ -69,6 +68,50 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Op op, uint64_t count, Lo
     run += v[k];
   }
 }
+
+template <class Op>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan(Op op, uint64_t count, LookbackState status,
+                                                       uint32_t* tile_counter, uint32_t epoch,
+                                                       const int32_t* __restrict__ flag) {
+  if (*flag) return;
+  scan_tile(op, count, status, tile_counter, epoch);
+}
+
+// Two independent scans (each with its own look-back state and ticket) and a
+// zero fill of up to two buffers in ONE launch: CTAs [0, ga) scan A, the next
+// gb scan B, the rest zero-fill.  Per level: the tile prefixes of the level,
+// its node tables, and the node-count buffer the pass fills (plus, before the
+// fused pass, the last level's bitmap); at the end: the last level's
+// superblocks and C.
+struct ZeroFill {
+  uint4* p0;
+  uint64_t n0;  // 16-byte units
+  uint4* p1;
+  uint64_t n1;
+};
+template <class OpA, class OpB>
+__global__ void __launch_bounds__(SCAN_THREADS) k_prep(OpA a, uint64_t na, LookbackState sta, uint32_t* ca, uint32_t ea,
+                                                       OpB b, uint64_t nb, LookbackState stb, uint32_t* cb, uint32_t eb,
+                                                       ZeroFill z, const int32_t* __restrict__ flag) {
+  if (*flag) return;
+  const uint32_t ga = (uint32_t)((na + SCAN_TILE - 1) / SCAN_TILE), gb = (uint32_t)((nb + SCAN_TILE - 1) / SCAN_TILE);
+  if (blockIdx.x < ga) {
+    scan_tile(a, na, sta, ca, ea);
+  } else if (blockIdx.x < ga + gb) {
+    scan_tile(b, nb, stb, cb, eb);
+  } else {
+    const uint64_t nt = (uint64_t)(gridDim.x - ga - gb) * SCAN_THREADS;
+    const uint64_t t0 = (uint64_t)(blockIdx.x - ga - gb) * SCAN_THREADS + threadIdx.x;
+    for (uint64_t i = t0; i < z.n0; i += nt) z.p0[i] = make_uint4(0, 0, 0, 0);
+    for (uint64_t i = t0; i < z.n1; i += nt) z.p1[i] = make_uint4(0, 0, 0, 0);
+  }
+}
+
+// a scan job that does nothing (count 0)
+struct OpNone {
+  __device__ uint64_t load(uint64_t) const { return 0; }
+  __device__ void store(uint64_t, uint64_t, uint64_t) const {}
+};
 
 // Per-tile prefixes: pre[t] = sum_{t' < t} agg[t'] (ones of the level before
 // tile t), from the per-tile ones counted by the previous pass.

@@ -84,14 +84,14 @@ def test_build_validates_before_touching_the_device(wt):
 
 
 def test_launch_plan(wt):
-    lv = ["tables", "memset", "tile_scan", "level"]
-    last = ["tile_scan", "last_level"]
-    # pass L-2 is fused with level L-1: it writes B_{L-1} (zeroed first), then C and the last superblocks
-    pair = ["memset", "memset", "tile_scan", "pair", "scan", "block_pop", "sb_scan"]
-    assert wt.launch_plan(1 << 20, 256, 1) == (["prologue", "tables", "memset", "tile_scan", "level"] + lv * 5
-                                               + ["tables"] + pair)
-    assert wt.launch_plan(1 << 20, 4, 1) == ["prologue", "tables"] + pair
-    assert wt.launch_plan(1 << 20, 8, 1) == ["prologue", "tables", "memset", "tile_scan", "level", "tables"] + pair
-    assert wt.launch_plan(100, 2, 1) == ["prologue", "scan"] + last
+    # per level one prep launch (tile prefixes, node tables, zeroing) and the
+    # pass; pass L-2 is fused with level L-1 (writes B_{L-1}), then the last
+    # level's block counts and one launch for its superblocks and C
+    lv = ["prep", "level"]
+    pair = ["prep", "pair", "block_pop", "final_scan"]
+    assert wt.launch_plan(1 << 20, 256, 1) == ["prologue"] + lv * 6 + pair
+    assert wt.launch_plan(1 << 20, 4, 1) == ["prologue"] + pair
+    assert wt.launch_plan(1 << 20, 8, 1) == ["prologue"] + lv + pair
+    assert wt.launch_plan(100, 2, 1) == ["prologue", "prep", "last_level"]
     assert wt.launch_plan(100, 1, 1) == ["prologue", "scan"]
     assert wt.launch_plan(0, 16, 1) == []

@@ -18,6 +18,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def kind_of(name: str) -> str:
+    if "k_prep" in name:
+        return "final_scan" if "OpBlockPop" in name else "prep"
     if "k_prologue" in name:
         return "prologue"
     if "k_level" in name:
