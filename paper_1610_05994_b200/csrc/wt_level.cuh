@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const uint4* own = S.own + (NH == 1 ? 0 : hh);  // own[NH * owner]
     // (4-byte entries: the 16 entries span 16 banks, one wavefront per word round)
     auto lut_of = [&](uint32_t m4) -> uint2 {
-      if constexpr (SPW == 1) return make_uint2(0, 0);
+      if constexpr (SPW <= 2) return make_uint2(0, 0);  // (u16 stores without the table)
       else if constexpr (SPW == 4) return make_uint2(S.lut[m4 & 15u].x, 0u);  // (u8: .y unused, 4-byte loads)
       else return S.lut[m4 & ((1u << SPW) - 1u)];
     };
@@ -312,6 +312,11 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
                                 uint2 e2) {
       if constexpr (SPW == 1) {
         st_shared<T>((m4 & 1u) ? O0 + R * (uint32_t)sizeof(T) : Z0 + (q0 - R) * (uint32_t)sizeof(T), x);
+      } else if constexpr (SPW == 2) {  // u16: each symbol straight to its slot (no partition table)
+        const uint32_t t = 2u * (m4 & 1u);              // 2 if symbol 0 is a one
+        const uint32_t Az = Z0 + (q0 - R) * 2u, Ao = O0 + R * 2u;
+        st_shared<T, 0>(t ? Ao : Az, x);
+        st_shared<T, 0>((m4 & 2u) ? Ao + t : Az + 2u - t, x >> 16);
       } else {
         const uint32_t e = e2.x;
         uint32_t y;
@@ -320,10 +325,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         const uint32_t Az = Z0 + (q0 - R) * (uint32_t)sizeof(T);
         const uint32_t Ao = O0 + (R - nz) * (uint32_t)sizeof(T);
         st_shared<T, 0>(e >= (1u << 16) ? Az : Ao, y);
-        if constexpr (SPW == 2)  // (u16: slot 1 by a multiply-add, FMA pipe)
-          st_shared<T, sizeof(T)>(Ao + e2.y * (Az - Ao), __umulhi(y, 1u << (32 - 8 * sizeof(T))));
-        else
-          st_shared<T, sizeof(T)>(e >= (2u << 16) ? Az : Ao, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
+        st_shared<T, sizeof(T)>(e >= (2u << 16) ? Az : Ao, __umulhi(y, 1u << (32 - 8 * sizeof(T))));
         if constexpr (SPW > 2) {
           st_shared<T, 2>(e >= (3u << 16) ? Az : Ao, __umulhi(y, 1u << 16));
           st_shared<T, 3>(e >= (4u << 16) ? Az : Ao, __umulhi(y, 1u << 8));
