@@ -189,6 +189,32 @@ struct Launcher {
   }
 };
 
+// Kernel launch with programmatic stream serialization (PDL): the kernel may
+// start while its predecessor finishes; it calls pdl_wait() before touching
+// the predecessor's results.  WT_NO_PDL=1 launches normally (A/B, debugging).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("WT_NO_PDL");
+    return !(v && *v && *v != '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), uint32_t grid, uint32_t block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 enum Kind : uint32_t {
   K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7, K_PAIR = 8, K_SBSCAN = 9,
   K_BLKPOP = 10, K_PREP = 11, K_FINAL = 12
@@ -273,9 +299,10 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       const uint64_t gz = zu ? std::min<uint64_t>((zu + 4 * wt::SCAN_THREADS - 1) / (4 * wt::SCAN_THREADS),
                                                   2ull * num_sms())
                              : (ga + gb ? 0 : 1);
-      wt::k_prep<decltype(opA), decltype(opB)><<<(uint32_t)(ga + gb + gz), wt::SCAN_THREADS, 0, stream>>>(
-          opA, na, status, counters + counter, epoch, opB, nb, status2, counters + counter + 1, epoch + 1, z, flag);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, what);
+      e = launch_pdl(wt::k_prep<decltype(opA), decltype(opB)>, (uint32_t)(ga + gb + gz), wt::SCAN_THREADS, 0, stream,
+                     opA, na, status, counters + counter, epoch, opB, nb, status2, counters + counter + 1, epoch + 1, z,
+                     (const int32_t*)flag);
+      if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, what);
       if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
     }
     epoch += 2;
@@ -318,16 +345,18 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     uint32_t* cn = mode == 0 ? nullptr : cnt[l & 1];
     if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
     const uint32_t n32 = (uint32_t)n, nt32 = (uint32_t)c.ntiles, w32 = (uint32_t)c.words, nsb32 = (uint32_t)c.nsb;
+    const uint32_t* pre_c = pre;
+    const int32_t* flag_c = flag;
     if (mode == 0)
-      wt::k_level<T, 0><<<grid_last, wt::LV_THREADS, lsmem, stream>>>(in, o, n32, nt32, sh, t, bits, w32, sb, nsb32,
-                                                                      pre, agg_next, cn, flag);
+      e = launch_pdl(wt::k_level<T, 0>, grid_last, wt::LV_THREADS, lsmem, stream, in, o, n32, nt32, sh, t, bits, w32,
+                     sb, nsb32, pre_c, agg_next, cn, flag_c);
     else if (mode == 2)
-      wt::k_level<T, 2><<<grid_pair, wt::LV_THREADS, lsmem, stream>>>(in, o, n32, nt32, sh, t, bits, w32, sb, nsb32,
-                                                                      pre, agg_next, cn, flag);
+      e = launch_pdl(wt::k_level<T, 2>, grid_pair, wt::LV_THREADS, lsmem, stream, in, o, n32, nt32, sh, t, bits, w32,
+                     sb, nsb32, pre_c, agg_next, cn, flag_c);
     else
-      wt::k_level<T, 1><<<grid_sc, wt::LV_THREADS, lsmem, stream>>>(in, o, n32, nt32, sh, t, bits, w32, sb, nsb32,
-                                                                    pre, agg_next, cn, flag);
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_level");
+      e = launch_pdl(wt::k_level<T, 1>, grid_sc, wt::LV_THREADS, lsmem, stream, in, o, n32, nt32, sh, t, bits, w32,
+                     sb, nsb32, pre_c, agg_next, cn, flag_c);
+    if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_level");
     if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
     return WT_OK;
   };
@@ -372,8 +401,9 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       const uint64_t nbk = c.nsb - 1, warps = (nbk + 31) / 32;
       const uint32_t g = (uint32_t)std::max<uint64_t>(
           1, std::min<uint64_t>((warps + wt::BP_THREADS / 32 - 1) / (wt::BP_THREADS / 32), 16ull * num_sms()));
-      wt::k_block_pop<<<g, wt::BP_THREADS, 0, stream>>>(lastbits, blk, nbk, flag);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_block_pop");
+      e = launch_pdl(wt::k_block_pop, g, wt::BP_THREADS, 0, stream, (const uint32_t*)lastbits, blk, nbk,
+                     (const int32_t*)flag);
+      if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_block_pop");
       if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
     }
     unsigned long long* sbl =

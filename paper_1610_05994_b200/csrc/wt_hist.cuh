@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(PRO_THREADS) k_prologue(const T* __restrict__ 
   constexpr uint32_t TILE = LvTile<T>::TILE;
   constexpr uint32_t VL = TILE / PER / 32;  // 16-byte vectors per lane per tile (4)
   static_assert(VL * PER * 32 == TILE, "tile layout");
+  pdl_trigger();  // (launched normally, after the control-block memset) the first k_prep may start waiting
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (uint64_t)blockIdx.x * (PRO_THREADS / 32) + (threadIdx.x >> 5);
   const uint64_t nwarps = (uint64_t)gridDim.x * (PRO_THREADS / 32);

@@ -93,6 +93,7 @@ template <class OpA, class OpB>
 __global__ void __launch_bounds__(SCAN_THREADS) k_prep(OpA a, uint64_t na, LookbackState sta, uint32_t* ca, uint32_t ea,
                                                        OpB b, uint64_t nb, LookbackState stb, uint32_t* cb, uint32_t eb,
                                                        ZeroFill z, const int32_t* __restrict__ flag) {
+  pdl_wait();
   if (*flag) return;
   const uint32_t ga = (uint32_t)((na + SCAN_TILE - 1) / SCAN_TILE), gb = (uint32_t)((nb + SCAN_TILE - 1) / SCAN_TILE);
   if (blockIdx.x < ga) {
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_prep(OpA a, uint64_t na, Lookb
     for (uint64_t i = t0; i < z.n0; i += nt) z.p0[i] = make_uint4(0, 0, 0, 0);
     for (uint64_t i = t0; i < z.n1; i += nt) z.p1[i] = make_uint4(0, 0, 0, 0);
   }
+  pdl_trigger();  // at the tail: the next pass's CTAs launch as this grid drains
 }
 
 // a scan job that does nothing (count 0)
@@ -180,6 +182,8 @@ struct OpLeafC {
 constexpr int BP_THREADS = 256;
 __global__ void __launch_bounds__(BP_THREADS) k_block_pop(const uint32_t* __restrict__ bits, uint32_t* __restrict__ cnt,
                                                           uint64_t nblocks, const int32_t* __restrict__ flag) {
+  pdl_wait();
+  pdl_trigger();
   if (*flag) return;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * (BP_THREADS / 32);

@@ -109,7 +109,6 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LevelSmem<T>& S = *reinterpret_cast<LevelSmem<T>*>(smem_raw);
 
-  if (*flag) return;
   // n < 2^32 (wt_sizes rejects larger n): every position, rank and node
   // offset of the pass fits 32 bits; only pointers are 64-bit.
   const uint32_t lane = threadIdx.x;
@@ -132,8 +131,13 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
   if (lane == 0) {
     for (int b = 0; b < NB; ++b) mbar_init(&S.bar[b], 1);
     fence_mbar_init();
-    for (int b = 0; b < (SCATTER ? NB - 1 : NB); ++b) issue((uint32_t)b);
   }
+  // everything above overlaps the predecessor (k_prep): from here on its
+  // outputs (tile prefixes, node tables, zeroed counts) and T_l are read
+  pdl_wait();
+  if (*flag) return;
+  if (lane == 0)
+    for (int b = 0; b < (SCATTER ? NB - 1 : NB); ++b) issue((uint32_t)b);
   if (SCATTER && lane < 16) {
     S.lut[lane] = make_uint2(partition_lut_entry<T>(lane), (partition_lut_entry<T>(lane) >> 16) > 1);
   }
@@ -1014,6 +1018,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     __syncwarp();
     if (lane == 0 && it >= 1) issue(it + NB - 2);
   }
+  pdl_trigger();  // (at the tail: the next launch's CTAs do not crowd the pass)
   if (SCATTER) {
     cc_flush();
     if (lane < (uint32_t)LV_NREG) bulk_wait<0>();

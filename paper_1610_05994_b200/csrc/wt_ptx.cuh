@@ -43,6 +43,14 @@ template <int N>
 __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
+// Programmatic dependent launch (the build's kernels are launched with
+// programmatic stream serialization): a kernel may start while its
+// predecessor still runs; pdl_wait() blocks until the predecessor grid has
+// completed and its writes are visible (a no-op when launched normally).
+// pdl_trigger() lets the successor launch (it then waits in its pdl_wait()).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
   asm volatile(
       "{\n"
