@@ -139,6 +139,22 @@ wt_status wt_build_from_host(const void* h_seq, uint64_t n, uint64_t sigma, uint
                              wt_stream_t stream);
 
 /*
+ * wt_build_from_host_async: the same, enqueued on `stream` WITHOUT the final
+ * synchronisation: H2D of h_seq, the build, D2H of the tree into h_out, and
+ * the build's status word into *h_status (host memory, pinned for the copy
+ * to stay asynchronous).  After synchronising the stream, *h_status is WT_OK
+ * or WT_ERR_SYMBOL_RANGE (h_out is then unspecified).  Builds on different
+ * streams with different workspaces run concurrently (their copies overlap
+ * each other's compute: H2D and D2H use separate copy engines).  The host
+ * buffers must stay valid until the stream reaches the end of the build.
+ * Errors (returned at once): as wt_build_from_host, WT_ERR_ARG if h_status
+ * is NULL.
+ */
+wt_status wt_build_from_host_async(const void* h_seq, uint64_t n, uint64_t sigma, uint32_t width,
+                                   const wt_tree_t* h_out, void* d_workspace, size_t workspace_bytes,
+                                   int32_t* h_status, wt_stream_t stream);
+
+/*
  * wt_access: d_sym[k] = S[d_pos[k]] for k < m, by the top-down traversal of
  * P:353-380 simulated with rank on the level bitmaps.
  * tree: device pointers of a finished build of (n, sigma).

@@ -59,6 +59,7 @@ _lib.wt_sizes.argtypes = [_u64, _u64, _u32, ctypes.POINTER(WtSizes)]
 _lib.wt_build_async.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(WtTree), _vp, _sz, _vp, _vp]
 _lib.wt_build.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(WtTree), _vp, _sz, _vp]
 _lib.wt_build_from_host.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(WtTree), _vp, _sz, _vp]
+_lib.wt_build_from_host_async.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(WtTree), _vp, _sz, _vp, _vp]
 _lib.wt_access.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _u64, _vp, _vp, _vp]
 _lib.wt_rank.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
 _lib.wt_select.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
@@ -72,11 +73,12 @@ _lib.wt_status_string.argtypes = [ctypes.c_int]
 _lib.wt_status_string.restype = ctypes.c_char_p
 _lib.wt_last_error.argtypes = []
 _lib.wt_last_error.restype = ctypes.c_char_p
-for _f in (_lib.wt_sizes, _lib.wt_build_async, _lib.wt_build, _lib.wt_build_from_host, _lib.wt_access,
-           _lib.wt_rank, _lib.wt_select):
+for _f in (_lib.wt_sizes, _lib.wt_build_async, _lib.wt_build, _lib.wt_build_from_host,
+           _lib.wt_build_from_host_async, _lib.wt_access, _lib.wt_rank, _lib.wt_select):
     _f.restype = ctypes.c_int
 
-EXPORTS = ["wt_sizes", "wt_build_async", "wt_build", "wt_build_from_host", "wt_access", "wt_rank",
+EXPORTS = ["wt_sizes", "wt_build_async", "wt_build", "wt_build_from_host", "wt_build_from_host_async",
+           "wt_access", "wt_rank",
            "wt_select", "wt_launch_plan", "wt_debug_offsets", "wt_set_profile_events", "wt_status_string",
            "wt_last_error"]
 
@@ -266,6 +268,29 @@ def build_from_host(h_seq: torch.Tensor, sigma: int, h_tree: HostTree | None = N
     st = _lib.wt_build_from_host(h_seq.data_ptr() if n else None, n, sigma, w, ctypes.byref(ct),
                                  workspace.data_ptr(), workspace.numel(), _stream_ptr(stream))
     _check(st, "wt_build_from_host")
+    return h_tree
+
+
+def build_from_host_async(h_seq: torch.Tensor, sigma: int, h_tree: HostTree, workspace: torch.Tensor,
+                          h_status: torch.Tensor, stream=None) -> HostTree:
+    """wt_build_from_host_async: H2D, build and D2H of the tree enqueued on `stream`, no
+    synchronisation; after the stream is synchronised, h_status (a pinned int32 host
+    tensor of one element) holds WT_OK or WT_ERR_SYMBOL_RANGE.  Two builds on two
+    streams with two workspaces overlap each other's copies and compute."""
+    if h_seq.is_cuda or h_status.is_cuda:
+        raise ValueError("h_seq and h_status must be host tensors")
+    if h_status.dtype != torch.int32 or h_status.numel() < 1:
+        raise ValueError("h_status must be an int32 host tensor")
+    h_seq = h_seq.contiguous()
+    w = width_of(h_seq)
+    n = h_seq.numel()
+    ct = WtTree(h_tree.bitmaps.data_ptr() if h_tree.bitmaps.numel() else None,
+                h_tree.superblocks.data_ptr() if h_tree.superblocks.numel() else None,
+                h_tree.node_offsets.data_ptr())
+    st = _lib.wt_build_from_host_async(h_seq.data_ptr() if n else None, n, sigma, w, ctypes.byref(ct),
+                                       workspace.data_ptr(), workspace.numel(), h_status.data_ptr(),
+                                       _stream_ptr(stream))
+    _check(st, "wt_build_from_host_async")
     return h_tree
 
 

@@ -499,12 +499,13 @@ wt_status wt_build(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t width
   return WT_OK;
 }
 
-wt_status wt_build_from_host(const void* h_seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* h_out,
-                             void* d_workspace, size_t workspace_bytes, wt_stream_t stream) {
+wt_status wt_build_from_host_async(const void* h_seq, uint64_t n, uint64_t sigma, uint32_t width,
+                                   const wt_tree_t* h_out, void* d_workspace, size_t workspace_bytes,
+                                   int32_t* h_status, wt_stream_t stream) {
   g_last_error.clear();
   wt_status st = check_args(n, sigma, width);
   if (st != WT_OK) return st;
-  if (!h_out || !h_out->node_offsets || (n > 0 && !h_seq)) return fail(WT_ERR_ARG, "NULL host pointer");
+  if (!h_out || !h_out->node_offsets || (n > 0 && !h_seq) || !h_status) return fail(WT_ERR_ARG, "NULL host pointer");
   const Carve c = carve(n, sigma, width);
   if (!d_workspace || workspace_bytes < c.host_total) return fail(WT_ERR_WORKSPACE, "workspace too small");
   if (reinterpret_cast<uintptr_t>(d_workspace) & (ALIGN - 1))
@@ -528,10 +529,20 @@ wt_status wt_build_from_host(const void* h_seq, uint64_t n, uint64_t sigma, uint
     return fail_cuda(e, "D2H superblocks");
   if ((e = cudaMemcpyAsync(h_out->node_offsets, dtree.node_offsets, cb, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return fail_cuda(e, "D2H node offsets");
+  if ((e = cudaMemcpyAsync(h_status, ws + c.off_flag, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return fail_cuda(e, "status readback");
+  return WT_OK;
+}
+
+wt_status wt_build_from_host(const void* h_seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* h_out,
+                             void* d_workspace, size_t workspace_bytes, wt_stream_t stream) {
   int32_t h_flag = 0;
-  if ((e = cudaMemcpyAsync(&h_flag, ws + c.off_flag, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-    return fail_cuda(e, "flag readback");
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail_cuda(e, "stream sync");
+  wt_status st = wt_build_from_host_async(h_seq, n, sigma, width, h_out, d_workspace, workspace_bytes, &h_flag,
+                                          stream);
+  if (st != WT_OK) return st;
+  cudaError_t e;
+  if ((e = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream))) != cudaSuccess)
+    return fail_cuda(e, "stream sync");
   if (h_flag) return fail(WT_ERR_SYMBOL_RANGE, "a symbol is >= sigma");
   return WT_OK;
 }

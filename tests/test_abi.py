@@ -79,6 +79,11 @@ def test_build_validates_before_touching_the_device(wt):
     assert lib.wt_build_async(32, 10, 4, 1, ctypes.byref(tree), 257, 1 << 20, None, None) == wt.WT_ERR_ARG
     assert lib.wt_build_async(32, 10, 4, 3, ctypes.byref(tree), 256, 1 << 20, None, None) == wt.WT_ERR_ARG
     assert lib.wt_access(None, 10, 4, None, 1, None, None, None) == wt.WT_ERR_ARG
+    # the host-buffer build: NULL status word / host pointers, then the workspace size
+    htree = wt.WtTree(16, 16, 16)
+    assert lib.wt_build_from_host_async(32, 10, 4, 1, ctypes.byref(htree), 256, 1 << 20, None, None) == wt.WT_ERR_ARG
+    assert lib.wt_build_from_host_async(None, 10, 4, 1, ctypes.byref(htree), 256, 1 << 20, 64, None) == wt.WT_ERR_ARG
+    assert lib.wt_build_from_host_async(32, 10, 4, 1, ctypes.byref(htree), 256, 16, 64, None) == wt.WT_ERR_WORKSPACE
     assert b"workspace" in lib.wt_last_error() or lib.wt_last_error() == b"tree is NULL"
     assert lib.wt_status_string(2) == b"WT_ERR_SYMBOL_RANGE"
 

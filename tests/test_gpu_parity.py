@@ -144,6 +144,39 @@ def test_build_from_host_matches(wt):
     assert np.array_equal(h.node_offsets.numpy().view(np.uint64), ot.node_offsets)
 
 
+def test_build_from_host_async_two_streams(wt):
+    # two builds in flight on two streams (different inputs, workspaces, host trees),
+    # each compared with the oracle; then the range error through the status word
+    cases = [(wt_inputs.random_case(12, 700_001, 256, "zipf"), 256),
+             (wt_inputs.random_case(13, 300_007, 1 << 16, "uniform", dtype=np.uint16), 1 << 16)]
+    dev = torch.device("cuda", 0)
+    streams = [torch.cuda.Stream(device=dev) for _ in cases]
+    outs = []
+    for (S, sigma), st in zip(cases, streams):
+        h = torch.from_numpy(S).pin_memory()
+        ht = wt.alloc_host_tree(S.size, sigma, S.itemsize)
+        ws = wt.alloc_workspace(S.size, sigma, S.itemsize, dev, host=True)
+        status = torch.full((1,), -1, dtype=torch.int32).pin_memory()
+        wt.build_from_host_async(h, sigma, ht, ws, status, stream=st)
+        outs.append((S, sigma, ht, status, h, ws))
+    torch.cuda.synchronize()
+    for S, sigma, ht, status, _, _ in outs:
+        assert int(status.item()) == wt.WT_OK
+        ot = oracle.build(S, sigma)
+        assert np.array_equal(ht.bitmaps.numpy().view(np.uint32), ot.bitmaps)
+        assert np.array_equal(ht.superblocks.numpy().view(np.uint64), ot.superblocks)
+        assert np.array_equal(ht.node_offsets.numpy().view(np.uint64), ot.node_offsets)
+    bad = np.array([0, 1, 5, 2] * 1000, np.uint8)
+    ht = wt.alloc_host_tree(bad.size, 4, 1)
+    ws = wt.alloc_workspace(bad.size, 4, 1, dev, host=True)
+    status = torch.zeros(1, dtype=torch.int32).pin_memory()
+    wt.build_from_host_async(torch.from_numpy(bad).pin_memory(), 4, ht, ws, status, stream=streams[0])
+    streams[0].synchronize()
+    assert int(status.item()) == wt.WT_ERR_SYMBOL_RANGE
+    with pytest.raises(ValueError):
+        wt.build_from_host_async(torch.from_numpy(bad), 4, ht, ws, status.cuda())
+
+
 # ------------------------------------------------------------------- queries
 
 
