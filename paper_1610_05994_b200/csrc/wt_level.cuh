@@ -78,7 +78,7 @@ struct LevelSmem {
   uint2 kt[C::MAXSEG];                // segment g: shared-memory byte addresses {Z0, O0}: a zero at q with
                                       // R ones before it goes to Z0 + (q - R) W, a one to O0 + R W
   uint2 lut[16];                      // in-word stable partition: {selector | nz << 16 (nz zeros first),
-                                      // nz > 1}; 8-byte entries: one wavefront per word round
+                                      // 2^nz - 1 (the zero slots)}
   int32_t s1, am, Rs1, Ram;           // first-segment end, last-segment start, ranks there
   alignas(8) unsigned long long bar[C::NB];
 };
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
   if (lane == 0)
     for (int b = 0; b < (SCATTER ? NB - 1 : NB); ++b) issue((uint32_t)b);
   if (SCATTER && lane < 16) {
-    S.lut[lane] = make_uint2(partition_lut_entry<T>(lane), (partition_lut_entry<T>(lane) >> 16) > 1);
+    S.lut[lane] = make_uint2(partition_lut_entry<T>(lane), (1u << (partition_lut_entry<T>(lane) >> 16)) - 1u);
   }
   __syncwarp();
 
@@ -430,13 +430,14 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
             op += b;
           } else {
             const uint32_t m4 = (m[h] >> (SPW * kk)) & ((1u << SPW) - 1u);
-            const uint32_t e = S.lut[m4].x, nz = e >> 16;
+            const uint2 ee = S.lut[m4];
+            const uint32_t e = ee.x, nz = e >> 16;
             uint32_t y;
             asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(xw[k]), "r"(e));
             uint32_t g;  // bit 0 of the partitioned symbols, slot j at bit j
             if constexpr (SPW == 4) g = ((y & 0x01010101u) * 0x10204080u) >> 28;
             else g = (y & 1u) | ((y >> 15) & 2u);
-            Zs |= (g & ((1u << nz) - 1u)) << zp;
+            Zs |= (g & ee.y) << zp;
             Os |= (g >> nz) << op;
             zp += nz;
             op += SPW - nz;
