@@ -79,6 +79,7 @@ struct LevelSmem {
                                       // R ones before it goes to Z0 + (q - R) W, a one to O0 + R W
   uint2 lut[16];                      // in-word stable partition: {selector | nz << 16 (nz zeros first),
                                       // 2^nz - 1 (the zero slots)}
+  uint2 lutp[16];                     // MODE 2 bit compaction: {2^nz, 2^(SPW-nz)} (string position multipliers)
   int32_t s1, am, Rs1, Ram;           // first-segment end, last-segment start, ranks there
   alignas(8) unsigned long long bar[C::NB];
 };
@@ -139,7 +140,9 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
   if (lane == 0)
     for (int b = 0; b < (SCATTER ? NB - 1 : NB); ++b) issue((uint32_t)b);
   if (SCATTER && lane < 16) {
-    S.lut[lane] = make_uint2(partition_lut_entry<T>(lane), (1u << (partition_lut_entry<T>(lane) >> 16)) - 1u);
+    const uint32_t e = partition_lut_entry<T>(lane), nz = e >> 16;
+    S.lut[lane] = make_uint2(e, (1u << nz) - 1u);
+    S.lutp[lane] = make_uint2(1u << nz, 1u << (4 / sizeof(T) - nz));
   }
   __syncwarp();
 
@@ -418,32 +421,41 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       uint32_t Zh[NH], Oh[NH], nzh[NH];
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
-        uint32_t Zs = 0, Os = 0, zp = 0, op = 0;
+        uint32_t Zs = 0, Os = 0;
+        if constexpr (SPW == 1) {
+          uint32_t zp = 0, op = 0;
 #pragma unroll
-        for (int kk = 0; kk < HW; ++kk) {
-          const int k = h * HW + kk;
-          if constexpr (SPW == 1) {
+          for (int kk = 0; kk < HW; ++kk) {
+            const int k = h * HW + kk;
             const uint32_t b = (m[h] >> kk) & 1u, g = xw[k] & 1u;
             Zs |= (b ? 0u : g) << zp;
             Os |= (b ? g : 0u) << op;
             zp += 1u - b;
             op += b;
-          } else {
+          }
+        } else {
+          // the string positions as multipliers (pz = 2^zp, po = 2^op): the
+          // appends and position updates are multiply-adds (FMA pipe), the
+          // ALU pipe keeps only the table index, PRMT, gather and mask
+          uint32_t pz = 1, po = 1;
+#pragma unroll
+          for (int kk = 0; kk < HW; ++kk) {
+            const int k = h * HW + kk;
             const uint32_t m4 = (m[h] >> (SPW * kk)) & ((1u << SPW) - 1u);
-            const uint2 ee = S.lut[m4];
-            const uint32_t e = ee.x, nz = e >> 16;
+            const uint2 ee = S.lut[m4], pp = S.lutp[m4];
             uint32_t y;
-            asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(xw[k]), "r"(e));
+            asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(xw[k]), "r"(ee.x));
             uint32_t g;  // bit 0 of the partitioned symbols, slot j at bit j
             if constexpr (SPW == 4) g = ((y & 0x01010101u) * 0x10204080u) >> 28;
             else g = (y & 1u) | ((y >> 15) & 2u);
-            Zs |= (g & ee.y) << zp;
-            Os |= (g >> nz) << op;
-            zp += nz;
-            op += SPW - nz;
+            Zs += (g & ee.y) * pz;          // disjoint bits: + is |
+            Os += (g >> (ee.x >> 16)) * po;
+            pz *= pp.x;
+            po *= pp.y;
           }
         }
-        Zh[h] = Zs, Oh[h] = Os, nzh[h] = zp;
+        Zh[h] = Zs, Oh[h] = Os;
+        nzh[h] = (uint32_t)(HW * SPW) - (uint32_t)__popc(m[h]);  // (positions past the tile end count as zeros)
       }
       // 64-bit strings (low, high).  Positions past the tile end (m = 0)
       // count as zeros after every valid zero: the zero string is cut to nzl
