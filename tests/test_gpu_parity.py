@@ -85,6 +85,23 @@ def test_two_hundred_random_cases(wt):
         check_case(wt, S, sigma, f"k={k}")
 
 
+@pytest.mark.parametrize("y", [4, 8, 12, 14])
+def test_cont_rand_locality(wt, y):
+    # the paper's locality workloads: n/sigma copies of each symbol,
+    # sorted (cont) or shuffled (rand), 4-byte symbols; cont makes every T_l = S
+    sigma = 1 << y
+    for kind in ("cont", "rand"):
+        S = wt_inputs.random_case(y, 150_001, sigma, kind, dtype=np.uint32)
+        tree = check_case(wt, S, sigma, f"{kind} sigma=2^{y}")
+        if kind == "cont":
+            B, _, _ = np_tree(tree)
+            L = tree.levels
+            bits = ((S[None, :] >> (L - 1 - np.arange(L))[:, None]) & 1).astype(np.uint8)
+            packed = np.packbits(bits, axis=1, bitorder="little")
+            for l in range(L):
+                assert np.array_equal(B[l].view(np.uint8)[:packed.shape[1]], packed[l])
+
+
 def test_many_tiles_lookback(wt):
     # thousands of tiles per level: exercises look-back windows beyond 32 tiles
     for sigma, dtype in [(4, np.uint8), (256, np.uint8), (1 << 16, np.uint16), (1 << 20, np.uint32)]:
