@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const uint32_t hh = soff / 32, sub = soff % 32;
     const uint32_t submask = lowmask(sub), subhead = lowmask(sub + 1);
     const uint32_t lutrot = (sub - 3u) & 31u;  // rotr by this puts bits [sub, sub + 4) at [3, 7)
+    const uint32_t rot2 = (sub - 1u) & 31u;    // rotr by this puts bits [sub, sub + 2) at [1, 3)
     const uint4* own = S.own + (NH == 1 ? 0 : hh);  // own[NH * owner]
     // (4-byte entries: the 16 entries span 16 banks, one wavefront per word round)
     auto lut_of = [&](uint32_t m4) -> uint2 {
@@ -580,7 +581,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
             const uint2 ow = *reinterpret_cast<const uint2*>(&own[NH * (w / XW)]);
             xs[k] = Win[w];
             Rs[k] = ow.y + (uint32_t)__popc(ow.x & submask);
-            ms[k] = SPW == 4 ? ow.x : ow.x >> sub;
+            ms[k] = SPW == 1 ? ow.x >> sub : ow.x;  // (u8, u16: rotated at use)
           }
 #pragma unroll
           for (int k = 0; k < BK; ++k) {
@@ -592,8 +593,21 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
             }
           }
 #pragma unroll
-          for (int k = 0; k < BK; ++k)
-            word_one_segment(xs[k], (lane + 32 * (k0 + k)) * SPW, Rs[k], ms[k], Z0, O0, es[k]);
+          for (int k = 0; k < BK; ++k) {
+            if constexpr (SPW == 2) {
+              // u16: one rotation brings both symbols' bits to bits 1 and 2
+              // (bit 1 = 2 if symbol 0 is a one); Az / Ao are symbol 0's zero /
+              // one slots, symbol 1 goes 2 bytes after the slot of its kind
+              // minus what symbol 0 took
+              const uint32_t r = __funnelshift_r(ms[k], ms[k], rot2), t = r & 2u;
+              const uint32_t q0 = (lane + 32 * (k0 + k)) * 2u;
+              const uint32_t Az = Z0 + 2u * q0 - 2u * Rs[k], Ao = O0 + 2u * Rs[k];
+              st_shared<T, 0>(t ? Ao : Az, xs[k]);
+              st_shared<T, 0>((r & 4u) ? Ao + t : Az + 2u - t, xs[k] >> 16);
+            } else {
+              word_one_segment(xs[k], (lane + 32 * (k0 + k)) * SPW, Rs[k], ms[k], Z0, O0, es[k]);
+            }
+          }
         }
       } else {  // the last, partial tile
         const uint2 kF = make_uint2(Z0, O0);
