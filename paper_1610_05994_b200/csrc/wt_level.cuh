@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         const uint32_t b = r2 ? b2 : b1, l = r2 ? o0 : z0, D = r2 ? D0o : D0z;
         const uint32_t fs = (b + A - 1) & ~(uint32_t)(A - 1), fe = (b + l) & ~(uint32_t)(A - 1);
         if (lane < 2 && fe > fs) bulk_s2g(out + (D - b + fs), S.buf[ob] + fs, (fe - fs) * (uint32_t)sizeof(T));
-        if (lane < (uint32_t)LV_NREG) bulk_commit();
+        bulk_commit();  // every lane (empty groups too): no divergence
 #pragma unroll
         for (uint32_t base = 0; base < (uint32_t)(4 * A); base += 32) {
           const uint32_t slot = base + lane, e = slot % (2 * A);
@@ -1003,7 +1003,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
 #pragma unroll
           for (int r = 0; r < LV_NREG; ++r) emit_region(rb[r], rl[r], rD[r]);
         }
-        if (lane < (uint32_t)LV_NREG) bulk_commit();  // lanes 1.. commit empty groups (uniform wait below)
+        bulk_commit();  // every lane commits (empty groups too): a uniform wait below, no divergence
       } else {
         // lane r < LV_NREG: region r's bulk store; then all regions' edge
         // symbols (<= 2A each) as one lane-parallel list of slots
@@ -1017,7 +1017,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         const int32_t end = b + l, fs = (b + A - 1) / A * A, fe = end / A * A;
         const uint32_t Dmb = D - (uint32_t)b;  // HBM position of stage position q: Dmb + q
         if (l > 0 && fe > fs) bulk_s2g(out + (Dmb + (uint32_t)fs), S.buf[ob] + fs, (uint32_t)(fe - fs) * (uint32_t)sizeof(T));
-        if (lane < (uint32_t)LV_NREG) bulk_commit();
+        bulk_commit();  // every lane (empty groups too): no divergence
         const int32_t hend = l > 0 ? min(fs, end) : b, tst = max(fe, hend), endv = l > 0 ? end : b;
 #pragma unroll
         for (uint32_t base = 0; base < (uint32_t)(2 * A * LV_NREG); base += 32) {
@@ -1041,14 +1041,14 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       }  // !BITS
     }
     // the previous tile's output buffer: once its bulk stores have read it, load a new tile into it
-    if (lane < (uint32_t)LV_NREG) bulk_wait_read<1>();  // each lane's own groups
+    bulk_wait_read<1>();  // each lane waits for its own groups (lanes without bulk stores: empty)
     __syncwarp();
     if (lane == 0 && it >= 1) issue(it + NB - 2);
   }
   pdl_trigger();  // (at the tail: the next launch's CTAs do not crowd the pass)
   if (SCATTER) {
     cc_flush();
-    if (lane < (uint32_t)LV_NREG) bulk_wait<0>();
+    bulk_wait<0>();
   }
 }
 
