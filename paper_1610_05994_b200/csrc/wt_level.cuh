@@ -719,9 +719,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
 
       // ---------------- constants of the tile's regions (every lane; lane r keeps region r)
       const bool segtab = nseg <= (uint32_t)Cfg::MAXSEG;  // warp-uniform
-      constexpr bool one = false;  // (this branch: nseg > 1)
-      const int32_t s1 = one ? (int32_t)len : S.s1, am = one ? (int32_t)len : S.am;
-      const int32_t Rs1 = one ? (int32_t)tot : S.Rs1, Ram = one ? (int32_t)tot : S.Ram;
+      const int32_t s1 = S.s1, am = S.am, Rs1 = S.Rs1, Ram = S.Ram;
       const int32_t z0 = s1 - Rs1, o0 = Rs1;
       const int32_t om = (int32_t)tot - Ram, zm = ((int32_t)len - am) - om;
       // HBM destinations (mod 2^32 arithmetic; the results are positions < n)
@@ -741,7 +739,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       const uint32_t rD[LV_NREG] = {T0 + (uint32_t)s1, D0z, D0o, Dmz, Dmo};  // HBM destination of rb[r]
       // symbols of side region r with rank < ksplit_r land in destination tile
       // floor(D_r / TILE), the rest in the next tile
-      if (segtab && !one) {
+      if (segtab) {
         if (lane == 0) S.kt[0] = make_uint2(sa(K0F), sa(K1F));
         if (lane == 1) S.kt[nseg - 1] = make_uint2(sa(K0L), sa(K1L));
         // interior segment g (1 <= g <= nseg-2) lies wholly inside the tile: its
@@ -797,14 +795,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           if (lane == (uint32_t)key + 1) mycnt = sum >> 16;
         };
         uint32_t M[NH], lo, hi;
-        if (one) {  // warp-uniform: one segment, only the first-segment runs
-#pragma unroll
-          for (int h = 0; h < NH; ++h) M[h] = vm[h] & ~m[h];
-          split(M, (int32_t)(i0 - mypre), ksplit(D0z, z0), lo, hi);
-          put2(2, lo, hi);
-          split(m, (int32_t)mypre, ksplit(D0o, o0), lo, hi);
-          put2(4, lo, hi);
-        } else {
+        {
           uint32_t fm[NH], lm[NH];
 #pragma unroll
           for (int h = 0; h < NH; ++h) {
@@ -839,17 +830,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       // ---------------- progressive counting: level-(l+2) node sizes, i.e. the
       // symbols of each level-l node by their (level-l, level-(l+1)) bit pair
 #ifndef WT_EXP_SKIP_PCOUNT
-      if (one) {  // warp-uniform: all symbols in node vF.  The (b, nb) pair counts
-        // follow from the next-level ones already reduced above (keys 2..5: nb
-        // ones among the zeros / the ones, split by destination tile)
-        const uint32_t c01 = __shfl_sync(FULL, mycnt, 2) + __shfl_sync(FULL, mycnt, 3);
-        const uint32_t c11 = __shfl_sync(FULL, mycnt, 4) + __shfl_sync(FULL, mycnt, 5);
-        if (vF != cc_node) {
-          cc_flush();
-          cc_node = vF;
-        }
-        cc_acc += lane == 0 ? (len - tot) - c01 : lane == 1 ? c01 : lane == 2 ? tot - c11 : c11;
-      } else if (nvalid) {  // the lane's pieces: maximal runs of its symbols inside one node
+      if (nvalid) {  // the lane's pieces: maximal runs of its symbols inside one node
         // (two node counts per 64-bit atomic: each stays < 2^32, no carry)
         auto piece = [&](uint32_t node, uint32_t c00, uint32_t c01, uint32_t c10, uint32_t c11) {
           unsigned long long* dst = reinterpret_cast<unsigned long long*>(cnt_next + 4u * node);
@@ -885,7 +866,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         }
       }
 #endif
-      if (segtab && !one) __syncwarp();  // kt[]
+      if (segtab) __syncwarp();  // kt[]
 
       // ---------------- phase D: every symbol from the input buffer to its stage position
 #ifndef WT_EXP_SKIP_D
@@ -996,13 +977,8 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         if (lane < (uint32_t)(2 * A) && ((lane < (uint32_t)A) ? (q < hend) : (q < end))) go[q] = S.buf[ob][q];
       };
       if constexpr (sizeof(T) == 1) {  // (A = 16: one region's two edges fill the warp)
-        if (one) {  // warp-uniform: the first segment's two runs only
-          emit_region(b1, z0, D0z);
-          emit_region(b2, o0, D0o);
-        } else {
 #pragma unroll
-          for (int r = 0; r < LV_NREG; ++r) emit_region(rb[r], rl[r], rD[r]);
-        }
+        for (int r = 0; r < LV_NREG; ++r) emit_region(rb[r], rl[r], rD[r]);
         bulk_commit();  // every lane commits (empty groups too): a uniform wait below, no divergence
       } else {
         // lane r < LV_NREG: region r's bulk store; then all regions' edge
@@ -1035,7 +1011,7 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
       if (lane < (uint32_t)LV_NKEY && mycnt) {  // next-level ones per destination tile
         const int r = (int)(lane >> 1);
         uint32_t D = r == 1 ? D0z : D0o;
-        if (!one) D = r == 3 ? Dmz : r == 4 ? Dmo : D;
+        D = r == 3 ? Dmz : r == 4 ? Dmo : D;
         atomicAdd(&agg_next[r == 0 ? tile : D / TILE + (lane & 1)], mycnt);
       }
       }  // !BITS
