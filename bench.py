@@ -192,6 +192,23 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def max_over_ranks(ms: float, world: int, device) -> float:
+    """The step time of an N-rank job: the slowest rank's device time (all_reduce MAX).
+    device: the collective's tensor device (cuda for NCCL, cpu for gloo)."""
+    if world <= 1:
+        return ms
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(n_per_rank: int, world: int, ms_per_step: float) -> float:
+    """Whole-job Gsymbols/s: every rank builds its own replica of n symbols (weak scaling)."""
+    return world * n_per_rank / (ms_per_step * 1e-3) / 1e9
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -251,13 +268,9 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    elapsed_ms = t_start.elapsed_time(t_end)
-    if world > 1:
-        t = torch.tensor([elapsed_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+    elapsed_ms = max_over_ranks(t_start.elapsed_time(t_end), world, dev)
     ms_per_step = elapsed_ms / steps
-    value = world * n / (ms_per_step * 1e-3) / 1e9
+    value = job_throughput(n, world, ms_per_step)
 
     # timed region 2 (the per-kernel breakdown and roofline): the same K builds
     # with a CUDA event pair recorded by the library around every launch, on
@@ -295,7 +308,7 @@ def main():
             g1.record(stream)
             torch.cuda.synchronize()
             gms = g0.elapsed_time(g1) / steps
-            graph = {"ms_per_step": gms, "value": world * n / (gms * 1e-3) / 1e9, "unit": UNIT}
+            graph = {"ms_per_step": gms, "value": job_throughput(n, world, gms), "unit": UNIT}
             assert int(status.item()) == wt.WT_OK
         except Exception as e:  # report, do not fail the bench line
             graph = {"error": str(e)[:200]}
@@ -361,12 +374,8 @@ def main():
             streams[0].wait_event(done)
         e1.record(streams[0])
         torch.cuda.synchronize()
-        e_ms = e0.elapsed_time(e1) / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        e2e = {"value": world * n / (e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e_ms,
+        e_ms = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, world, dev)
+        e2e = {"value": job_throughput(n, world, e_ms), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": n * w,
                "d2h_bytes_per_step": int(sz.bitmap_bytes + sz.superblock_bytes + sz.node_offset_bytes + 4),
                "api": f"wt_build_from_host_async (pinned host buffers; {INFLIGHT} builds in flight on "
