@@ -183,6 +183,31 @@ wt_status wt_select(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uin
                     const uint64_t* d_j, uint64_t m, uint64_t* d_out, int32_t* d_status,
                     wt_stream_t stream);
 
+/*
+ * Select index (createRankSelect's select half):
+ * per level l and bit value b, the position of every 4096-th bit equal to b:
+ *   d_samples[(2 l + b) * Q + k] = position of the (4096 k)-th (0-based) bit
+ *   equal to b in B_l, or n when the level has fewer such bits,
+ * with Q = wt_select_index_entries(n) / (2 L) = n / 4096 + 2 uint32 entries.
+ * Built from a finished tree (device pointers) in one pass over the bitmaps
+ * (L * n / 8 bytes); like the paper's rank/select structures it is not part
+ * of the tree construction.  d_samples: caller-owned device memory of
+ * wt_select_index_entries(n, sigma) uint32.  Asynchronous.
+ * Errors: WT_ERR_ARG (NULL pointers, bad sigma), WT_ERR_CUDA.
+ */
+uint64_t wt_select_index_entries(uint64_t n, uint64_t sigma);
+wt_status wt_select_index(const wt_tree_t* tree, uint64_t n, uint64_t sigma, uint32_t* d_samples,
+                          wt_stream_t stream);
+
+/*
+ * wt_select_indexed: wt_select with the select index of the same tree: each
+ * level's superblock search is narrowed to the stretch between two samples
+ * (at most 4096 bits of that value).  Same results and errors as wt_select.
+ */
+wt_status wt_select_indexed(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint32_t* d_samples,
+                            const uint32_t* d_c, const uint64_t* d_j, uint64_t m, uint64_t* d_out,
+                            int32_t* d_status, wt_stream_t stream);
+
 /* Kernel launches one wt_build_async(n, sigma, width) enqueues, and their kinds
  * (kinds may be NULL): 1 pass over S (prologue), 2 scan of node_offsets
  * (sigma = 1 only), 4 level pass with scatter (a3), 5 last level (a4, only

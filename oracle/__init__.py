@@ -132,6 +132,20 @@ class OracleTree:
     def rank1(self, level: int, q: int) -> int:
         return int(lib().oracle_rank1(_ptr(self.bitmaps[level]), _ptr(self.superblocks[level]), q))
 
+    def select_samples(self, shift: int = 12) -> np.ndarray:
+        """The select index by its definition (createRankSelect's select half,
+        P:556, 599-600): out[l, b, k] = position of the (k * 2^shift)-th (0-based)
+        bit equal to b in B_l, n where the level has fewer; shape (L, 2, n >> shift + 2).
+        Plain numpy over this oracle's bitmaps."""
+        q = (self.n >> shift) + 2
+        out = np.full((self.L, 2, q), self.n, np.uint32)
+        for l in range(self.L):
+            bits = np.unpackbits(self.bitmaps[l].view(np.uint8), bitorder="little")[: self.n]
+            for b in (0, 1):
+                pos = np.flatnonzero(bits == b)[:: 1 << shift]
+                out[l, b, : pos.size] = pos
+        return out
+
 
 def validate(S: np.ndarray, sigma: int) -> int:
     S, w = _seq(S)

@@ -63,6 +63,10 @@ _lib.wt_build_from_host_async.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(
 _lib.wt_access.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _u64, _vp, _vp, _vp]
 _lib.wt_rank.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
 _lib.wt_select.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
+_lib.wt_select_index_entries.argtypes = [_u64, _u64]
+_lib.wt_select_index_entries.restype = _u64
+_lib.wt_select_index.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp]
+_lib.wt_select_indexed.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _vp, _u64, _vp, _vp, _vp]
 _lib.wt_launch_plan.argtypes = [_u64, _u64, _u32, _vp, _u32]
 _lib.wt_launch_plan.restype = _u32
 _lib.wt_debug_offsets.argtypes = [_u64, _u64, _u32, _vp, _u32]
@@ -74,11 +78,12 @@ _lib.wt_status_string.restype = ctypes.c_char_p
 _lib.wt_last_error.argtypes = []
 _lib.wt_last_error.restype = ctypes.c_char_p
 for _f in (_lib.wt_sizes, _lib.wt_build_async, _lib.wt_build, _lib.wt_build_from_host,
-           _lib.wt_build_from_host_async, _lib.wt_access, _lib.wt_rank, _lib.wt_select):
+           _lib.wt_build_from_host_async, _lib.wt_access, _lib.wt_rank, _lib.wt_select, _lib.wt_select_index,
+           _lib.wt_select_indexed):
     _f.restype = ctypes.c_int
 
 EXPORTS = ["wt_sizes", "wt_build_async", "wt_build", "wt_build_from_host", "wt_build_from_host_async",
-           "wt_access", "wt_rank",
+           "wt_access", "wt_rank", "wt_select_index_entries", "wt_select_index", "wt_select_indexed",
            "wt_select", "wt_launch_plan", "wt_debug_offsets", "wt_set_profile_events", "wt_status_string",
            "wt_last_error"]
 
@@ -326,16 +331,43 @@ def rank(tree: WaveletTree, c: torch.Tensor, pos: torch.Tensor, stream=None,
     return out
 
 
+SELECT_SAMPLE_SHIFT = 12  # the select index samples every 2^12-th bit of each value
+
+
+def select_index(tree: WaveletTree, stream=None) -> torch.Tensor:
+    """wt_select_index: per level l and bit b, the positions of every 4096-th bit equal to
+    b, as an int32 tensor of shape (L, 2, n // 4096 + 2) (entries past the count hold n)."""
+    e = int(_lib.wt_select_index_entries(tree.n, tree.sigma))
+    L = tree.levels
+    q = tree.n // 4096 + 2
+    out = torch.empty((L, 2, q) if L else (0,), dtype=torch.int32, device=tree.bitmaps.device)
+    assert out.numel() == e
+    ct = tree._ctree()
+    st = _lib.wt_select_index(ctypes.byref(ct), tree.n, tree.sigma, out.data_ptr() if e else None,
+                              _stream_ptr(stream))
+    _check(st, "wt_select_index")
+    return out
+
+
 def select(tree: WaveletTree, c: torch.Tensor, j: torch.Tensor, stream=None,
-           status: torch.Tensor | None = None) -> torch.Tensor:
-    """position of the j-th (1-based) occurrence of c, for paired batches."""
+           status: torch.Tensor | None = None, index: torch.Tensor | None = None) -> torch.Tensor:
+    """position of the j-th (1-based) occurrence of c, for paired batches; with the tree's
+    select index (select_index) each level's search is narrowed to one sample stretch."""
     c = c.to(torch.int32).contiguous()
     j = j.to(torch.int64).contiguous()
     m = j.numel()
     out = torch.empty(m, dtype=torch.int64, device=j.device)
     ct = tree._ctree()
-    st = _lib.wt_select(ctypes.byref(ct), tree.n, tree.sigma, c.data_ptr() if m else None,
-                        j.data_ptr() if m else None, m, out.data_ptr() if m else None,
-                        status.data_ptr() if status is not None else None, _stream_ptr(stream))
-    _check(st, "wt_select")
+    if index is None:
+        st = _lib.wt_select(ctypes.byref(ct), tree.n, tree.sigma, c.data_ptr() if m else None,
+                            j.data_ptr() if m else None, m, out.data_ptr() if m else None,
+                            status.data_ptr() if status is not None else None, _stream_ptr(stream))
+        _check(st, "wt_select")
+    else:
+        st = _lib.wt_select_indexed(ctypes.byref(ct), tree.n, tree.sigma,
+                                    index.data_ptr() if index.numel() else None,
+                                    c.data_ptr() if m else None, j.data_ptr() if m else None, m,
+                                    out.data_ptr() if m else None,
+                                    status.data_ptr() if status is not None else None, _stream_ptr(stream))
+        _check(st, "wt_select_indexed")
     return out

@@ -592,7 +592,51 @@ wt_status wt_select(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uin
   if (!d_c || !d_j || !d_out) return fail(WT_ERR_ARG, "NULL query pointer");
   const uint32_t grid = (uint32_t)((m + 255) / 256);
   wt::k_select<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      view_of(tree, n, sigma), sigma, d_c, d_j, m, reinterpret_cast<unsigned long long*>(d_out), d_status);
+      view_of(tree, n, sigma), sigma, d_c, d_j, m, reinterpret_cast<unsigned long long*>(d_out), d_status, nullptr);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_select");
+}
+
+uint64_t wt_select_index_entries(uint64_t n, uint64_t sigma) {
+  if (sigma == 0 || levels_of(sigma) > 30) return 0;
+  return 2ull * levels_of(sigma) * wt::select_samples_per_level(n);
+}
+
+wt_status wt_select_index(const wt_tree_t* tree, uint64_t n, uint64_t sigma, uint32_t* d_samples,
+                          wt_stream_t stream) {
+  g_last_error.clear();
+  wt_status st = query_args(tree, n, sigma);
+  if (st != WT_OK) return st;
+  const uint32_t L = levels_of(sigma);
+  if (L == 0) return WT_OK;
+  if (!d_samples) return fail(WT_ERR_ARG, "NULL samples pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const wt::TreeView v = view_of(tree, n, sigma);
+  const uint64_t entries = wt_select_index_entries(n, sigma);
+  wt::k_fill_u32<<<(uint32_t)std::min<uint64_t>((entries + 255) / 256, 4ull * num_sms()), 256, 0, s>>>(
+      d_samples, entries, (uint32_t)n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail_cuda(e, "k_fill_u32");
+  const uint64_t blocks = (uint64_t)L * (v.NSB - 1);
+  if (blocks) {
+    wt::k_select_samples_fill<<<(uint32_t)((blocks + 255) / 256), 256, 0, s>>>(v, d_samples);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_select_samples_fill");
+  }
+  return WT_OK;
+}
+
+wt_status wt_select_indexed(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint32_t* d_samples,
+                            const uint32_t* d_c, const uint64_t* d_j, uint64_t m, uint64_t* d_out,
+                            int32_t* d_status, wt_stream_t stream) {
+  g_last_error.clear();
+  wt_status st = query_args(tree, n, sigma);
+  if (st != WT_OK) return st;
+  if (m == 0) return WT_OK;
+  if (!d_c || !d_j || !d_out || (levels_of(sigma) > 0 && !d_samples)) return fail(WT_ERR_ARG, "NULL pointer");
+  const uint32_t grid = (uint32_t)((m + 255) / 256);
+  wt::k_select<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      view_of(tree, n, sigma), sigma, d_c, d_j, m, reinterpret_cast<unsigned long long*>(d_out), d_status,
+      d_samples);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_select");
 }

@@ -298,9 +298,57 @@ __global__ void k_rank(TreeView t, uint64_t sigma, const uint32_t* __restrict__ 
   cnt[k] = r;
 }
 
-// position of the `target`-th (1-based, global) bit equal to b in one level
+// Select index (NEXT-1; createRankSelect's select half):
+// per level and bit value b, the position of every 2^SEL_SHIFT-th bit equal to
+// b: samples[l][b][k] = position of the (k * 2^SEL_SHIFT)-th (0-based) such bit;
+// entries past the level's count hold n.  One thread per 512-bit block finds
+// the multiples of 2^SEL_SHIFT that fall inside its block from SB.
+constexpr uint32_t SEL_SHIFT = 12;
+__host__ __device__ constexpr uint64_t select_samples_per_level(uint64_t n) { return (n >> SEL_SHIFT) + 2; }
+
+__global__ void k_fill_u32(uint32_t* __restrict__ p, uint64_t count, uint32_t value) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] = value;
+}
+
+__global__ void k_select_samples_fill(TreeView t, uint32_t* __restrict__ samples) {
+  const uint64_t nblk = t.NSB - 1, Q = select_samples_per_level(t.n);
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (uint64_t)t.L * nblk) return;
+  const uint32_t l = (uint32_t)(gid / nblk);
+  const uint64_t blk = gid % nblk;
+  const uint32_t* B = t.bitmaps + (uint64_t)l * t.W + 16 * blk;
+  const unsigned long long* SB = t.sb + (uint64_t)l * t.NSB;
+  const uint64_t pos0 = blk * 512, len = min((uint64_t)512, t.n - pos0);
+  const uint64_t r1 = SB[blk], r0 = pos0 - r1;
+  const uint64_t c1 = SB[blk + 1] - r1, c0 = len - c1;
+#pragma unroll
+  for (uint32_t b = 0; b < 2; ++b) {
+    const uint64_t r = b ? r1 : r0, c = b ? c1 : c0;
+    const uint64_t S = 1ull << SEL_SHIFT;
+    uint64_t k = (r + S - 1) >> SEL_SHIFT;  // first multiple of S at or after rank r
+    for (; (k << SEL_SHIFT) < r + c; ++k) {  // (at most one per block: 512 < S)
+      uint64_t need = (k << SEL_SHIFT) - r + 1;  // 1-based rank inside the block
+      for (uint32_t w = 0; w < 16; ++w) {
+        uint32_t word = b ? B[w] : ~B[w];
+        if (32 * w + 32 > len) word &= (len > 32 * w) ? ((len - 32 * w >= 32) ? ~0u : ((1u << (len - 32 * w)) - 1u)) : 0u;
+        const uint32_t pc = (uint32_t)__popc(word);
+        if (need <= pc) {
+          for (uint64_t d = 1; d < need; ++d) word &= word - 1;
+          samples[((uint64_t)l * 2 + b) * Q + k] = (uint32_t)(pos0 + 32 * w + (uint32_t)(__ffs(word) - 1));
+          break;
+        }
+        need -= pc;
+      }
+    }
+  }
+}
+
+// position of the `target`-th (1-based, global) bit equal to b in one level;
+// [tlo, thi] brackets the answer's superblock (the whole level without an index)
 __device__ uint64_t select_bit(const uint32_t* __restrict__ B, const unsigned long long* __restrict__ SB,
-                               uint64_t n, uint64_t nsb, uint32_t b, uint64_t target) {
+                               uint64_t n, uint64_t nsb, uint32_t b, uint64_t target, uint64_t tlo = 0,
+                               uint64_t thi = ~0ull) {
   // rank_b at superblock t
   auto rb = [&](uint64_t t) -> uint64_t {
     const uint64_t ones = SB[t];
@@ -308,7 +356,7 @@ __device__ uint64_t select_bit(const uint32_t* __restrict__ B, const unsigned lo
     return b ? ones : pos - ones;
   };
   // largest t with rb(t) < target
-  uint64_t lo = 0, hi = nsb - 1;  // rb(0) = 0 < target, rb(nsb-1) = total >= target
+  uint64_t lo = tlo, hi = min(thi, nsb - 1);  // rb(lo) < target <= rb(hi)
   while (hi - lo > 1) {
     const uint64_t mid = (lo + hi) >> 1;
     if (rb(mid) < target) lo = mid;
@@ -330,7 +378,7 @@ __device__ uint64_t select_bit(const uint32_t* __restrict__ B, const unsigned lo
 
 __global__ void k_select(TreeView t, uint64_t sigma, const uint32_t* __restrict__ cs,
                          const uint64_t* __restrict__ js, uint64_t m, unsigned long long* __restrict__ out,
-                         int32_t* status) {
+                         int32_t* status, const uint32_t* __restrict__ samples) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m) return;
   const uint64_t c = cs[k], j = js[k];
@@ -347,7 +395,17 @@ __global__ void k_select(TreeView t, uint64_t sigma, const uint32_t* __restrict_
     const uint64_t lo = t.C[v << (t.L - l)];
     const uint32_t b = (uint32_t)(c >> (t.L - 1 - l)) & 1u;
     const uint64_t before = b ? rank1(B, SB, lo) : lo - rank1(B, SB, lo);
-    const uint64_t q = select_bit(B, SB, t.n, t.NSB, b, before + p + 1);
+    const uint64_t target = before + p + 1;
+    uint64_t tlo = 0, thi = ~0ull;
+    if (samples) {  // the sampled positions bracket the target's superblock
+      const uint64_t Q = select_samples_per_level(t.n);
+      const uint32_t* sm = samples + ((uint64_t)l * 2 + b) * Q;
+      const uint64_t kk = (target - 1) >> SEL_SHIFT;
+      tlo = sm[kk] / 512;                 // the (kk * 2^s)-th bit is at or before the target
+      const uint32_t nx = sm[kk + 1];     // the next sample (or n) is at or after it
+      thi = (uint64_t)nx / 512 + 1;
+    }
+    const uint64_t q = select_bit(B, SB, t.n, t.NSB, b, target, tlo, thi);
     p = q - lo;
   }
   out[k] = p;

@@ -232,6 +232,35 @@ def test_queries(wt, sigma, n):
             want.append(occ[j - 1])
     got = tree.select(torch.tensor(np.array(cs, np.int32)).cuda(), torch.tensor(js).cuda()).cpu().numpy()
     assert np.array_equal(got, np.array(want))
+    # the select index (NEXT-1): the samples equal the oracle's by definition, and
+    # the indexed select returns the same positions
+    idx = wt.select_index(tree)
+    if ot.L:
+        assert np.array_equal(idx.cpu().numpy().view(np.uint32), ot.select_samples(12))
+        got2 = wt.select(tree, torch.tensor(np.array(cs, np.int32)).cuda(), torch.tensor(js).cuda(),
+                         index=idx).cpu().numpy()
+        assert np.array_equal(got2, np.array(want))
+
+
+@pytest.mark.parametrize("sigma,n", [(2, 1), (4, 511), (4, 512), (256, 4097), (256, 300_001), (1 << 16, 1_000_003)])
+def test_select_index_edges(wt, sigma, n):
+    # sample boundaries: n around 512 / 4096, a single symbol, many samples per level
+    S = wt_inputs.random_case(n, n, sigma, "uniform", dtype=np.uint16 if sigma > 256 else None)
+    tree = check_case(wt, S, sigma)
+    ot = oracle.build(S, sigma)
+    idx = wt.select_index(tree)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), ot.select_samples(12))
+    rng = np.random.default_rng(n)
+    cs, js, want = [], [], []
+    for sym in rng.choice(np.unique(S), size=min(50, np.unique(S).size), replace=False):
+        occ = np.nonzero(S == sym)[0]
+        for j in np.unique(rng.integers(1, occ.size + 1, 5)):
+            cs.append(sym)
+            js.append(int(j))
+            want.append(occ[j - 1])
+    c_t = torch.tensor(np.array(cs, np.int32)).cuda()
+    j_t = torch.tensor(js).cuda()
+    assert np.array_equal(wt.select(tree, c_t, j_t, index=idx).cpu().numpy(), np.array(want))
 
 
 def test_query_index_errors(wt):

@@ -212,6 +212,27 @@ def test_queries_vs_brute_force(sigma):
             assert t.select(c, k + 1) == int(occ[k])
 
 
+def test_select_samples_vs_brute_force():
+    # the select index (NEXT-1) pinned to the brute-force bitmaps (stable-sort
+    # definition) and to occurrence counting: sample k of (level l, bit b) is the
+    # position of the (k * 2^s)-th b-bit; a small shift exercises many samples
+    for sigma, n, kind in [(16, 5000, "zipf"), (256, 20000, "uniform"), (3, 9001, "runs"), (1 << 10, 777, "sorted")]:
+        S = wt_inputs.random_case(n + sigma, n, sigma, kind)
+        ot = oracle.build(S, sigma)
+        shift = 5
+        smp = ot.select_samples(shift)
+        for l, bits in enumerate(brute.levels_by_stable_sort(S, sigma)):
+            bits = np.asarray(bits, np.uint8)
+            for b in (0, 1):
+                cnt = 0
+                for q in range(n):       # walk the level: every 2^shift-th b-bit is sampled
+                    if bits[q] == b:
+                        if cnt % (1 << shift) == 0:
+                            assert smp[l, b, cnt >> shift] == q
+                        cnt += 1
+                assert np.all(smp[l, b, (cnt + (1 << shift) - 1) >> shift:] == n)   # the rest: sentinel n
+
+
 def test_sigma_one_and_empty():
     t = oracle.build(np.zeros(5, np.uint8), 1)
     assert t.L == 0 and list(t.node_offsets) == [0, 5]
