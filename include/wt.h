@@ -208,6 +208,33 @@ wt_status wt_select_indexed(const wt_tree_t* tree, uint64_t n, uint64_t sigma, c
                             const uint32_t* d_c, const uint64_t* d_j, uint64_t m, uint64_t* d_out,
                             int32_t* d_status, wt_stream_t stream);
 
+/*
+ * Wavelet matrix (NEXT-4; the variant P:1409-1413 names): level l is the
+ * sequence T_l stably partitioned, over the WHOLE sequence (no nodes), by bit
+ * (L-1-l): T_0 = S, T_{l+1} = zeros of T_l then ones; B_l[j] = bit (L-1-l) of
+ * T_l[j]; zeros[l] = number of zeros of level l.  Same bitmap and superblock
+ * layout as the tree (bitmaps L x words_per_level, superblocks L x
+ * sb_per_level); zeros: L uint64.  Built by the same level kernels with one
+ * global node per level; workspace as wt_sizes().workspace_bytes.
+ * d_status as wt_build_async.  Errors as wt_build_async.
+ */
+typedef struct {
+  uint32_t* bitmaps;
+  uint64_t* superblocks;
+  uint64_t* zeros;
+} wt_matrix_t;
+
+wt_status wt_matrix_build_async(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t width,
+                                const wt_matrix_t* out, void* d_workspace, size_t workspace_bytes,
+                                int32_t* d_status, wt_stream_t stream);
+/* d_sym[k] = S[d_pos[k]] (positions >= n: UINT32_MAX and *d_status = WT_ERR_INDEX). */
+wt_status wt_matrix_access(const wt_matrix_t* mx, uint64_t n, uint64_t sigma, const uint64_t* d_pos,
+                           uint64_t m, uint32_t* d_sym, int32_t* d_status, wt_stream_t stream);
+/* d_cnt[k] = #{j <= d_pos[k] : S[j] = d_c[k]} (inclusive; invalid: UINT64_MAX, WT_ERR_INDEX). */
+wt_status wt_matrix_rank(const wt_matrix_t* mx, uint64_t n, uint64_t sigma, const uint32_t* d_c,
+                         const uint64_t* d_pos, uint64_t m, uint64_t* d_cnt, int32_t* d_status,
+                         wt_stream_t stream);
+
 /* Kernel launches one wt_build_async(n, sigma, width) enqueues, and their kinds
  * (kinds may be NULL): 1 pass over S (prologue), 2 scan of node_offsets
  * (sigma = 1 only), 4 level pass with scatter (a3), 5 last level (a4, only

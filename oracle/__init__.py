@@ -186,3 +186,43 @@ def build(S: np.ndarray, sigma: int) -> OracleTree:
     if st != OK:
         raise OracleError(st, "build")
     return OracleTree(n=n, sigma=sigma, L=L, bitmaps=B, superblocks=SB, node_offsets=C)
+
+
+@dataclass
+class OracleMatrix:
+    n: int
+    sigma: int
+    L: int
+    bitmaps: np.ndarray        # (L, words_per_level) uint32, LSB-first
+    superblocks: np.ndarray    # (L, sb_per_level) uint64
+    zeros: np.ndarray          # (L,) uint64
+
+
+def build_matrix(S: np.ndarray, sigma: int) -> OracleMatrix:
+    """The wavelet matrix (NEXT-4) by its definition, plain numpy:
+    T_0 = S; B_l[j] = bit (L-1-l) of T_l[j]; T_{l+1} = the zeros of T_l then its
+    ones, each in order (a global stable partition, no nodes); zeros[l] = the
+    number of zeros of level l; superblocks as the tree's (one cumulative count
+    per 512 bits plus the total)."""
+    seq = np.asarray(S).astype(np.int64)
+    n = seq.size
+    L = levels(sigma)
+    if n and int(seq.max(initial=0)) >= sigma:
+        raise OracleError(2, "symbol >= sigma")
+    W, NSB = words_per_level(n), sb_per_level(n)
+    bm = np.zeros((L, W), np.uint32)
+    sb = np.zeros((L, NSB), np.uint64)
+    zeros = np.zeros(L, np.uint64)
+    T = seq
+    for l in range(L):
+        bits = ((T >> (L - 1 - l)) & 1).astype(np.uint8)
+        buf = np.zeros(W * 4, np.uint8)
+        packed = np.packbits(bits, bitorder="little")
+        buf[: packed.size] = packed
+        bm[l] = buf.view("<u4")
+        ones_before = np.concatenate([[0], np.cumsum(bits, dtype=np.uint64)])
+        sb[l] = ones_before[np.minimum(np.arange(NSB) * 512, n)]
+        zeros[l] = n - int(bits.sum())
+        T = np.concatenate([T[bits == 0], T[bits == 1]])
+    return OracleMatrix(n, sigma, L, bm, sb, zeros)
+

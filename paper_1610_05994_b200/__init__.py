@@ -63,6 +63,13 @@ _lib.wt_build_from_host_async.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(
 _lib.wt_access.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _u64, _vp, _vp, _vp]
 _lib.wt_rank.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
 _lib.wt_select.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
+class WtMatrix(ctypes.Structure):
+    _fields_ = [("bitmaps", _vp), ("superblocks", _vp), ("zeros", _vp)]
+
+
+_lib.wt_matrix_build_async.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(WtMatrix), _vp, _sz, _vp, _vp]
+_lib.wt_matrix_access.argtypes = [ctypes.POINTER(WtMatrix), _u64, _u64, _vp, _u64, _vp, _vp, _vp]
+_lib.wt_matrix_rank.argtypes = [ctypes.POINTER(WtMatrix), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
 _lib.wt_select_index_entries.argtypes = [_u64, _u64]
 _lib.wt_select_index_entries.restype = _u64
 _lib.wt_select_index.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp]
@@ -79,11 +86,12 @@ _lib.wt_last_error.argtypes = []
 _lib.wt_last_error.restype = ctypes.c_char_p
 for _f in (_lib.wt_sizes, _lib.wt_build_async, _lib.wt_build, _lib.wt_build_from_host,
            _lib.wt_build_from_host_async, _lib.wt_access, _lib.wt_rank, _lib.wt_select, _lib.wt_select_index,
-           _lib.wt_select_indexed):
+           _lib.wt_select_indexed, _lib.wt_matrix_build_async, _lib.wt_matrix_access, _lib.wt_matrix_rank):
     _f.restype = ctypes.c_int
 
 EXPORTS = ["wt_sizes", "wt_build_async", "wt_build", "wt_build_from_host", "wt_build_from_host_async",
            "wt_access", "wt_rank", "wt_select_index_entries", "wt_select_index", "wt_select_indexed",
+           "wt_matrix_build_async", "wt_matrix_access", "wt_matrix_rank",
            "wt_select", "wt_launch_plan", "wt_debug_offsets", "wt_set_profile_events", "wt_status_string",
            "wt_last_error"]
 
@@ -370,4 +378,73 @@ def select(tree: WaveletTree, c: torch.Tensor, j: torch.Tensor, stream=None,
                                     out.data_ptr() if m else None,
                                     status.data_ptr() if status is not None else None, _stream_ptr(stream))
         _check(st, "wt_select_indexed")
+    return out
+
+
+# ---------------------------------------------------------------- wavelet matrix (NEXT-4)
+
+
+@dataclass
+class WaveletMatrix:
+    n: int
+    sigma: int
+    levels: int
+    bitmaps: torch.Tensor       # (L, words_per_level) int32 (uint32 bit pattern)
+    superblocks: torch.Tensor   # (L, sb_per_level) int64
+    zeros: torch.Tensor         # (L,) int64: zeros of each level
+
+    def _cmatrix(self) -> WtMatrix:
+        return WtMatrix(self.bitmaps.data_ptr() if self.bitmaps.numel() else None,
+                        self.superblocks.data_ptr() if self.superblocks.numel() else None,
+                        self.zeros.data_ptr() if self.zeros.numel() else None)
+
+
+def build_matrix(seq: torch.Tensor, sigma: int, workspace: torch.Tensor | None = None,
+                 stream=None) -> WaveletMatrix:
+    """wt_matrix_build_async + one synchronisation to read the range flag."""
+    if not seq.is_cuda:
+        raise ValueError("seq must be a CUDA tensor")
+    seq = seq.contiguous()
+    w = width_of(seq)
+    n = seq.numel()
+    sz = sizes(n, sigma, w)
+    L = sz.levels
+    dev = seq.device
+    mx = WaveletMatrix(n=n, sigma=sigma, levels=L,
+                       bitmaps=torch.empty((L, sz.words_per_level), dtype=torch.int32, device=dev),
+                       superblocks=torch.empty((L, sz.sb_per_level), dtype=torch.int64, device=dev),
+                       zeros=torch.empty((L,), dtype=torch.int64, device=dev))
+    if workspace is None:
+        workspace = alloc_workspace(n, sigma, w, dev)
+    status = _status_tensor(dev)
+    cm = mx._cmatrix()
+    st = _lib.wt_matrix_build_async(seq.data_ptr() if n else None, n, sigma, w, ctypes.byref(cm),
+                                    workspace.data_ptr(), workspace.numel(), status.data_ptr(), _stream_ptr(stream))
+    _check(st, "wt_matrix_build_async")
+    if int(status.item()) != WT_OK:
+        raise WtError(int(status.item()), "wt_matrix_build_async: a symbol is >= sigma")
+    return mx
+
+
+def matrix_access(mx: WaveletMatrix, pos: torch.Tensor, stream=None) -> torch.Tensor:
+    pos = pos.to(torch.int64).contiguous()
+    m = pos.numel()
+    out = torch.empty(m, dtype=torch.int32, device=pos.device)
+    cm = mx._cmatrix()
+    st = _lib.wt_matrix_access(ctypes.byref(cm), mx.n, mx.sigma, pos.data_ptr() if m else None, m,
+                               out.data_ptr() if m else None, None, _stream_ptr(stream))
+    _check(st, "wt_matrix_access")
+    return out.to(torch.int64) & 0xFFFFFFFF
+
+
+def matrix_rank(mx: WaveletMatrix, c: torch.Tensor, pos: torch.Tensor, stream=None) -> torch.Tensor:
+    c = c.to(torch.int32).contiguous()
+    pos = pos.to(torch.int64).contiguous()
+    m = pos.numel()
+    out = torch.empty(m, dtype=torch.int64, device=pos.device)
+    cm = mx._cmatrix()
+    st = _lib.wt_matrix_rank(ctypes.byref(cm), mx.n, mx.sigma, c.data_ptr() if m else None,
+                             pos.data_ptr() if m else None, m, out.data_ptr() if m else None, None,
+                             _stream_ptr(stream))
+    _check(st, "wt_matrix_rank")
     return out

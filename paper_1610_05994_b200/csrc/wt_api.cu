@@ -223,7 +223,11 @@ enum Kind : uint32_t {
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
 template <typename T>
 wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out, char* ws, const Carve& c,
-                  cudaStream_t stream, uint32_t* kinds, uint32_t cap, uint32_t* count) {
+                  cudaStream_t stream, uint32_t* kinds, uint32_t cap, uint32_t* count,
+                  unsigned long long* mzeros = nullptr) {
+  // mzeros != nullptr: the wavelet matrix (NEXT-4): every level one global
+  // node, per-level zeros to mzeros[l], no node offsets
+  const bool matrix = mzeros != nullptr;
   const bool dry = (seq == nullptr && out == nullptr);
   uint32_t nk = 0;
   auto note = [&](uint32_t kind) {
@@ -243,7 +247,7 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   uint32_t* cnt[2] = {reinterpret_cast<uint32_t*>(ws + c.off_cnt),
                       reinterpret_cast<uint32_t*>(ws + c.off_cnt + align_up(c.cnt_entries * sizeof(uint32_t)))};
   T* buf[2] = {reinterpret_cast<T*>(ws + c.off_bufA), reinterpret_cast<T*>(ws + c.off_bufB)};
-  unsigned long long* C = dry ? nullptr : reinterpret_cast<unsigned long long*>(out->node_offsets);
+  unsigned long long* C = (dry || matrix) ? nullptr : reinterpret_cast<unsigned long long*>(out->node_offsets);
   const uint32_t L = c.L;
   Launcher lk{stream};
   cudaError_t e;
@@ -251,7 +255,12 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   if (!dry) {
     if ((e = cudaMemsetAsync(ws, 0, c.ctrl_bytes, stream)) != cudaSuccess) return fail_cuda(e, "memset ctrl");
     if (n == 0) {
-      if ((e = cudaMemsetAsync(C, 0, c.c_len * 8, stream)) != cudaSuccess) return fail_cuda(e, "memset C");
+      if (matrix) {
+        if (L && (e = cudaMemsetAsync(mzeros, 0, (size_t)L * 8, stream)) != cudaSuccess)
+          return fail_cuda(e, "memset zeros");
+      } else if ((e = cudaMemsetAsync(C, 0, c.c_len * 8, stream)) != cudaSuccess) {
+        return fail_cuda(e, "memset C");
+      }
       if (L && (e = cudaMemsetAsync(out->superblocks, 0, (size_t)L * c.nsb * 8, stream)) != cudaSuccess)
         return fail_cuda(e, "memset sb");
       if (count) *count = 0;
@@ -311,6 +320,10 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   };
   const wt::ZeroFill nozero{nullptr, 0, nullptr, 0};
 
+  if (L == 0 && matrix) {  // no levels, nothing but the range check
+    if (count) *count = nk;
+    return WT_OK;
+  }
   if (L == 0) {  // sigma = 1: C = [0, n]
     note(K_SCAN);
     if ((st = scan(wt::OpLeafC{nullptr, C, 1, n, nullptr}, 1, "k_scan(C)")) != WT_OK) return st;
@@ -337,8 +350,8 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
     T* o = mode == 0 ? nullptr : mode == 2 ? reinterpret_cast<T*>(out->bitmaps + (uint64_t)(L - 1) * c.words)
                                            : buf[l & 1];
-    const uint32_t sh = L - 1 - l;
-    const uint2* t = mode == 0 ? nullptr : tab + ((1ull << l) - 1);
+    const uint32_t sh = (L - 1 - l) | (matrix ? wt::LV_MATRIX : 0u);
+    const uint2* t = mode == 0 ? nullptr : matrix ? tab + l : tab + ((1ull << l) - 1);
     uint32_t* bits = out->bitmaps + (uint64_t)l * c.words;
     unsigned long long* sb = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
     uint32_t* agg_next = mode == 1 ? agg + (uint64_t)(l + 1) * c.ntiles : nullptr;
@@ -362,9 +375,14 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   };
 
   if (L == 1) {  // C from ones0, the tile prefixes of level 0, the single (last) level
-    if ((st = prep(K_PREP, wt::OpTilePrefix{agg, pre}, c.ntiles, wt::OpLeafC{nullptr, C, 2, n, ones0}, 2, nozero,
-                   "k_prep")) != WT_OK)
+    if (matrix) {
+      if ((st = prep(K_PREP, wt::OpTilePrefix{agg, pre}, c.ntiles,
+                     wt::OpMatrixTab{agg, tab, mzeros, n, c.ntiles}, c.ntiles, nozero, "k_prep")) != WT_OK)
+        return st;
+    } else if ((st = prep(K_PREP, wt::OpTilePrefix{agg, pre}, c.ntiles, wt::OpLeafC{nullptr, C, 2, n, ones0}, 2,
+                          nozero, "k_prep")) != WT_OK) {
       return st;
+    }
     if ((st = level(0, 0)) != WT_OK) return st;
     if (count) *count = nk;
     return WT_OK;
@@ -382,13 +400,21 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     // pre_l (scan of agg_l), the node tables of level l (from the level-(l+1)
     // node sizes counted by pass l-1, or from ones0 for l = 0), and zero the
     // node-count buffer pass l fills (and B_{L-1}, OR-ed by the fused pass)
-    wt::OpLevelTab tb = (l == 0) ? wt::OpLevelTab{nullptr, tab, n, ones0}
-                                 : wt::OpLevelTab{dry ? nullptr : cnt[(l - 1) & 1], tab + ((1ull << l) - 1), n, nullptr};
-    wt::ZeroFill z{dry ? nullptr : reinterpret_cast<uint4*>(cnt[l & 1]), 1ull << l,
+    wt::ZeroFill z{dry ? nullptr : reinterpret_cast<uint4*>(cnt[l & 1]), matrix ? 1ull : 1ull << l,
                    pair && !dry ? reinterpret_cast<uint4*>(lastbits) : nullptr, pair ? c.words / 4 : 0};
-    if ((st = prep(K_PREP, wt::OpTilePrefix{agg + (uint64_t)l * c.ntiles, pre}, c.ntiles, tb, 1ull << l, z,
-                   "k_prep")) != WT_OK)
-      return st;
+    if (matrix) {  // the level's one-node table from the scan of its per-tile ones
+      wt::OpMatrixTab tb{agg + (uint64_t)l * c.ntiles, tab + l, mzeros + l, n, c.ntiles};
+      if ((st = prep(K_PREP, wt::OpTilePrefix{agg + (uint64_t)l * c.ntiles, pre}, c.ntiles, tb, c.ntiles, z,
+                     "k_prep")) != WT_OK)
+        return st;
+    } else {
+      wt::OpLevelTab tb = (l == 0) ? wt::OpLevelTab{nullptr, tab, n, ones0}
+                                   : wt::OpLevelTab{dry ? nullptr : cnt[(l - 1) & 1], tab + ((1ull << l) - 1), n,
+                                                    nullptr};
+      if ((st = prep(K_PREP, wt::OpTilePrefix{agg + (uint64_t)l * c.ntiles, pre}, c.ntiles, tb, 1ull << l, z,
+                     "k_prep")) != WT_OK)
+        return st;
+    }
     if ((st = level(l, pair ? 2 : 1)) != WT_OK) return st;
   }
   if (Lrun == L - 1) {
@@ -408,21 +434,28 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     }
     unsigned long long* sbl =
         dry ? nullptr : reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)(L - 1) * c.nsb;
-    if ((st = prep(K_FINAL, wt::OpBlockPop{blk, sbl, c.nsb - 1}, c.nsb - 1,
-                   wt::OpLeafC{dry ? nullptr : cnt[(L - 2) & 1], C, 1ull << L, n, nullptr}, 1ull << L, nozero,
-                   "k_prep(final)")) != WT_OK)
+    if (matrix) {
+      if ((st = prep(K_FINAL, wt::OpBlockPopZ{blk, sbl, c.nsb - 1, mzeros + (L - 1), n}, c.nsb - 1, wt::OpNone{}, 0,
+                     nozero, "k_prep(final)")) != WT_OK)
+        return st;
+    } else if ((st = prep(K_FINAL, wt::OpBlockPop{blk, sbl, c.nsb - 1}, c.nsb - 1,
+                          wt::OpLeafC{dry ? nullptr : cnt[(L - 2) & 1], C, 1ull << L, n, nullptr}, 1ull << L, nozero,
+                          "k_prep(final)")) != WT_OK) {
       return st;
+    }
   }
   if (count) *count = nk;
   return WT_OK;
 }
 
 wt_status dispatch(const void* seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* out, char* ws,
-                   const Carve& c, cudaStream_t stream, uint32_t* kinds, uint32_t cap, uint32_t* count) {
+                   const Carve& c, cudaStream_t stream, uint32_t* kinds, uint32_t cap, uint32_t* count,
+                   unsigned long long* mzeros = nullptr) {
   switch (width) {
-    case 1: return enqueue<uint8_t>((const uint8_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count);
-    case 2: return enqueue<uint16_t>((const uint16_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count);
-    default: return enqueue<uint32_t>((const uint32_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count);
+    case 1: return enqueue<uint8_t>((const uint8_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count, mzeros);
+    case 2: return enqueue<uint16_t>((const uint16_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count, mzeros);
+    default:
+      return enqueue<uint32_t>((const uint32_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count, mzeros);
   }
 }
 
@@ -482,6 +515,64 @@ wt_status wt_build_async(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t
     if (e != cudaSuccess) return fail_cuda(e, "status copy");
   }
   return WT_OK;
+}
+
+wt_status wt_matrix_build_async(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t width,
+                                const wt_matrix_t* out, void* d_workspace, size_t workspace_bytes, int32_t* d_status,
+                                wt_stream_t stream) {
+  g_last_error.clear();
+  wt_status st = check_args(n, sigma, width);
+  if (st != WT_OK) return st;
+  const uint32_t L = levels_of(sigma);
+  if (!out || (L > 0 && (!out->zeros || !out->superblocks || (n > 0 && !out->bitmaps))))
+    return fail(WT_ERR_ARG, "output pointers are NULL");
+  if (n > 0 && !d_seq) return fail(WT_ERR_ARG, "d_seq is NULL");
+  if (n > 0 && (reinterpret_cast<uintptr_t>(d_seq) & 15)) return fail(WT_ERR_ARG, "d_seq must be 16-byte aligned");
+  const Carve c = carve(n, sigma, width);
+  if (!d_workspace || workspace_bytes < c.total) return fail(WT_ERR_WORKSPACE, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(d_workspace) & (ALIGN - 1))
+    return fail(WT_ERR_ARG, "workspace must be 256-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(d_workspace);
+  wt_tree_t t{out->bitmaps, out->superblocks, nullptr};
+  unsigned long long dummy = 0;  // (L = 0: no zeros array; the pointer only marks the matrix mode)
+  unsigned long long* z = L ? reinterpret_cast<unsigned long long*>(out->zeros) : &dummy;
+  st = dispatch(d_seq, n, sigma, width, &t, ws, c, s, nullptr, 0, nullptr, z);
+  if (st != WT_OK) return st;
+  if (d_status) {
+    cudaError_t e = cudaMemcpyAsync(d_status, ws + c.off_flag, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return fail_cuda(e, "status copy");
+  }
+  return WT_OK;
+}
+
+wt_status wt_matrix_access(const wt_matrix_t* mx, uint64_t n, uint64_t sigma, const uint64_t* d_pos, uint64_t m,
+                           uint32_t* d_sym, int32_t* d_status, wt_stream_t stream) {
+  g_last_error.clear();
+  if (!mx || sigma == 0 || levels_of(sigma) > 30) return fail(WT_ERR_ARG, "bad matrix / sigma");
+  if (m == 0) return WT_OK;
+  if (!d_pos || !d_sym) return fail(WT_ERR_ARG, "NULL query pointer");
+  wt_tree_t t{mx->bitmaps, mx->superblocks, nullptr};
+  wt::TreeView v = view_of(&t, n, sigma);
+  wt::k_matrix_access<<<(uint32_t)((m + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      v, reinterpret_cast<const unsigned long long*>(mx->zeros), d_pos, m, d_sym, d_status);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_matrix_access");
+}
+
+wt_status wt_matrix_rank(const wt_matrix_t* mx, uint64_t n, uint64_t sigma, const uint32_t* d_c,
+                         const uint64_t* d_pos, uint64_t m, uint64_t* d_cnt, int32_t* d_status, wt_stream_t stream) {
+  g_last_error.clear();
+  if (!mx || sigma == 0 || levels_of(sigma) > 30) return fail(WT_ERR_ARG, "bad matrix / sigma");
+  if (m == 0) return WT_OK;
+  if (!d_c || !d_pos || !d_cnt) return fail(WT_ERR_ARG, "NULL query pointer");
+  wt_tree_t t{mx->bitmaps, mx->superblocks, nullptr};
+  wt::TreeView v = view_of(&t, n, sigma);
+  wt::k_matrix_rank<<<(uint32_t)((m + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      v, reinterpret_cast<const unsigned long long*>(mx->zeros), sigma, d_c, d_pos, m,
+      reinterpret_cast<unsigned long long*>(d_cnt), d_status);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_matrix_rank");
 }
 
 wt_status wt_build(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* out,

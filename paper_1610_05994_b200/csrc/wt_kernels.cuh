@@ -109,6 +109,40 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_prep(OpA a, uint64_t na, Lookb
   pdl_trigger();  // at the tail: the next pass's CTAs launch as this grid drains
 }
 
+// Wavelet matrix (NEXT-4): a level is one global node.  The level's zeros
+// Z_l = n - (ones of the level) come out of a scan of its per-tile ones: the
+// last element writes tab[0] = {0 ones before the node, Z_l} and zeros[0] = Z_l.
+struct OpMatrixTab {
+  const uint32_t* agg;
+  uint2* tab;
+  unsigned long long* zeros;
+  uint64_t n, count;
+  __device__ uint64_t load(uint64_t i) const { return agg[i]; }
+  __device__ void store(uint64_t i, uint64_t excl, uint64_t val) const {
+    if (i + 1 == count) {
+      const uint64_t z = n - (excl + val);
+      tab[0] = make_uint2(0u, (uint32_t)z);
+      zeros[0] = z;
+    }
+  }
+};
+// the last level's superblocks (as OpBlockPop) and its zeros
+struct OpBlockPopZ {
+  const uint32_t* cnt;
+  unsigned long long* sb;
+  uint64_t nblocks;
+  unsigned long long* zeros;
+  uint64_t n;
+  __device__ uint64_t load(uint64_t i) const { return cnt[i]; }
+  __device__ void store(uint64_t i, uint64_t excl, uint64_t val) const {
+    sb[i] = excl;
+    if (i + 1 == nblocks) {
+      sb[nblocks] = excl + val;
+      zeros[0] = n - (excl + val);
+    }
+  }
+};
+
 // a scan job that does nothing (count 0)
 struct OpNone {
   __device__ uint64_t load(uint64_t) const { return 0; }
@@ -296,6 +330,56 @@ __global__ void k_rank(TreeView t, uint64_t sigma, const uint32_t* __restrict__ 
     lo = t.C[(c >> (t.L - 1 - l)) << (t.L - 1 - l)];
   }
   cnt[k] = r;
+}
+
+// Wavelet matrix queries (NEXT-4).  Level l partitions the whole sequence by
+// bit (L-1-l), zeros first, stably (no nodes); zeros[l] = Z_l.
+//   access(i): b = B_l[i]; i = b ? Z_l + rank1_l(i) : i - rank1_l(i)
+//   rank(c, i) (inclusive): the prefix [0, i] of S maps to [s, e) per level
+__global__ void k_matrix_access(TreeView t, const unsigned long long* __restrict__ zeros,
+                                const uint64_t* __restrict__ pos, uint64_t m, uint32_t* __restrict__ sym,
+                                int32_t* status) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  uint64_t i = pos[k];
+  if (i >= t.n) {
+    sym[k] = 0xffffffffu;
+    if (status) *status = 3;
+    return;
+  }
+  uint32_t v = 0;
+  for (uint32_t l = 0; l < t.L; ++l) {
+    const uint32_t* B = t.bitmaps + l * t.W;
+    const unsigned long long* SB = t.sb + l * t.NSB;
+    const uint32_t b = (B[i >> 5] >> (i & 31)) & 1u;
+    const uint64_t r1 = rank1(B, SB, i);
+    i = b ? zeros[l] + r1 : i - r1;
+    v = 2 * v + b;
+  }
+  sym[k] = v;
+}
+
+__global__ void k_matrix_rank(TreeView t, const unsigned long long* __restrict__ zeros, uint64_t sigma,
+                              const uint32_t* __restrict__ cs, const uint64_t* __restrict__ pos, uint64_t m,
+                              unsigned long long* __restrict__ cnt, int32_t* status) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const uint64_t i = pos[k], c = cs[k];
+  if (i >= t.n || c >= sigma) {
+    cnt[k] = ~0ull;
+    if (status) *status = 3;
+    return;
+  }
+  uint64_t s = 0, e = i + 1;  // the symbols equal to c's top bits so far lie in [s, e) of T_l
+  for (uint32_t l = 0; l < t.L; ++l) {
+    const uint32_t* B = t.bitmaps + l * t.W;
+    const unsigned long long* SB = t.sb + l * t.NSB;
+    const uint32_t b = (uint32_t)(c >> (t.L - 1 - l)) & 1u;
+    const uint64_t rs = rank1(B, SB, s), re = rank1(B, SB, e);
+    if (b) s = zeros[l] + rs, e = zeros[l] + re;
+    else s = s - rs, e = e - re;
+  }
+  cnt[k] = e - s;
 }
 
 // Select index (NEXT-1; createRankSelect's select half):

@@ -47,6 +47,7 @@ namespace wt {
 constexpr int LV_NREG = 5;  // regions: identity, first zeros/ones, last zeros/ones
 constexpr int LV_NKEY = 2 * LV_NREG;
 constexpr int LV_THREADS = 32;  // one warp per CTA
+constexpr uint32_t LV_MATRIX = 0x100;  // k_level `shf` flag: wavelet-matrix level (global partition)
 
 template <typename T>
 struct LvTile {
@@ -98,7 +99,7 @@ constexpr size_t level_smem_bytes() {
 // (words shared with other tiles are OR-ed); no next-level tile counts.
 template <typename T, int MODE>
 __global__ void __launch_bounds__(32, LvTile<T>::MINB)
-    k_level(const T* __restrict__ in, T* __restrict__ out, uint32_t n32, uint32_t ntiles, uint32_t sh,
+    k_level(const T* __restrict__ in, T* __restrict__ out, uint32_t n32, uint32_t ntiles, uint32_t shf,
             const uint2* __restrict__ tab, uint32_t* __restrict__ bits, uint32_t words_per_level,
             unsigned long long* __restrict__ sb, uint32_t nsb, const uint32_t* __restrict__ pre,
             uint32_t* __restrict__ agg_next, uint32_t* __restrict__ cnt_next, const int32_t* __restrict__ flag) {
@@ -113,7 +114,11 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
   // n < 2^32 (wt_sizes rejects larger n): every position, rank and node
   // offset of the pass fits 32 bits; only pointers are 64-bit.
   const uint32_t lane = threadIdx.x;
-  const uint32_t nsh = sh + 1;   // node id = symbol >> nsh
+  // shf = the level's bit sh, | LV_MATRIX for the wavelet matrix (NEXT-4,
+  // P:1409-1413): one global node per level (symbols < 2^30, so s >> 31 = 0)
+  // and tab[0] = {0, zeros of the level}; every tile is then a one-segment tile
+  const uint32_t sh = shf & 0xffu;
+  const uint32_t nsh = (shf & LV_MATRIX) ? 31u : sh + 1;  // node id = symbol >> nsh
   const uint32_t i0 = lane * E;  // first tile position of this lane (phase A)
 
   auto tile_of = [&](uint32_t it) -> uint32_t { return blockIdx.x + it * gridDim.x; };

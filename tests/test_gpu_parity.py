@@ -330,3 +330,32 @@ def test_config_parity(wt, cfg):
     idx = rng.integers(0, S.size, 200_000)
     got = tree.access(torch.from_numpy(idx).cuda()).cpu().numpy()
     assert np.array_equal(got, S[idx].astype(np.int64))
+
+
+# ------------------------------------------------------------ wavelet matrix (NEXT-4)
+
+
+@pytest.mark.parametrize("sigma,n,dtype", [(2, 1, None), (4, 70001, None), (256, 4097, None), (256, 300_001, None),
+                                           (230, 100_000, None), (1 << 16, 200_003, np.uint16),
+                                           (1 << 20, 99_991, np.uint32), (5, 0, None)])
+def test_matrix_parity_and_queries(wt, sigma, n, dtype):
+    for kind in ("uniform", "zipf", "runs"):
+        S = wt_inputs.random_case(n + sigma, n, sigma, kind, dtype=dtype)
+        mx = wt.build_matrix(to_dev(S), sigma)
+        om = oracle.build_matrix(S, sigma)
+        B = mx.bitmaps.cpu().numpy().view(np.uint32)
+        assert np.array_equal(B, om.bitmaps), f"matrix bitmaps {kind}"
+        assert np.array_equal(mx.superblocks.cpu().numpy().view(np.uint64), om.superblocks), f"matrix sb {kind}"
+        assert np.array_equal(mx.zeros.cpu().numpy().view(np.uint64), om.zeros), f"matrix zeros {kind}"
+        if n == 0:
+            continue
+        got = wt.matrix_access(mx, torch.arange(n, device="cuda")).cpu().numpy()
+        assert np.array_equal(got, S.astype(np.int64))
+        rng = np.random.default_rng(n)
+        m = 2000
+        c = S[rng.integers(0, n, m)].astype(np.int64)
+        i = rng.integers(0, n, m)
+        cnt = wt.matrix_rank(mx, torch.from_numpy(c.astype(np.int32)).cuda(), torch.from_numpy(i).cuda()).cpu().numpy()
+        for k in range(0, m, 97):
+            assert cnt[k] == int((S[: i[k] + 1] == c[k]).sum())
+

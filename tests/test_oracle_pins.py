@@ -260,3 +260,26 @@ def test_errors():
         t.rank(3, 0)
     with pytest.raises(oracle.OracleError):
         t.select(0, 2)
+
+
+@pytest.mark.parametrize("sigma", [2, 3, 16, 230, 1 << 12])
+def test_matrix_oracle_vs_reversed_prefix_sort(sigma):
+    # the wavelet matrix (NEXT-4) pinned to an independent characterisation:
+    # T_l = S stably sorted by its top l bits READ IN REVERSE (the global stable
+    # partitions by bit 0, then bit 1, ... compose to that order); B_l = bit
+    # (L-1-l) of T_l; zeros[l] = #{s : bit (L-1-l) of s = 0} in any order
+    for kind in ("uniform", "zipf", "runs", "sorted"):
+        S = wt_inputs.random_case(sigma + 7, 3001, sigma, kind)
+        om = oracle.build_matrix(S, sigma)
+        L = om.L
+        s64 = S.astype(np.int64)
+        for l in range(L):
+            top = s64 >> (L - l) if l else np.zeros_like(s64)
+            rev = np.zeros_like(top)
+            for k in range(l):                    # reverse the l-bit prefix
+                rev |= ((top >> k) & 1) << (l - 1 - k)
+            T = s64[np.argsort(rev, kind="stable")]
+            bits = ((T >> (L - 1 - l)) & 1).astype(np.uint8)
+            assert np.array_equal(om.bitmaps[l], brute.pack_bits(bits, om.bitmaps.shape[1]))
+            assert int(om.zeros[l]) == int(((s64 >> (L - 1 - l)) & 1 == 0).sum())
+            assert int(om.superblocks[l, -1]) == int(bits.sum())
