@@ -335,6 +335,24 @@ def test_config_parity(wt, cfg):
 # ------------------------------------------------------------ wavelet matrix (NEXT-4)
 
 
+def test_degenerate_host_and_matrix_builds(wt):
+    # n = 0 through the asynchronous host path; sigma = 1 (no levels) for the matrix
+    # and the select index
+    dev = torch.device("cuda", 0)
+    st = torch.full((1,), -1, dtype=torch.int32).pin_memory()
+    ht = wt.alloc_host_tree(0, 16, 1)
+    ws = wt.alloc_workspace(0, 16, 1, dev, host=True)
+    wt.build_from_host_async(torch.zeros(0, dtype=torch.uint8), 16, ht, ws, st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == wt.WT_OK and int(ht.node_offsets.abs().sum()) == 0
+    S = np.zeros(100, np.uint8)
+    mx = wt.build_matrix(to_dev(S), 1)
+    assert mx.levels == 0 and mx.zeros.numel() == 0
+    assert np.array_equal(wt.matrix_access(mx, torch.arange(100, device="cuda")).cpu().numpy(), np.zeros(100))
+    tree = check_case(wt, S, 1)
+    assert wt.select_index(tree).numel() == 0
+
+
 @pytest.mark.parametrize("sigma,n,dtype", [(2, 1, None), (4, 70001, None), (256, 4097, None), (256, 300_001, None),
                                            (230, 100_000, None), (1 << 16, 200_003, np.uint16),
                                            (1 << 20, 99_991, np.uint32), (5, 0, None)])
