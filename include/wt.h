@@ -235,6 +235,24 @@ wt_status wt_matrix_rank(const wt_matrix_t* mx, uint64_t n, uint64_t sigma, cons
                          const uint64_t* d_pos, uint64_t m, uint64_t* d_cnt, int32_t* d_status,
                          wt_stream_t stream);
 
+/*
+ * Alphabet remap (NEXT-4, the effective alphabet of P:467-470): replaces every
+ * symbol of d_seq (n symbols of `width` bytes, all < sigma) by its rank among
+ * the distinct values present, so a sequence over a sparse alphabet builds a
+ * tree of ceil(lg sigma') levels, sigma' = number of distinct values.
+ *   d_out[j] = #{distinct values < d_seq[j]}   (same width; may alias d_seq)
+ *   d_alphabet[r] = the r-th smallest distinct value, r < sigma' (capacity sigma)
+ *   *d_sigma_out = sigma' (uint64, device)
+ * sigma <= 2^(8 width) (<= 2^32).  Device scratch: wt_remap_workspace_bytes(sigma)
+ * (a presence bitmap of sigma bits plus per-word ranks).  Asynchronous; *d_status
+ * (device, optional) becomes WT_ERR_SYMBOL_RANGE if a symbol is >= sigma.
+ * Errors: WT_ERR_ARG, WT_ERR_WORKSPACE, WT_ERR_CUDA.
+ */
+size_t wt_remap_workspace_bytes(uint64_t sigma);
+wt_status wt_remap_alphabet(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t width, void* d_out,
+                            uint32_t* d_alphabet, uint64_t* d_sigma_out, void* d_workspace,
+                            size_t workspace_bytes, int32_t* d_status, wt_stream_t stream);
+
 /* Kernel launches one wt_build_async(n, sigma, width) enqueues, and their kinds
  * (kinds may be NULL): 1 pass over S (prologue), 2 scan of node_offsets
  * (sigma = 1 only), 4 level pass with scatter (a3), 5 last level (a4, only

@@ -70,6 +70,9 @@ class WtMatrix(ctypes.Structure):
 _lib.wt_matrix_build_async.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(WtMatrix), _vp, _sz, _vp, _vp]
 _lib.wt_matrix_access.argtypes = [ctypes.POINTER(WtMatrix), _u64, _u64, _vp, _u64, _vp, _vp, _vp]
 _lib.wt_matrix_rank.argtypes = [ctypes.POINTER(WtMatrix), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
+_lib.wt_remap_workspace_bytes.argtypes = [_u64]
+_lib.wt_remap_workspace_bytes.restype = _sz
+_lib.wt_remap_alphabet.argtypes = [_vp, _u64, _u64, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _vp]
 _lib.wt_select_index_entries.argtypes = [_u64, _u64]
 _lib.wt_select_index_entries.restype = _u64
 _lib.wt_select_index.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp]
@@ -86,12 +89,14 @@ _lib.wt_last_error.argtypes = []
 _lib.wt_last_error.restype = ctypes.c_char_p
 for _f in (_lib.wt_sizes, _lib.wt_build_async, _lib.wt_build, _lib.wt_build_from_host,
            _lib.wt_build_from_host_async, _lib.wt_access, _lib.wt_rank, _lib.wt_select, _lib.wt_select_index,
-           _lib.wt_select_indexed, _lib.wt_matrix_build_async, _lib.wt_matrix_access, _lib.wt_matrix_rank):
+           _lib.wt_select_indexed, _lib.wt_matrix_build_async, _lib.wt_matrix_access, _lib.wt_matrix_rank,
+           _lib.wt_remap_alphabet):
     _f.restype = ctypes.c_int
 
 EXPORTS = ["wt_sizes", "wt_build_async", "wt_build", "wt_build_from_host", "wt_build_from_host_async",
            "wt_access", "wt_rank", "wt_select_index_entries", "wt_select_index", "wt_select_indexed",
-           "wt_matrix_build_async", "wt_matrix_access", "wt_matrix_rank",
+           "wt_matrix_build_async", "wt_matrix_access", "wt_matrix_rank", "wt_remap_workspace_bytes",
+           "wt_remap_alphabet",
            "wt_select", "wt_launch_plan", "wt_debug_offsets", "wt_set_profile_events", "wt_status_string",
            "wt_last_error"]
 
@@ -448,3 +453,28 @@ def matrix_rank(mx: WaveletMatrix, c: torch.Tensor, pos: torch.Tensor, stream=No
                              _stream_ptr(stream))
     _check(st, "wt_matrix_rank")
     return out
+
+
+def remap_alphabet(seq: torch.Tensor, sigma: int, stream=None):
+    """wt_remap_alphabet: (remapped sequence, sorted alphabet, sigma') for a CUDA tensor
+    of symbols < sigma; every symbol becomes its rank among the distinct values present."""
+    if not seq.is_cuda:
+        raise ValueError("seq must be a CUDA tensor")
+    seq = seq.contiguous()
+    w = width_of(seq)
+    n = seq.numel()
+    dev = seq.device
+    out = torch.empty_like(seq)
+    alphabet = torch.empty((max(sigma, 1),), dtype=torch.int32, device=dev)
+    sig = torch.zeros(1, dtype=torch.int64, device=dev)
+    status = _status_tensor(dev)
+    ws = torch.empty((max(int(_lib.wt_remap_workspace_bytes(sigma)), 256),), dtype=torch.uint8, device=dev)
+    st = _lib.wt_remap_alphabet(seq.data_ptr() if n else None, n, sigma, w, out.data_ptr() if n else None,
+                                alphabet.data_ptr(), sig.data_ptr(), ws.data_ptr(), ws.numel(), status.data_ptr(),
+                                _stream_ptr(stream))
+    _check(st, "wt_remap_alphabet")
+    if int(status.item()) != WT_OK:
+        raise WtError(int(status.item()), "wt_remap_alphabet: a symbol is >= sigma")
+    s2 = int(sig.item())
+    return out, alphabet[:s2], s2
+

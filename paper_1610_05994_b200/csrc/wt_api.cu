@@ -688,6 +688,90 @@ wt_status wt_select(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uin
   return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_select");
 }
 
+// ---------------------------------------------------------------- alphabet remap (NEXT-4)
+namespace {
+struct RemapCarve {
+  uint64_t words = 0, tiles = 0;
+  size_t off_flag = 0, off_counter = 0, off_total = 0, off_status = 0, ctrl = 0, off_value = 0, off_present = 0,
+         off_rank = 0, total = 0;
+};
+RemapCarve remap_carve(uint64_t sigma) {
+  RemapCarve r;
+  r.words = (sigma + 31) / 32;
+  r.tiles = std::max<uint64_t>(1, (r.words + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+  size_t o = 0;
+  r.off_flag = o;
+  o += ALIGN;
+  r.off_counter = o;
+  o += ALIGN;
+  r.off_total = o;
+  o += ALIGN;
+  r.off_status = o;
+  o += align_up(r.tiles * sizeof(uint32_t));
+  r.off_present = o;  // zeroed with the control block
+  o += align_up(r.words * sizeof(uint32_t));
+  r.ctrl = o;
+  r.off_value = o;
+  o += align_up(2 * r.tiles * sizeof(uint64_t));
+  r.off_rank = o;
+  o += align_up(r.words * sizeof(uint32_t));
+  r.total = o;
+  return r;
+}
+}  // namespace
+
+size_t wt_remap_workspace_bytes(uint64_t sigma) { return (sigma == 0 || sigma > (1ull << 32)) ? 0 : remap_carve(sigma).total; }
+
+wt_status wt_remap_alphabet(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t width, void* d_out,
+                            uint32_t* d_alphabet, uint64_t* d_sigma_out, void* d_workspace, size_t workspace_bytes,
+                            int32_t* d_status, wt_stream_t stream) {
+  g_last_error.clear();
+  if (width != 1 && width != 2 && width != 4) return fail(WT_ERR_ARG, "width must be 1, 2 or 4");
+  if (sigma == 0 || sigma > (1ull << (8 * width))) return fail(WT_ERR_ARG, "sigma out of range for the width");
+  if (n >= (1ull << 32)) return fail(WT_ERR_ARG, "n must be < 2^32");
+  if ((n > 0 && (!d_seq || !d_out)) || !d_alphabet || !d_sigma_out) return fail(WT_ERR_ARG, "NULL pointer");
+  const RemapCarve r = remap_carve(sigma);
+  if (!d_workspace || workspace_bytes < r.total) return fail(WT_ERR_WORKSPACE, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(d_workspace) & (ALIGN - 1))
+    return fail(WT_ERR_ARG, "workspace must be 256-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(d_workspace);
+  int32_t* flag = reinterpret_cast<int32_t*>(ws + r.off_flag);
+  uint32_t* present = reinterpret_cast<uint32_t*>(ws + r.off_present);
+  uint32_t* rank = reinterpret_cast<uint32_t*>(ws + r.off_rank);
+  unsigned long long* total = reinterpret_cast<unsigned long long*>(ws + r.off_total);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(ws, 0, r.ctrl, s)) != cudaSuccess) return fail_cuda(e, "memset remap control");
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 8ull * num_sms()));
+  auto launch_w = [&](auto tag) -> cudaError_t {
+    using T = decltype(tag);
+    wt::k_remap_mark<T><<<g, 256, 0, s>>>(static_cast<const T*>(d_seq), n, sigma, present, flag);
+    return cudaGetLastError();
+  };
+  e = width == 1 ? launch_w(uint8_t{}) : width == 2 ? launch_w(uint16_t{}) : launch_w(uint32_t{});
+  if (e != cudaSuccess) return fail_cuda(e, "k_remap_mark");
+  const wt::LookbackState lb{reinterpret_cast<uint32_t*>(ws + r.off_status), reinterpret_cast<uint64_t*>(ws + r.off_value),
+                             r.tiles};
+  wt::k_scan<wt::OpPopPrefix><<<(uint32_t)r.tiles, wt::SCAN_THREADS, 0, s>>>(
+      wt::OpPopPrefix{present, rank, r.words, total}, r.words, lb, reinterpret_cast<uint32_t*>(ws + r.off_counter), 1u,
+      flag);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(remap)");
+  auto apply_w = [&](auto tag) -> cudaError_t {
+    using T = decltype(tag);
+    if (n) wt::k_remap_apply<T><<<g, 256, 0, s>>>(static_cast<const T*>(d_seq), n, present, rank, static_cast<T*>(d_out), flag);
+    return cudaGetLastError();
+  };
+  e = width == 1 ? apply_w(uint8_t{}) : width == 2 ? apply_w(uint16_t{}) : apply_w(uint32_t{});
+  if (e != cudaSuccess) return fail_cuda(e, "k_remap_apply");
+  wt::k_remap_alphabet<<<(uint32_t)((r.words + 255) / 256), 256, 0, s>>>(present, rank, r.words, d_alphabet);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_remap_alphabet");
+  if ((e = cudaMemcpyAsync(d_sigma_out, total, 8, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+    return fail_cuda(e, "sigma copy");
+  if (d_status && (e = cudaMemcpyAsync(d_status, flag, 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+    return fail_cuda(e, "status copy");
+  return WT_OK;
+}
+
 uint64_t wt_select_index_entries(uint64_t n, uint64_t sigma) {
   if (sigma == 0 || levels_of(sigma) > 30) return 0;
   return 2ull * levels_of(sigma) * wt::select_samples_per_level(n);

@@ -143,6 +143,59 @@ struct OpBlockPopZ {
   }
 };
 
+// ---------------------------------------------------------------- alphabet remap (NEXT-4)
+// The symbols that occur, ranked: map(s) = #{present values < s} (P:467-470's
+// effective alphabet; the tree over the remapped sequence has ceil(lg sigma')
+// levels for sigma' distinct values).  A presence bitmap over [0, sigma), a
+// scan of its word popcounts, then every symbol is replaced by its rank.
+template <typename T>
+__global__ void k_remap_mark(const T* __restrict__ seq, uint64_t n, uint64_t sigma, uint32_t* __restrict__ present,
+                             int32_t* __restrict__ flag) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = (uint64_t)seq[j];
+    if (s >= sigma) {
+      *flag = 2;  // WT_ERR_SYMBOL_RANGE
+      continue;
+    }
+    const uint32_t bit = 1u << (s & 31);
+    uint32_t* w = present + (s >> 5);
+    if (!(__ldg(w) & bit)) atomicOr(w, bit);  // (the read skips the atomic for repeats)
+  }
+}
+struct OpPopPrefix {  // rank of the first value of word w = set bits of the words before w
+  const uint32_t* present;
+  uint32_t* rank;
+  uint64_t words;
+  unsigned long long* total;
+  __device__ uint64_t load(uint64_t w) const { return (uint64_t)__popc(present[w]); }
+  __device__ void store(uint64_t w, uint64_t excl, uint64_t val) const {
+    rank[w] = (uint32_t)excl;
+    if (w + 1 == words) *total = excl + val;
+  }
+};
+template <typename T>
+__global__ void k_remap_apply(const T* __restrict__ seq, uint64_t n, const uint32_t* __restrict__ present,
+                              const uint32_t* __restrict__ rank, T* __restrict__ out, const int32_t* __restrict__ flag) {
+  if (*flag) return;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = (uint64_t)seq[j];
+    const uint64_t w = s >> 5;
+    out[j] = (T)(rank[w] + (uint32_t)__popc(present[w] & ((1u << (s & 31)) - 1u)));
+  }
+}
+// alphabet[rank] = value: one thread per presence word
+__global__ void k_remap_alphabet(const uint32_t* __restrict__ present, const uint32_t* __restrict__ rank,
+                                 uint64_t words, uint32_t* __restrict__ alphabet) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= words) return;
+  uint32_t x = present[w], r = rank[w];
+  while (x) {
+    const uint32_t b = (uint32_t)(__ffs(x) - 1);
+    x &= x - 1;
+    alphabet[r++] = (uint32_t)(32 * w + b);
+  }
+}
+
 // a scan job that does nothing (count 0)
 struct OpNone {
   __device__ uint64_t load(uint64_t) const { return 0; }

@@ -377,3 +377,28 @@ def test_matrix_parity_and_queries(wt, sigma, n, dtype):
         for k in range(0, m, 97):
             assert cnt[k] == int((S[: i[k] + 1] == c[k]).sum())
 
+
+@pytest.mark.parametrize("sigma,n,dtype,kind", [(1 << 20, 200_003, np.uint32, "zipf"), (1 << 16, 50_000, np.uint16, "runs"),
+                                                (256, 4097, None, "uniform"), (1 << 32, 100_000, np.uint32, "sparse"),
+                                                (7, 1, None, "uniform"), (1000, 0, np.uint16, "uniform")])
+def test_alphabet_remap(wt, sigma, n, dtype, kind):
+    # NEXT-4's alphabet remap against its definition (np.unique); then the tree of the
+    # remapped sequence has ceil(lg sigma') levels and matches the oracle
+    if kind == "sparse":   # a few thousand distinct values spread over [0, 2^32)
+        rng = np.random.default_rng(5)
+        vals = np.unique(rng.integers(0, 1 << 32, 3000, dtype=np.uint64)).astype(np.uint32)
+        S = vals[rng.integers(0, vals.size, n)]
+    else:
+        S = wt_inputs.random_case(n + 3, n, min(sigma, 1 << 24), kind, dtype=dtype)
+    d = to_dev(S)
+    out, alphabet, s2 = wt.remap_alphabet(d, sigma)
+    uniq, inv = np.unique(S, return_inverse=True)
+    assert s2 == uniq.size
+    assert np.array_equal(alphabet.cpu().numpy().view(np.uint32), uniq.astype(np.uint32))
+    got = out.cpu().numpy()
+    got = got.view(np.uint32) if got.dtype == np.int32 else got
+    assert np.array_equal(got.astype(np.int64), inv.astype(np.int64))
+    if n and s2 > 0:
+        R = got.astype(S.dtype)
+        check_case(wt, R, max(s2, 1), f"remapped sigma'={s2}")
+
