@@ -673,9 +673,11 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
           if (slot < (uint32_t)(4 * A) && (e < (uint32_t)A ? q < hend : q < end)) out[DD - bb + q] = S.buf[ob][q];
         }
       }
-      if (lane < 4) {  // next-level ones per destination tile
-        const uint32_t v = lane == 0 ? Lz : lane == 1 ? c01 - Lz : lane == 2 ? Lo : c11 - Lo;
-        if (v) atomicAdd(&agg_next[(lane < 2 ? D0z : D0o) / TILE + (lane & 1)], v);
+      {  // next-level ones per destination tile: lanes 0..3, one predicated reduction (no branch)
+        const uint32_t cx = (lane & 2u) ? c11 : c01, lx = (lane & 2u) ? Lo : Lz;
+        const uint32_t v = lane < 4 ? ((lane & 1u) ? cx - lx : lx) : 0u;
+        const uint32_t dt = ((lane & 2u) ? D0o : D0z) / TILE + (lane & 1u);
+        if (v) atomicAdd(&agg_next[dt], v);
       }
       }  // !BITS
     } else {
