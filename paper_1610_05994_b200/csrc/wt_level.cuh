@@ -10,34 +10,43 @@
 //   b = 0: dest = j - r(j) + ob[v]            b = 1: dest = r(j) + Zn[v]
 //
 // Execution model (B200-first, not the paper's thread-per-level): barrier-free
-// WARP TILES.  Every CTA is one warp, a persistent worker; ~24 of them per SM
+// WARP TILES.  Every CTA is one warp, a persistent worker; 20 of them per SM
 // run independently (no block barriers to wait on, only __syncwarp).  A warp
 // tile is 2 KiB of symbols (2048 / 1024 / 512 for 1 / 2 / 4-byte symbols, a
 // multiple of 512 positions: every bitmap word and superblock belongs to one
-// tile); tiles go round-robin over the warps.  Per warp a ring of NB buffers:
-// tile `it` is TMA-bulk-loaded (cp.async.bulk + mbarrier) into buf[it % NB]
-// and its partitioned output is staged in buf[(it-1) % NB], the previous
+// tile); tiles go round-robin over the warps.  Per warp a ring of 4 buffers:
+// tile `it` is TMA-bulk-loaded (cp.async.bulk + mbarrier) into buf[it % 4]
+// and its partitioned output is staged in buf[(it-1) % 4], the previous
 // tile's input buffer.
 //   * NO look-back: the ones of level l in every tile (agg_l[t]) were counted
-//     by the pass that wrote T_l (the histogram pass for l = 0) and a tiny
-//     scan turned them into pre_l[t], so the tiles of a pass are independent;
-//   * phase A (lane owns 64 consecutive bytes): SWAR bit extraction, bitmap
-//     words, warp scan of popcounts -> tile-local rank R(q), superblocks;
-//   * nodes are sorted along T_l, so a tile is: a first segment (node vF,
-//     may start before the tile), interior nodes (wholly inside the tile, so
-//     by node locality their destinations are exactly their own positions:
-//     an identity region), and a last segment (node vL, may run past the
-//     tile).  The first and last segments' zeros/ones runs are staged in four
-//     side regions, each at an offset congruent to its HBM destination
-//     modulo 16 bytes;
-//   * phase D (lane handles 16 words, word w = lane + 32 k: lanes touch
-//     consecutive 32-bit words, so the byte stores are bank-conflict free)
-//     writes every symbol to its stage position, a PRMT partitioning each
-//     word's symbols (zeros first) so they go out with immediate offsets;
-//   * phase E: lane r issues a TMA bulk store (cp.async.bulk shared->global)
-//     of region r's 16-byte-aligned body; lanes store the <= 10 partial edge
-//     chunks; the next level's ones per destination tile (agg_{l+1}) were
-//     counted from the lanes' masks and go out as <= 9 global atomics.
+//     by the pass that wrote T_l (the prologue for l = 0) and a tiny scan
+//     (k_prep) turned them into pre_l[t], so the tiles of a pass are independent;
+//   * phase A (lane owns 64 consecutive bytes, read in a lane-rotated chunk
+//     order against bank conflicts): SWAR bit extraction, bitmap words, warp
+//     scan of popcounts -> tile-local rank R(q), superblocks;
+//   * ONE-SEGMENT tiles (the whole tile in one node: the common case) take a
+//     dedicated path: the zeros go to one run, the ones to another, each
+//     staged congruent mod 16 bytes to its HBM destination; the split of each
+//     run at its destination tile boundary (for agg_{l+1}) is counted from the
+//     staged symbols around the boundary;
+//   * MULTI-SEGMENT tiles: a first segment (node vF, may start before the
+//     tile), interior nodes (wholly inside the tile: by node locality their
+//     destinations are their own positions, an identity region), a last
+//     segment (node vL); the first and last segments' runs go to four side
+//     regions; a per-tile segment table in shared memory gives each word its
+//     stage addresses (global node tables beyond MAXSEG segments);
+//   * phase D (word w = lane + 32 k: lanes touch consecutive 32-bit words, so
+//     the byte stores are bank-conflict free) writes every symbol to its stage
+//     position: u8 words are partitioned by a PRMT from a 16-entry selector
+//     table, u16 words store each symbol straight to its slot;
+//   * phase E: TMA bulk stores (cp.async.bulk shared->global) of each region's
+//     16-byte-aligned body, lane-parallel stores of the edge symbols, and the
+//     next level's ones per destination tile as a few global atomics;
+//   * MODE 2 (pass L-2 fused with level L-1) writes B_{L-1} instead of T_{L-1}:
+//     one-segment tiles compact the last-level bits per lane (no symbol moves);
+//     multi-segment tiles take them from the byte stage;
+//   * LV_MATRIX (wavelet matrix): one global node per level, every tile is a
+//     one-segment tile.
 #pragma once
 #include "wt_ptx.cuh"
 
