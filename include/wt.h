@@ -253,6 +253,22 @@ wt_status wt_remap_alphabet(const void* d_seq, uint64_t n, uint64_t sigma, uint3
                             uint32_t* d_alphabet, uint64_t* d_sigma_out, void* d_workspace,
                             size_t workspace_bytes, int32_t* d_status, wt_stream_t stream);
 
+/*
+ * Domain-decomposition merge (NEXT-3 on one GPU; the paper's dd, P:633-687,
+ * 773-822): the trees of k <= 8 contiguous segments of S (built with
+ * wt_build_async over the same sigma; segs[g] device pointers, seg_n[g]
+ * their lengths) are merged into the tree of the whole sequence: node v of
+ * every level holds segment 0's run of v, then segment 1's, ...; C is the sum
+ * of the segments' node offsets; superblocks are recomputed.  This is the
+ * merge step a multi-GPU or out-of-core build needs (segments built where the
+ * data is, then concatenated).  d_scratch: wt_dd_merge_scratch_bytes(n) bytes
+ * of device memory, n = sum seg_n.  Asynchronous.
+ * Errors: WT_ERR_ARG (k = 0 or > 8, NULL pointers, n >= 2^32), WT_ERR_WORKSPACE.
+ */
+size_t wt_dd_merge_scratch_bytes(uint64_t n);
+wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, uint64_t sigma,
+                      const wt_tree_t* out, void* d_scratch, size_t scratch_bytes, wt_stream_t stream);
+
 /* Kernel launches one wt_build_async(n, sigma, width) enqueues, and their kinds
  * (kinds may be NULL): 1 pass over S (prologue), 2 scan of node_offsets
  * (sigma = 1 only), 4 level pass with scatter (a3), 5 last level (a4, only

@@ -70,6 +70,9 @@ class WtMatrix(ctypes.Structure):
 _lib.wt_matrix_build_async.argtypes = [_vp, _u64, _u64, _u32, ctypes.POINTER(WtMatrix), _vp, _sz, _vp, _vp]
 _lib.wt_matrix_access.argtypes = [ctypes.POINTER(WtMatrix), _u64, _u64, _vp, _u64, _vp, _vp, _vp]
 _lib.wt_matrix_rank.argtypes = [ctypes.POINTER(WtMatrix), _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp]
+_lib.wt_dd_merge_scratch_bytes.argtypes = [_u64]
+_lib.wt_dd_merge_scratch_bytes.restype = _sz
+_lib.wt_dd_merge.argtypes = [_u32, _vp, _vp, _u64, ctypes.POINTER(WtTree), _vp, _sz, _vp]
 _lib.wt_remap_workspace_bytes.argtypes = [_u64]
 _lib.wt_remap_workspace_bytes.restype = _sz
 _lib.wt_remap_alphabet.argtypes = [_vp, _u64, _u64, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _vp]
@@ -90,13 +93,13 @@ _lib.wt_last_error.restype = ctypes.c_char_p
 for _f in (_lib.wt_sizes, _lib.wt_build_async, _lib.wt_build, _lib.wt_build_from_host,
            _lib.wt_build_from_host_async, _lib.wt_access, _lib.wt_rank, _lib.wt_select, _lib.wt_select_index,
            _lib.wt_select_indexed, _lib.wt_matrix_build_async, _lib.wt_matrix_access, _lib.wt_matrix_rank,
-           _lib.wt_remap_alphabet):
+           _lib.wt_remap_alphabet, _lib.wt_dd_merge):
     _f.restype = ctypes.c_int
 
 EXPORTS = ["wt_sizes", "wt_build_async", "wt_build", "wt_build_from_host", "wt_build_from_host_async",
            "wt_access", "wt_rank", "wt_select_index_entries", "wt_select_index", "wt_select_indexed",
            "wt_matrix_build_async", "wt_matrix_access", "wt_matrix_rank", "wt_remap_workspace_bytes",
-           "wt_remap_alphabet",
+           "wt_remap_alphabet", "wt_dd_merge_scratch_bytes", "wt_dd_merge",
            "wt_select", "wt_launch_plan", "wt_debug_offsets", "wt_set_profile_events", "wt_status_string",
            "wt_last_error"]
 
@@ -477,4 +480,42 @@ def remap_alphabet(seq: torch.Tensor, sigma: int, stream=None):
         raise WtError(int(status.item()), "wt_remap_alphabet: a symbol is >= sigma")
     s2 = int(sig.item())
     return out, alphabet[:s2], s2
+
+
+# ---------------------------------------------------------------- domain decomposition (NEXT-3)
+
+
+def dd_merge(segments: list, sigma: int, stream=None) -> WaveletTree:
+    """wt_dd_merge: the tree of the concatenation of k <= 8 segment trees (each a
+    WaveletTree over the same sigma, on the same device)."""
+    k = len(segments)
+    if not 1 <= k <= 8:
+        raise ValueError("1..8 segments")
+    n = sum(t.n for t in segments)
+    dev = segments[0].node_offsets.device
+    w = 4  # (the tree layout does not depend on the symbol width; 4 admits every sigma)
+    out = alloc_tree(n, sigma, w, dev)
+    arr = (WtTree * k)(*[t._ctree() for t in segments])
+    ns = (ctypes.c_uint64 * k)(*[t.n for t in segments])
+    scratch = torch.empty((max(int(_lib.wt_dd_merge_scratch_bytes(n)), 256),), dtype=torch.uint8, device=dev)
+    ct = out._ctree()
+    st = _lib.wt_dd_merge(k, ctypes.cast(arr, _vp), ctypes.cast(ns, _vp), sigma, ctypes.byref(ct),
+                          scratch.data_ptr(), scratch.numel(), _stream_ptr(stream))
+    _check(st, "wt_dd_merge")
+    torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+    return out
+
+
+def build_dd(seq: torch.Tensor, sigma: int, k: int) -> WaveletTree:
+    """The paper's domain decomposition on one GPU: k contiguous segments built
+    separately (16-byte-aligned cut points), then merged."""
+    seq = seq.contiguous()
+    n = seq.numel()
+    w = width_of(seq)
+    step = -(-n // k) if n else 0
+    align = 16 // w
+    step = -(-step // align) * align if step else 0
+    cuts = [min(i * step, n) for i in range(k)] + [n]
+    segs = [build(seq[cuts[i]:cuts[i + 1]], sigma) for i in range(k)]
+    return dd_merge(segs, sigma)
 

@@ -772,6 +772,78 @@ wt_status wt_remap_alphabet(const void* d_seq, uint64_t n, uint64_t sigma, uint3
   return WT_OK;
 }
 
+// ---------------------------------------------------------------- domain decomposition merge (NEXT-3)
+size_t wt_dd_merge_scratch_bytes(uint64_t n) {
+  const uint64_t nsb = (n + 511) / 512 + 1, tiles = std::max<uint64_t>(1, (nsb + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+  return 3 * ALIGN + align_up(tiles * 4) + align_up(2 * tiles * 8) + align_up(nsb * 4);
+}
+
+wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, uint64_t sigma,
+                      const wt_tree_t* out, void* d_scratch, size_t scratch_bytes, wt_stream_t stream) {
+  g_last_error.clear();
+  if (k == 0 || k > (uint32_t)wt::DD_MAX_SEGMENTS || !segs || !seg_n || !out || !out->node_offsets)
+    return fail(WT_ERR_ARG, "bad segment list or output");
+  if (sigma == 0 || levels_of(sigma) > 30) return fail(WT_ERR_ARG, "bad sigma");
+  const uint32_t L = levels_of(sigma);
+  uint64_t n = 0;
+  wt::DdSegments sg{};
+  sg.k = k;
+  sg.L = L;
+  sg.wbase[0] = 0;
+  for (uint32_t g = 0; g < k; ++g) {
+    if (!segs[g].node_offsets || (L && seg_n[g] && !segs[g].bitmaps)) return fail(WT_ERR_ARG, "NULL segment tree");
+    sg.bits[g] = segs[g].bitmaps;
+    sg.C[g] = reinterpret_cast<const unsigned long long*>(segs[g].node_offsets);
+    sg.n[g] = seg_n[g];
+    sg.W[g] = 16 * ((seg_n[g] + 511) / 512);
+    sg.wbase[g + 1] = sg.wbase[g] + sg.W[g];
+    n += seg_n[g];
+  }
+  if (n >= (1ull << 32)) return fail(WT_ERR_ARG, "n must be < 2^32");
+  if (L && (!out->bitmaps || !out->superblocks)) return fail(WT_ERR_ARG, "NULL output");
+  if (!d_scratch || scratch_bytes < wt_dd_merge_scratch_bytes(n)) return fail(WT_ERR_WORKSPACE, "scratch too small");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  unsigned long long* C = reinterpret_cast<unsigned long long*>(out->node_offsets);
+  const uint64_t clen = (1ull << L) + 1;
+  cudaError_t e;
+  wt::k_dd_sum_offsets<<<(uint32_t)std::min<uint64_t>((clen + 255) / 256, 4ull * num_sms()), 256, 0, s>>>(sg, clen, C);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_dd_sum_offsets");
+  if (L == 0) return WT_OK;
+  const uint64_t W = 16 * ((n + 511) / 512), nsb = (n + 511) / 512 + 1;
+  if ((e = cudaMemsetAsync(out->bitmaps, 0, (size_t)L * W * 4, s)) != cudaSuccess) return fail_cuda(e, "memset bitmaps");
+  // scratch: flag, ticket counters (one per level), look-back status/values, block counts
+  char* sc = static_cast<char*>(d_scratch);
+  const uint64_t tiles = std::max<uint64_t>(1, (nsb + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+  int32_t* flag = reinterpret_cast<int32_t*>(sc);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(sc + ALIGN);  // (32 levels * 4 B fit in ALIGN * 2)
+  const size_t off_status = 3 * ALIGN, off_value = off_status + align_up(tiles * 4),
+               off_blk = off_value + align_up(2 * tiles * 8);
+  if ((e = cudaMemsetAsync(sc, 0, off_value, s)) != cudaSuccess) return fail_cuda(e, "memset scratch");
+  const wt::LookbackState lb{reinterpret_cast<uint32_t*>(sc + off_status), reinterpret_cast<uint64_t*>(sc + off_value),
+                             tiles};
+  uint32_t* blk = reinterpret_cast<uint32_t*>(sc + off_blk);
+  for (uint32_t l = 0; l < L; ++l) {
+    if (sg.wbase[k]) {
+      wt::k_dd_merge_level<<<(uint32_t)((sg.wbase[k] + 255) / 256), 256, 0, s>>>(sg, l, C, out->bitmaps + (uint64_t)l * W);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_dd_merge_level");
+    }
+    const uint32_t* lb_bits = out->bitmaps + (uint64_t)l * W;
+    unsigned long long* sbl = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * nsb;
+    if (nsb > 1) {
+      const uint64_t warps = (nsb - 1 + 31) / 32;
+      wt::k_block_pop<<<(uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, 16ull * num_sms())),
+                        wt::BP_THREADS, 0, s>>>(lb_bits, blk, nsb - 1, flag);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_block_pop");
+      wt::k_scan<wt::OpBlockPop><<<(uint32_t)tiles, wt::SCAN_THREADS, 0, s>>>(wt::OpBlockPop{blk, sbl, nsb - 1}, nsb - 1,
+                                                                          lb, counters + l, l + 1, flag);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(dd superblocks)");
+    } else if ((e = cudaMemsetAsync(sbl, 0, 8, s)) != cudaSuccess) {
+      return fail_cuda(e, "memset sb");
+    }
+  }
+  return WT_OK;
+}
+
 uint64_t wt_select_index_entries(uint64_t n, uint64_t sigma) {
   if (sigma == 0 || levels_of(sigma) > 30) return 0;
   return 2ull * levels_of(sigma) * wt::select_samples_per_level(n);

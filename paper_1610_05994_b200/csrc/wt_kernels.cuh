@@ -435,6 +435,80 @@ __global__ void k_matrix_rank(TreeView t, const unsigned long long* __restrict__
   cnt[k] = e - s;
 }
 
+// ---------------------------------------------------------------- domain decomposition merge (NEXT-3)
+// The paper's dd: S is split into k contiguous segments,
+// each built on its own (the partial trees), then every level's node runs are
+// concatenated: node v of level l in the merged tree holds segment 0's run of
+// node v, then segment 1's, ... (stability across segments).  With Cg the
+// segments' node offsets and C = sum_g Cg, segment g's run of node v goes to
+//   C[v << (L-l)] + sum_{g' < g} (Cg'[(v+1) << (L-l)] - Cg'[v << (L-l)]).
+// One thread per 32-bit word of a segment's level bitmap: it finds the node
+// of its first bit (binary search over the segment's level-l node starts),
+// then moves each node piece of its word with at most two atomicOr (the
+// merged bitmap is zeroed first; runs of different segments share words).
+constexpr int DD_MAX_SEGMENTS = 8;
+struct DdSegments {
+  const uint32_t* bits[DD_MAX_SEGMENTS];  // level-major bitmaps of each segment
+  const unsigned long long* C[DD_MAX_SEGMENTS];
+  uint64_t n[DD_MAX_SEGMENTS], W[DD_MAX_SEGMENTS];
+  uint64_t wbase[DD_MAX_SEGMENTS + 1];  // prefix of the segments' words per level (thread -> (g, word))
+  uint32_t k, L;
+};
+__global__ void k_dd_merge_level(DdSegments sg, uint32_t l, const unsigned long long* __restrict__ C,
+                                 uint32_t* __restrict__ out_bits) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= sg.wbase[sg.k]) return;
+  uint32_t g = 0;
+  while (t >= sg.wbase[g + 1]) ++g;
+  const uint64_t w = t - sg.wbase[g];
+  const uint64_t ng = sg.n[g];
+  const uint64_t p0 = 32 * w;
+  if (p0 >= ng) return;
+  const uint64_t pend = min(p0 + 32, ng);
+  const uint32_t word = sg.bits[g][(uint64_t)l * sg.W[g] + w];
+  const uint32_t sh = sg.L - l;  // node v of level l spans leaves [v << sh, (v + 1) << sh)
+  const unsigned long long* Cg = sg.C[g];
+  // node of position p0: largest v with Cg[v << sh] <= p0
+  uint64_t lo = 0, hi = 1ull << l;  // Cg[lo << sh] <= p0 < Cg[hi << sh] (= ng)
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (Cg[mid << sh] <= p0) lo = mid;
+    else hi = mid;
+  }
+  uint64_t v = lo, pos = p0;
+  while (pos < pend) {
+    if (Cg[(v + 1) << sh] <= pos) {  // past node v: the node holding pos (skipping empty nodes)
+      uint64_t a = v + 1, z = 1ull << l;  // Cg[a << sh] <= pos < Cg[z << sh]
+      while (z - a > 1) {
+        const uint64_t mid = (a + z) >> 1;
+        if (Cg[mid << sh] <= pos) a = mid;
+        else z = mid;
+      }
+      v = a;
+    }
+    const uint64_t vs = Cg[v << sh], ve = Cg[(v + 1) << sh];
+    const uint64_t e = min(pend, ve);
+    uint64_t dst = C[v << sh] + (pos - vs);
+    for (uint32_t h = 0; h < g; ++h) dst += sg.C[h][(v + 1) << sh] - sg.C[h][v << sh];
+    const uint32_t len = (uint32_t)(e - pos), off = (uint32_t)(pos - p0);
+    const uint32_t piece = (word >> off) & (len >= 32 ? 0xffffffffu : ((1u << len) - 1u));
+    if (piece) {
+      const uint32_t d = (uint32_t)(dst & 31);
+      atomicOr(&out_bits[dst >> 5], piece << d);
+      if (d && d + len > 32) atomicOr(&out_bits[(dst >> 5) + 1], piece >> (32 - d));
+    }
+    pos = e;
+  }
+}
+// C = sum over the segments' node offsets
+__global__ void k_dd_sum_offsets(DdSegments sg, uint64_t count, unsigned long long* __restrict__ C) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long s = 0;
+    for (uint32_t g = 0; g < sg.k; ++g) s += sg.C[g][i];
+    C[i] = s;
+  }
+}
+
 // Select index (NEXT-1; createRankSelect's select half):
 // per level and bit value b, the position of every 2^SEL_SHIFT-th bit equal to
 // b: samples[l][b][k] = position of the (k * 2^SEL_SHIFT)-th (0-based) such bit;

@@ -402,3 +402,25 @@ def test_alphabet_remap(wt, sigma, n, dtype, kind):
         R = got.astype(S.dtype)
         check_case(wt, R, max(s2, 1), f"remapped sigma'={s2}")
 
+
+# ------------------------------------------------------------ domain decomposition (NEXT-3)
+
+
+@pytest.mark.parametrize("sigma,n,k,dtype", [(16, 30, 3, None), (4, 1_000_003, 2, None), (256, 300_001, 5, None),
+                                             (1 << 16, 200_000, 8, np.uint16), (1 << 20, 150_001, 4, np.uint32),
+                                             (3, 5000, 7, None), (256, 100, 8, None)])
+def test_dd_merge_equals_direct_build(wt, sigma, n, k, dtype):
+    # the merged tree of k segment trees is the tree of the whole sequence
+    for kind in ("uniform", "zipf", "runs"):
+        S = wt_inputs.random_case(n * k + sigma, n, sigma, kind, dtype=dtype)
+        merged = wt.build_dd(to_dev(S), sigma, k)
+        assert_same(merged, oracle.build(S, sigma), f"dd k={k} {kind}")
+
+
+def test_dd_fig2_segments(wt):
+    # SURVEY Appendix A's dd split of the worked example: 3 segments of 10
+    S = np.array([0, 1, 2, 3, 4, 5, 6, 0, 1, 4, 7, 4, 8, 9, 10, 3, 4, 7, 4, 11, 12, 13, 4, 14, 8, 5, 15, 3, 1, 8],
+                 np.uint8)
+    merged = wt.dd_merge([wt.build(to_dev(S[i:i + 10]), 16) for i in (0, 10, 20)], 16)
+    assert_same(merged, oracle.build(S, 16), "fig2 dd")
+
