@@ -789,14 +789,12 @@ wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, 
   wt::DdSegments sg{};
   sg.k = k;
   sg.L = L;
-  sg.wbase[0] = 0;
   for (uint32_t g = 0; g < k; ++g) {
     if (!segs[g].node_offsets || (L && seg_n[g] && !segs[g].bitmaps)) return fail(WT_ERR_ARG, "NULL segment tree");
     sg.bits[g] = segs[g].bitmaps;
     sg.C[g] = reinterpret_cast<const unsigned long long*>(segs[g].node_offsets);
     sg.n[g] = seg_n[g];
     sg.W[g] = 16 * ((seg_n[g] + 511) / 512);
-    sg.wbase[g + 1] = sg.wbase[g] + sg.W[g];
     n += seg_n[g];
   }
   if (n >= (1ull << 32)) return fail(WT_ERR_ARG, "n must be < 2^32");
@@ -810,7 +808,6 @@ wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, 
   if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_dd_sum_offsets");
   if (L == 0) return WT_OK;
   const uint64_t W = 16 * ((n + 511) / 512), nsb = (n + 511) / 512 + 1;
-  if ((e = cudaMemsetAsync(out->bitmaps, 0, (size_t)L * W * 4, s)) != cudaSuccess) return fail_cuda(e, "memset bitmaps");
   // scratch: flag, ticket counters (one per level), look-back status/values, block counts
   char* sc = static_cast<char*>(d_scratch);
   const uint64_t tiles = std::max<uint64_t>(1, (nsb + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
@@ -823,8 +820,10 @@ wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, 
                              tiles};
   uint32_t* blk = reinterpret_cast<uint32_t*>(sc + off_blk);
   for (uint32_t l = 0; l < L; ++l) {
-    if (sg.wbase[k]) {
-      wt::k_dd_merge_level<<<(uint32_t)((sg.wbase[k] + 255) / 256), 256, 0, s>>>(sg, l, C, out->bitmaps + (uint64_t)l * W);
+    if (W) {
+      const uint64_t threads = (W + wt::DD_WPT - 1) / wt::DD_WPT;
+      wt::k_dd_merge_level<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(sg, l, C, n, W,
+                                                                          out->bitmaps + (uint64_t)l * W);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_dd_merge_level");
     }
     const uint32_t* lb_bits = out->bitmaps + (uint64_t)l * W;

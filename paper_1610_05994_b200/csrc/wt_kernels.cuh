@@ -442,64 +442,92 @@ __global__ void k_matrix_rank(TreeView t, const unsigned long long* __restrict__
 // node v, then segment 1's, ... (stability across segments).  With Cg the
 // segments' node offsets and C = sum_g Cg, segment g's run of node v goes to
 //   C[v << (L-l)] + sum_{g' < g} (Cg'[(v+1) << (L-l)] - Cg'[v << (L-l)]).
-// One thread per 32-bit word of a segment's level bitmap: it finds the node
-// of its first bit (binary search over the segment's level-l node starts),
-// then moves each node piece of its word with at most two atomicOr (the
-// merged bitmap is zeroed first; runs of different segments share words).
+// Destination-driven: one thread per DD_WPT consecutive words of the merged
+// level bitmap.  It finds the node v holding its first position (binary search
+// over C's level-l node starts) and the segment run inside v, then walks the
+// runs (v, 0), (v, 1), ..., (v + 1, 0), ... in merged order, funnel-shifting
+// up to 32 source bits at a time into the word it assembles; every word is
+// written once with a plain store (no zero fill, no atomics), words past n are
+// written as zeros.
 constexpr int DD_MAX_SEGMENTS = 8;
 struct DdSegments {
   const uint32_t* bits[DD_MAX_SEGMENTS];  // level-major bitmaps of each segment
   const unsigned long long* C[DD_MAX_SEGMENTS];
   uint64_t n[DD_MAX_SEGMENTS], W[DD_MAX_SEGMENTS];
-  uint64_t wbase[DD_MAX_SEGMENTS + 1];  // prefix of the segments' words per level (thread -> (g, word))
   uint32_t k, L;
 };
-__global__ void k_dd_merge_level(DdSegments sg, uint32_t l, const unsigned long long* __restrict__ C,
-                                 uint32_t* __restrict__ out_bits) {
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= sg.wbase[sg.k]) return;
-  uint32_t g = 0;
-  while (t >= sg.wbase[g + 1]) ++g;
-  const uint64_t w = t - sg.wbase[g];
-  const uint64_t ng = sg.n[g];
-  const uint64_t p0 = 32 * w;
-  if (p0 >= ng) return;
-  const uint64_t pend = min(p0 + 32, ng);
-  const uint32_t word = sg.bits[g][(uint64_t)l * sg.W[g] + w];
+constexpr uint32_t DD_WPT = 8;  // merged words per thread
+__global__ void k_dd_merge_level(DdSegments sg, uint32_t l, const unsigned long long* __restrict__ C, uint64_t n,
+                                 uint64_t W, uint32_t* __restrict__ out_bits) {
+  const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * DD_WPT;
+  if (w0 >= W) return;
+  const uint64_t w1 = min(w0 + DD_WPT, W);
+  const uint64_t qend = min(32 * w1, n);
   const uint32_t sh = sg.L - l;  // node v of level l spans leaves [v << sh, (v + 1) << sh)
-  const unsigned long long* Cg = sg.C[g];
-  // node of position p0: largest v with Cg[v << sh] <= p0
-  uint64_t lo = 0, hi = 1ull << l;  // Cg[lo << sh] <= p0 < Cg[hi << sh] (= ng)
-  while (hi - lo > 1) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (Cg[mid << sh] <= p0) lo = mid;
-    else hi = mid;
-  }
-  uint64_t v = lo, pos = p0;
-  while (pos < pend) {
-    if (Cg[(v + 1) << sh] <= pos) {  // past node v: the node holding pos (skipping empty nodes)
-      uint64_t a = v + 1, z = 1ull << l;  // Cg[a << sh] <= pos < Cg[z << sh]
-      while (z - a > 1) {
-        const uint64_t mid = (a + z) >> 1;
-        if (Cg[mid << sh] <= pos) a = mid;
+  const uint64_t nodes = 1ull << l;
+  uint64_t q = 32 * w0;
+  if (q < qend) {
+    uint64_t v = 0, sp = 0, rem = 0;  // current run: segment h, source positions [sp, sp + rem)
+    uint32_t h = 0;
+    // (v, h, sp, rem) for merged position q, v searched in [lo, nodes)
+    auto enter = [&](uint64_t lo) {
+      uint64_t z = nodes;
+      while (z - lo > 1) {
+        const uint64_t mid = (lo + z) >> 1;
+        if (C[mid << sh] <= q) lo = mid;
         else z = mid;
       }
-      v = a;
+      v = lo;
+      uint64_t off = q - C[v << sh];
+      for (h = 0;; ++h) {  // q < C[(v + 1) << sh]: some segment holds it
+        const uint64_t a = sg.C[h][v << sh], sz = sg.C[h][(v + 1) << sh] - a;
+        if (off < sz) {
+          sp = a + off;
+          rem = sz - off;
+          return;
+        }
+        off -= sz;
+      }
+    };
+    enter(0);
+    uint32_t acc = 0;
+    for (;;) {
+      const uint32_t d = (uint32_t)(q & 31);
+      const uint32_t len = (uint32_t)min(min(rem, qend - q), (uint64_t)(32 - d));
+      const uint32_t* src = sg.bits[h] + (uint64_t)l * sg.W[h];
+      const uint32_t o = (uint32_t)(sp & 31);
+      const uint32_t lo_w = src[sp >> 5];
+      const uint32_t hi_w = (o + len > 32) ? src[(sp >> 5) + 1] : 0u;
+      uint32_t x = __funnelshift_r(lo_w, hi_w, o);
+      if (len < 32) x &= (1u << len) - 1u;
+      acc |= x << d;
+      q += len;
+      sp += len;
+      rem -= len;
+      if ((q & 31) == 0) {
+        out_bits[(q >> 5) - 1] = acc;
+        acc = 0;
+      }
+      if (q >= qend) break;
+      if (rem == 0) {  // next non-empty run: later segment of v, else a later node
+        uint32_t g = h + 1;
+        for (; g < sg.k; ++g) {
+          const uint64_t a = sg.C[g][v << sh], sz = sg.C[g][(v + 1) << sh] - a;
+          if (sz) {
+            h = g;
+            sp = a;
+            rem = sz;
+            break;
+          }
+        }
+        if (g == sg.k) enter(v + 1);
+      }
     }
-    const uint64_t vs = Cg[v << sh], ve = Cg[(v + 1) << sh];
-    const uint64_t e = min(pend, ve);
-    uint64_t dst = C[v << sh] + (pos - vs);
-    for (uint32_t h = 0; h < g; ++h) dst += sg.C[h][(v + 1) << sh] - sg.C[h][v << sh];
-    const uint32_t len = (uint32_t)(e - pos), off = (uint32_t)(pos - p0);
-    const uint32_t piece = (word >> off) & (len >= 32 ? 0xffffffffu : ((1u << len) - 1u));
-    if (piece) {
-      const uint32_t d = (uint32_t)(dst & 31);
-      atomicOr(&out_bits[dst >> 5], piece << d);
-      if (d && d + len > 32) atomicOr(&out_bits[(dst >> 5) + 1], piece >> (32 - d));
-    }
-    pos = e;
+    if (q & 31) out_bits[q >> 5] = acc;  // q == n: the last, partial word
   }
+  for (uint64_t w = max(w0, (n + 31) >> 5); w < w1; ++w) out_bits[w] = 0;  // padding past n
 }
+
 // C = sum over the segments' node offsets
 __global__ void k_dd_sum_offsets(DdSegments sg, uint64_t count, unsigned long long* __restrict__ C) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
