@@ -199,6 +199,16 @@ bool pdl_enabled() {
   }();
   return on;
 }
+// The final pair pass writes B_{L-1}'s runs with global OR-reductions when it
+// reads S itself (L = 2, where the pass is ALU-bound);
+// WT_PAIR_RED=0/1 forces it off/on (A/B).
+int pair_red_override() {
+  static const int v = [] {
+    const char* s = std::getenv("WT_PAIR_RED");
+    return (s && *s) ? (*s != '0' ? 1 : 0) : -1;
+  }();
+  return v;
+}
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), uint32_t grid, uint32_t block, size_t smem, cudaStream_t s,
                        Args... args) {
@@ -350,7 +360,9 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
     T* o = mode == 0 ? nullptr : mode == 2 ? reinterpret_cast<T*>(out->bitmaps + (uint64_t)(L - 1) * c.words)
                                            : buf[l & 1];
-    const uint32_t sh = (L - 1 - l) | (matrix ? wt::LV_MATRIX : 0u);
+    const int red = pair_red_override();
+    const bool red_runs = mode == 2 && (red < 0 ? l == 0 : red == 1);
+    const uint32_t sh = (L - 1 - l) | (matrix ? wt::LV_MATRIX : 0u) | (red_runs ? wt::LV_RED : 0u);
     const uint2* t = mode == 0 ? nullptr : matrix ? tab + l : tab + ((1ull << l) - 1);
     uint32_t* bits = out->bitmaps + (uint64_t)l * c.words;
     unsigned long long* sb = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;

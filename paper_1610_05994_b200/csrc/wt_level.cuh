@@ -57,6 +57,7 @@ constexpr int LV_NREG = 5;  // regions: identity, first zeros/ones, last zeros/o
 constexpr int LV_NKEY = 2 * LV_NREG;
 constexpr int LV_THREADS = 32;  // one warp per CTA
 constexpr uint32_t LV_MATRIX = 0x100;  // k_level `shf` flag: wavelet-matrix level (global partition)
+constexpr uint32_t LV_RED = 0x200;     // k_level `shf` flag (MODE 2): B_{L-1} runs as global OR-reductions
 
 template <typename T>
 struct LvTile {
@@ -500,36 +501,56 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
         cc_acc += (lane & 1u) ? cx : ((lane & 2u) ? o0 : z0) - cx;
       }
 #endif
-      // bit stage in the output buffer: zero-run words [0, WZ), one-run words [WZ, 2 WZ)
-      constexpr uint32_t WZ = (TILE / 32 + 2 + 3) & ~3u;  // (a multiple of 4 words: 16-byte zeroing)
-      uint32_t* const st = reinterpret_cast<uint32_t*>(S.buf[ob]);
-      for (uint32_t j = lane; j < 2 * WZ / 4; j += 32) reinterpret_cast<uint4*>(st)[j] = make_uint4(0, 0, 0, 0);
-      __syncwarp();
-      auto put = [&](uint32_t base, uint32_t pos, const uint32_t (&v)[2], uint32_t nb) {  // nb bits of v at bit pos
-        if (nb == 0) return;
-        const uint32_t j = pos >> 5, off = pos & 31u;
-        const uint32_t w0 = v[0] << off;
-        const uint32_t w1 = __funnelshift_lc(v[0], v[1], off);
-        const uint32_t w2 = __funnelshift_lc(v[1], 0u, off);
-        if (w0) atomicOr(&st[base + j], w0);
-        if (w1) atomicOr(&st[base + j + 1], w1);
-        if (w2) atomicOr(&st[base + j + 2], w2);
-      };
-      put(0, (D0z & 31u) + rz, Z, nzl);
-      put(WZ, (D0o & 31u) + ro, O, nol);
-      __syncwarp();
-      uint32_t* const nbits = reinterpret_cast<uint32_t*>(out);
-      // the two runs' words as one lane-parallel list: zero-run words [0, nwz), then one-run words
-      const uint32_t nwz = z0 ? ((D0z & 31u) + z0 + 31u) / 32u : 0u;
-      const uint32_t nwo = o0 ? ((D0o & 31u) + o0 + 31u) / 32u : 0u;
-      for (uint32_t s = lane; s < nwz + nwo; s += 32) {
-        const bool one_run = s >= nwz;
-        const uint32_t j = one_run ? s - nwz : s, nw = one_run ? nwo : nwz;
-        const uint32_t D = one_run ? D0o : D0z, l = one_run ? o0 : z0;
-        const uint32_t wv = st[(one_run ? WZ : 0u) + j];
-        const bool full = (j > 0 || (D & 31u) == 0) && (j + 1 < nw || ((D + l) & 31u) == 0);
-        if (full) nbits[D / 32u + j] = wv;
-        else if (wv) atomicOr(&nbits[D / 32u + j], wv);
+      // LV_RED: each lane ORs its two strings (at most three words each) into
+      // B_{L-1} with global reductions -- fewer instructions than the stage
+      // below, but every touched line of B_{L-1} is read back from HBM for the
+      // read-modify-write: the host sets it where the pass is ALU-bound (L = 2)
+      if (shf & LV_RED) {
+        uint32_t* const nbits = reinterpret_cast<uint32_t*>(out);
+        auto red = [&](uint32_t pos, const uint32_t (&v)[2], uint32_t nb) {  // nb bits of v at global bit pos
+          if (nb == 0) return;
+          const uint32_t j = pos >> 5, off = pos & 31u;
+          const uint32_t w0 = v[0] << off;
+          const uint32_t w1 = __funnelshift_lc(v[0], v[1], off);
+          const uint32_t w2 = __funnelshift_lc(v[1], 0u, off);
+          if (w0) atomicOr(&nbits[j], w0);
+          if (w1) atomicOr(&nbits[j + 1], w1);
+          if (w2) atomicOr(&nbits[j + 2], w2);
+        };
+        red(D0z + rz, Z, nzl);
+        red(D0o + ro, O, nol);
+      } else {
+        // bit stage in the output buffer: zero-run words [0, WZ), one-run words [WZ, 2 WZ)
+        constexpr uint32_t WZ = (TILE / 32 + 2 + 3) & ~3u;  // (a multiple of 4 words: 16-byte zeroing)
+        uint32_t* const st = reinterpret_cast<uint32_t*>(S.buf[ob]);
+        for (uint32_t j = lane; j < 2 * WZ / 4; j += 32) reinterpret_cast<uint4*>(st)[j] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        auto put = [&](uint32_t base, uint32_t pos, const uint32_t (&v)[2], uint32_t nb) {  // nb bits of v at bit pos
+          if (nb == 0) return;
+          const uint32_t j = pos >> 5, off = pos & 31u;
+          const uint32_t w0 = v[0] << off;
+          const uint32_t w1 = __funnelshift_lc(v[0], v[1], off);
+          const uint32_t w2 = __funnelshift_lc(v[1], 0u, off);
+          if (w0) atomicOr(&st[base + j], w0);
+          if (w1) atomicOr(&st[base + j + 1], w1);
+          if (w2) atomicOr(&st[base + j + 2], w2);
+        };
+        put(0, (D0z & 31u) + rz, Z, nzl);
+        put(WZ, (D0o & 31u) + ro, O, nol);
+        __syncwarp();
+        uint32_t* const nbits = reinterpret_cast<uint32_t*>(out);
+        // the two runs' words as one lane-parallel list: zero-run words [0, nwz), then one-run words
+        const uint32_t nwz = z0 ? ((D0z & 31u) + z0 + 31u) / 32u : 0u;
+        const uint32_t nwo = o0 ? ((D0o & 31u) + o0 + 31u) / 32u : 0u;
+        for (uint32_t s = lane; s < nwz + nwo; s += 32) {
+          const bool one_run = s >= nwz;
+          const uint32_t j = one_run ? s - nwz : s, nw = one_run ? nwo : nwz;
+          const uint32_t D = one_run ? D0o : D0z, l = one_run ? o0 : z0;
+          const uint32_t wv = st[(one_run ? WZ : 0u) + j];
+          const bool full = (j > 0 || (D & 31u) == 0) && (j + 1 < nw || ((D + l) & 31u) == 0);
+          if (full) nbits[D / 32u + j] = wv;
+          else if (wv) atomicOr(&nbits[D / 32u + j], wv);
+        }
       }
     } else if (nseg == 1) {
       // ================= one segment: the whole tile lies in node vF.  Zeros
