@@ -115,6 +115,14 @@ def test_symbol_range_error(wt):
         with pytest.raises(wt.WtError) as e:
             wt.build(to_dev(S), sigma)
         assert e.value.status == wt.WT_ERR_SYMBOL_RANGE
+    # L = 2, u8 (the pass that reads S itself checks the range): a bad symbol
+    # in a full tile and in the ragged last tile, sigma = 3 and 4
+    for pos, val, sigma in [(3000, 3, 3), (100, 7, 4), (4500, 255, 4), (4999, 3, 3), (0, 4, 3)]:
+        S = np.random.default_rng(pos).integers(0, sigma, 5000).astype(np.uint8)
+        S[pos] = val
+        with pytest.raises(wt.WtError) as e:
+            wt.build(to_dev(S), sigma)
+        assert e.value.status == wt.WT_ERR_SYMBOL_RANGE
     # a valid build afterwards on the same device still works
     check_case(wt, np.array([0, 1, 2, 3], np.uint8), 4)
 
