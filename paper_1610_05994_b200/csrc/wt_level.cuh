@@ -43,7 +43,9 @@
 //     16-byte-aligned body, lane-parallel stores of the edge symbols, and the
 //     next level's ones per destination tile as a few global atomics;
 //   * MODE 2 (pass L-2 fused with level L-1) writes B_{L-1} instead of T_{L-1}:
-//     one-segment tiles compact the last-level bits per lane (no symbol moves);
+//     one-segment tiles compact the last-level bits per lane (no symbol moves)
+//     and store the two runs' words from a bit stage (or, with LV_RED, OR
+//     each lane's strings straight into B_{L-1}: the L = 2 pass);
 //     multi-segment tiles take them from the byte stage;
 //   * LV_MATRIX (wavelet matrix): one global node per level, every tile is a
 //     one-segment tile.
