@@ -316,7 +316,7 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       const uint64_t ga = (na + wt::SCAN_TILE - 1) / wt::SCAN_TILE, gb = (nb + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
       const uint64_t zu = z.n0 + z.n1;
       const uint64_t gz = zu ? std::min<uint64_t>((zu + 4 * wt::SCAN_THREADS - 1) / (4 * wt::SCAN_THREADS),
-                                                  2ull * num_sms())
+                                                  4ull * num_sms())
                              : (ga + gb ? 0 : 1);
       e = launch_pdl(wt::k_prep<decltype(opA), decltype(opB)>, (uint32_t)(ga + gb + gz), wt::SCAN_THREADS, 0, stream,
                      opA, na, status, counters + counter, epoch, opB, nb, status2, counters + counter + 1, epoch + 1, z,
