@@ -74,8 +74,8 @@ def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
         tables = sum(4 * (2 << l) + 8 * (1 << l) for l in range(max(L - 1, 0)))
         zero = sum(16 * (1 << l) for l in range(max(L - 1, 0))) + (bitmap if L >= 2 else 0)
         return 8 * tiles + (tables + zero) // levels
-    if kind == "final_scan":  # last-level superblocks from the block counts, C from the leaf counts
-        return 4 * (nsb - 1) + 8 * nsb + 4 * (1 << L) + 8 * ((1 << L) + 1)
+    if kind == "final_scan":  # last-level superblocks from its bitmap, C from the leaf counts
+        return bitmap + 8 * nsb + 4 * (1 << L) + 8 * ((1 << L) + 1)
     return 0
 
 

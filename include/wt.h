@@ -273,11 +273,12 @@ wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, 
  * (kinds may be NULL): 1 pass over S (prologue), 2 scan of node_offsets
  * (sigma = 1 only), 4 level pass with scatter (a3), 5 last level (a4, only
  * when L = 1), 8 level pass L-2 fused with level L-1 (a5 with k = 2: writes
- * B_{L-2} and B_{L-1}, no T_{L-1}), 10 per-block ones of level L-1,
+ * B_{L-2} and B_{L-1}, no T_{L-1}),
  * 11 per-level preparation (the level's tile-prefix scan, its node-table scan
  * and the zeroing of the node counts the pass fills -- and of B_{L-1} before
- * pass 8), 12 final scans (superblocks of level L-1, node_offsets).
- * Kinds 3, 6, 7, 9 are retired (folded into 11 and 12). */
+ * pass 8), 12 final scans (superblocks of level L-1 straight from its bitmap,
+ * node_offsets).
+ * Kinds 3, 6, 7, 9, 10 are retired (folded into 11 and 12). */
 uint32_t wt_launch_plan(uint64_t n, uint64_t sigma, uint32_t width, uint32_t* kinds, uint32_t cap);
 
 /* Debug aid: byte offsets inside the workspace of wt_build_async(n, sigma,

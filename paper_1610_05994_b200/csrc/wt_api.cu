@@ -88,7 +88,7 @@ struct Carve {
   uint64_t status_entries = 0, tab_entries = 0, cnt_entries = 0;
   size_t off_flag = 0, off_counters = 0, off_ones0 = 0, off_status = 0, off_value = 0, off_agg = 0, ctrl_bytes = 0;
   size_t off_status2 = 0, off_value2 = 0;  // a second look-back state (two scans per k_prep launch)
-  size_t off_pre = 0, off_tab = 0, off_cnt = 0, off_blk = 0, off_bufA = 0, off_bufB = 0, total = 0;
+  size_t off_pre = 0, off_tab = 0, off_cnt = 0, off_bufA = 0, off_bufB = 0, total = 0;
   // host-API extras (after total)
   size_t off_seq = 0, off_bits = 0, off_sb = 0, off_c = 0, host_total = 0;
 };
@@ -130,8 +130,6 @@ Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
   o += align_up(c.tab_entries * sizeof(uint2));
   c.off_cnt = o;
   o += 2 * align_up(c.cnt_entries * sizeof(uint32_t));
-  c.off_blk = o;  // ones per 512-bit block of the last level (its superblock scan)
-  if (c.L >= 2) o += align_up((c.nsb - 1) * sizeof(uint32_t));
   const size_t seq_bytes = align_up(n * width);
   // T_1 .. T_{L-2} (the fused pass L-2 writes no T_{L-1})
   c.off_bufA = o;
@@ -227,7 +225,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), uint32_t grid, uint32_t block, si
 
 enum Kind : uint32_t {
   K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7, K_PAIR = 8, K_SBSCAN = 9,
-  K_BLKPOP = 10, K_PREP = 11, K_FINAL = 12
+  K_PREP = 11, K_FINAL = 12
 };
 
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
@@ -432,25 +430,15 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   if (Lrun == L - 1) {
     // superblocks of level L-1 from the bitmap the fused pass wrote, and C
     // (exclusive scan of the leaf counts pass L-2 made)
-    uint32_t* blk = reinterpret_cast<uint32_t*>(ws + c.off_blk);
-    note(K_BLKPOP);
-    if (!dry) {
-      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      const uint64_t nbk = c.nsb - 1, warps = (nbk + 31) / 32;
-      const uint32_t g = (uint32_t)std::max<uint64_t>(
-          1, std::min<uint64_t>((warps + wt::BP_THREADS / 32 - 1) / (wt::BP_THREADS / 32), 16ull * num_sms()));
-      e = launch_pdl(wt::k_block_pop, g, wt::BP_THREADS, 0, stream, (const uint32_t*)lastbits, blk, nbk,
-                     (const int32_t*)flag);
-      if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_block_pop");
-      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-    }
-    unsigned long long* sbl =
+    // superblocks of level L-1: one scan launch that reads B_{L-1} itself
+    // (block popcounts taken coalesced per scan tile), and C
+    unsigned long long* const sbl =
         dry ? nullptr : reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)(L - 1) * c.nsb;
     if (matrix) {
-      if ((st = prep(K_FINAL, wt::OpBlockPopZ{blk, sbl, c.nsb - 1, mzeros + (L - 1), n}, c.nsb - 1, wt::OpNone{}, 0,
-                     nozero, "k_prep(final)")) != WT_OK)
+      if ((st = prep(K_FINAL, wt::OpBitsPopZ{lastbits, sbl, c.nsb - 1, mzeros + (L - 1), n}, c.nsb - 1, wt::OpNone{},
+                     0, nozero, "k_prep(final)")) != WT_OK)
         return st;
-    } else if ((st = prep(K_FINAL, wt::OpBlockPop{blk, sbl, c.nsb - 1}, c.nsb - 1,
+    } else if ((st = prep(K_FINAL, wt::OpBitsPop{lastbits, sbl, c.nsb - 1}, c.nsb - 1,
                           wt::OpLeafC{dry ? nullptr : cnt[(L - 2) & 1], C, 1ull << L, n, nullptr}, 1ull << L, nozero,
                           "k_prep(final)")) != WT_OK) {
       return st;
@@ -787,7 +775,7 @@ wt_status wt_remap_alphabet(const void* d_seq, uint64_t n, uint64_t sigma, uint3
 // ---------------------------------------------------------------- domain decomposition merge (NEXT-3)
 size_t wt_dd_merge_scratch_bytes(uint64_t n) {
   const uint64_t nsb = (n + 511) / 512 + 1, tiles = std::max<uint64_t>(1, (nsb + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
-  return 3 * ALIGN + align_up(tiles * 4) + align_up(2 * tiles * 8) + align_up(nsb * 4);
+  return 3 * ALIGN + align_up(tiles * 4) + align_up(2 * tiles * 8);
 }
 
 wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, uint64_t sigma,
@@ -820,17 +808,15 @@ wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, 
   if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_dd_sum_offsets");
   if (L == 0) return WT_OK;
   const uint64_t W = 16 * ((n + 511) / 512), nsb = (n + 511) / 512 + 1;
-  // scratch: flag, ticket counters (one per level), look-back status/values, block counts
+  // scratch: flag, ticket counters (one per level), look-back status/values
   char* sc = static_cast<char*>(d_scratch);
   const uint64_t tiles = std::max<uint64_t>(1, (nsb + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
   int32_t* flag = reinterpret_cast<int32_t*>(sc);
   uint32_t* counters = reinterpret_cast<uint32_t*>(sc + ALIGN);  // (32 levels * 4 B fit in ALIGN * 2)
-  const size_t off_status = 3 * ALIGN, off_value = off_status + align_up(tiles * 4),
-               off_blk = off_value + align_up(2 * tiles * 8);
+  const size_t off_status = 3 * ALIGN, off_value = off_status + align_up(tiles * 4);
   if ((e = cudaMemsetAsync(sc, 0, off_value, s)) != cudaSuccess) return fail_cuda(e, "memset scratch");
   const wt::LookbackState lb{reinterpret_cast<uint32_t*>(sc + off_status), reinterpret_cast<uint64_t*>(sc + off_value),
                              tiles};
-  uint32_t* blk = reinterpret_cast<uint32_t*>(sc + off_blk);
   for (uint32_t l = 0; l < L; ++l) {
     if (W) {
       const uint64_t threads = (W + wt::DD_WPT - 1) / wt::DD_WPT;
@@ -841,12 +827,8 @@ wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, 
     const uint32_t* lb_bits = out->bitmaps + (uint64_t)l * W;
     unsigned long long* sbl = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * nsb;
     if (nsb > 1) {
-      const uint64_t warps = (nsb - 1 + 31) / 32;
-      wt::k_block_pop<<<(uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, 16ull * num_sms())),
-                        wt::BP_THREADS, 0, s>>>(lb_bits, blk, nsb - 1, flag);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_block_pop");
-      wt::k_scan<wt::OpBlockPop><<<(uint32_t)tiles, wt::SCAN_THREADS, 0, s>>>(wt::OpBlockPop{blk, sbl, nsb - 1}, nsb - 1,
-                                                                          lb, counters + l, l + 1, flag);
+      wt::k_scan<wt::OpBitsPop><<<(uint32_t)tiles, wt::SCAN_THREADS, 0, s>>>(wt::OpBitsPop{lb_bits, sbl, nsb - 1},
+                                                                         nsb - 1, lb, counters + l, l + 1, flag);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(dd superblocks)");
     } else if ((e = cudaMemsetAsync(sbl, 0, 8, s)) != cudaSuccess) {
       return fail_cuda(e, "memset sb");

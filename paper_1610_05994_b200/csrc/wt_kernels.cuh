@@ -28,6 +28,13 @@ constexpr int SCAN_THREADS = 512;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
+// Scan ops whose values are the popcounts of consecutive 512-bit blocks of a
+// bitmap (`bits`): scan_tile loads the tile's blocks itself, coalesced.
+template <class Op>
+struct ScanOfBits {
+  static constexpr bool value = false;
+};
+
 // Exclusive scan of uint64 values over [0, count) with a decoupled look-back.
 // Op supplies load(i) and store(i, exclusive, value).  One CTA scans one tile
 // of SCAN_TILE values; tile ids come from an atomic ticket (forward progress).
@@ -43,10 +50,43 @@ __device__ __forceinline__ void scan_tile(const Op& op, uint64_t count, const Lo
   const uint64_t base = tile * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_ITEMS;
   uint64_t v[SCAN_ITEMS];
   uint64_t tsum = 0;
+  if constexpr (ScanOfBits<Op>::value) {
+    // the tile's blocks as 16-byte chunks, chunk c read by thread c % SCAN_THREADS
+    // (a warp reads 512 consecutive bytes per load); 4 consecutive lanes
+    // hold one block: two shuffles sum it, its first lane stores the count
+    __shared__ uint32_t s_cnt[SCAN_TILE];
+    constexpr uint32_t CH = 4 * SCAN_TILE / SCAN_THREADS;  // chunks per thread
+    const uint4* src = reinterpret_cast<const uint4*>(op.bits) + 4 * tile * SCAN_TILE;
+    const uint64_t t0 = tile * SCAN_TILE;  // (a surplus CTA's tile lies past count: no chunks)
+    const uint64_t nch = t0 < count ? 4 * min((uint64_t)SCAN_TILE, count - t0) : 0;
 #pragma unroll
-  for (int k = 0; k < SCAN_ITEMS; ++k) {
-    v[k] = (base + k < count) ? op.load(base + k) : 0;
-    tsum += v[k];
+    for (uint32_t j0 = 0; j0 < CH; j0 += 8) {
+      uint32_t c[8];
+#pragma unroll
+      for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t ch = threadIdx.x + SCAN_THREADS * (j0 + k);
+        const uint4 q = ch < nch ? ldg_nc_v4(src + ch) : make_uint4(0, 0, 0, 0);
+        c[k] = (uint32_t)(__popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w));
+      }
+#pragma unroll
+      for (uint32_t k = 0; k < 8; ++k) {
+        c[k] += __shfl_xor_sync(FULL, c[k], 1);
+        c[k] += __shfl_xor_sync(FULL, c[k], 2);
+        if ((threadIdx.x & 3) == 0) s_cnt[(threadIdx.x + SCAN_THREADS * (j0 + k)) >> 2] = c[k];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+      v[k] = (base + k < count) ? s_cnt[threadIdx.x * SCAN_ITEMS + k] : 0;
+      tsum += v[k];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+      v[k] = (base + k < count) ? op.load(base + k) : 0;
+      tsum += v[k];
+    }
   }
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t incl = warp_incl_scan_u64(tsum);
@@ -126,14 +166,32 @@ struct OpMatrixTab {
     }
   }
 };
-// the last level's superblocks (as OpBlockPop) and its zeros
-struct OpBlockPopZ {
-  const uint32_t* cnt;
+// Superblocks of a level from its finished bitmap (the last level, whose bits
+// the fused pass L-2 wrote in place; every level after a dd merge):
+// SB[t] = ones in the 512-bit blocks before t, SB[nblocks] = the level's total
+// (reading R7 of DESIGN.md).  One scan launch: scan_tile takes the
+// block popcounts itself (ScanOfBits), coalesced.
+struct OpBitsPop {
+  const uint32_t* bits;
+  unsigned long long* sb;
+  uint64_t nblocks;
+  __device__ uint64_t load(uint64_t) const { return 0; }  // (unused: ScanOfBits)
+  __device__ void store(uint64_t i, uint64_t excl, uint64_t val) const {
+    sb[i] = excl;
+    if (i + 1 == nblocks) sb[nblocks] = excl + val;
+  }
+};
+template <>
+struct ScanOfBits<OpBitsPop> {
+  static constexpr bool value = true;
+};
+struct OpBitsPopZ {  // (wavelet matrix: also the level's zeros)
+  const uint32_t* bits;
   unsigned long long* sb;
   uint64_t nblocks;
   unsigned long long* zeros;
   uint64_t n;
-  __device__ uint64_t load(uint64_t i) const { return cnt[i]; }
+  __device__ uint64_t load(uint64_t) const { return 0; }  // (unused: ScanOfBits)
   __device__ void store(uint64_t i, uint64_t excl, uint64_t val) const {
     sb[i] = excl;
     if (i + 1 == nblocks) {
@@ -141,6 +199,10 @@ struct OpBlockPopZ {
       zeros[0] = n - (excl + val);
     }
   }
+};
+template <>
+struct ScanOfBits<OpBitsPopZ> {
+  static constexpr bool value = true;
 };
 
 // ---------------------------------------------------------------- alphabet remap (NEXT-4)
@@ -258,54 +320,6 @@ struct OpLeafC {
   __device__ void store(uint64_t i, uint64_t excl, uint64_t val) const {
     C[i] = excl;
     if (i + 1 == count) C[count] = excl + val;
-  }
-};
-
-// Superblocks of a level from its finished bitmap (the last level, whose
-// bits the fused pass L-2 wrote in place): SB[t] = ones in the 512-bit blocks
-// before t, SB[nblocks] = the level's total (reading R7 of DESIGN.md).
-// Two steps: k_block_pop writes the per-block ones (coalesced: a warp reads 32
-// blocks = 2 KiB as consecutive 16-byte chunks), then a scan of the counts.
-constexpr int BP_THREADS = 256;
-__global__ void __launch_bounds__(BP_THREADS) k_block_pop(const uint32_t* __restrict__ bits, uint32_t* __restrict__ cnt,
-                                                          uint64_t nblocks, const int32_t* __restrict__ flag) {
-  pdl_wait();
-  pdl_trigger();
-  if (*flag) return;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t nw = (uint64_t)gridDim.x * (BP_THREADS / 32);
-  const uint4* src = reinterpret_cast<const uint4*>(bits);
-  for (uint64_t wb = (uint64_t)blockIdx.x * (BP_THREADS / 32) + (threadIdx.x >> 5); wb * 32 < nblocks; wb += nw) {
-    uint32_t c[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {  // chunk lane + 32 k of the warp's 128 = block 8 k + lane / 4
-      const uint64_t ch = wb * 128 + lane + 32 * k;
-      c[k] = 0;
-      if (ch < 4 * nblocks) {
-        const uint4 q = ldg_nc_v4(src + ch);
-        c[k] = (uint32_t)(__popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w));
-      }
-      c[k] += __shfl_xor_sync(FULL, c[k], 1);
-      c[k] += __shfl_xor_sync(FULL, c[k], 2);
-    }
-    if ((lane & 3) == 0) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint64_t b = wb * 32 + 8 * k + lane / 4;
-        if (b < nblocks) cnt[b] = c[k];
-      }
-    }
-  }
-}
-
-struct OpBlockPop {
-  const uint32_t* cnt;  // ones per 512-bit block (k_block_pop)
-  unsigned long long* sb;
-  uint64_t nblocks;
-  __device__ uint64_t load(uint64_t i) const { return cnt[i]; }
-  __device__ void store(uint64_t i, uint64_t excl, uint64_t val) const {
-    sb[i] = excl;
-    if (i + 1 == nblocks) sb[nblocks] = excl + val;
   }
 };
 

@@ -91,9 +91,9 @@ def test_build_validates_before_touching_the_device(wt):
 def test_launch_plan(wt):
     # per level one prep launch (tile prefixes, node tables, zeroing) and the
     # pass; pass L-2 is fused with level L-1 (writes B_{L-1}), then the last
-    # level's block counts and one launch for its superblocks and C
+    # level's superblocks (from its bitmap) and C in one launch
     lv = ["prep", "level"]
-    pair = ["prep", "pair", "block_pop", "final_scan"]
+    pair = ["prep", "pair", "final_scan"]
     assert wt.launch_plan(1 << 20, 256, 1) == ["prologue"] + lv * 6 + pair
     assert wt.launch_plan(1 << 20, 4, 1) == ["prologue"] + pair
     assert wt.launch_plan(1 << 20, 8, 1) == ["prologue"] + lv + pair

@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def kind_of(name: str) -> str:
     if "k_prep" in name:
-        return "final_scan" if "OpBlockPop" in name else "prep"
+        return "final_scan" if ("OpBitsPop" in name or "OpBlockPop" in name) else "prep"
     if "k_prologue" in name:
         return "prologue"
     if "k_level" in name:
@@ -31,7 +31,7 @@ def kind_of(name: str) -> str:
         return "tables"
     if "OpLeafC" in name:
         return "scan"
-    if "OpBlockPop" in name:
+    if "OpBitsPop" in name or "OpBlockPop" in name:
         return "sb_scan"
     if "k_block_pop" in name:
         return "block_pop"
