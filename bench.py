@@ -59,8 +59,6 @@ def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
         return n * w + bitmap + 8 * nsb
     if kind == "pair":        # level L-2 fused with L-1: read T_{L-2}, both bitmaps, superblocks of L-2
         return n * w + 2 * bitmap + 8 * nsb
-    if kind == "block_pop":   # ones per 512-bit block of level L-1: read its bitmap, write uint32 counts
-        return bitmap + 4 * (nsb - 1)
     if kind == "sb_scan":     # superblocks of level L-1 from the block counts
         return 4 * (nsb - 1) + 8 * nsb
     if kind == "prologue":    # read S once (range check, level-0 tile ones)
