@@ -416,7 +416,10 @@ def test_alphabet_remap(wt, sigma, n, dtype, kind):
 
 @pytest.mark.parametrize("sigma,n,k,dtype", [(16, 30, 3, None), (4, 1_000_003, 2, None), (256, 300_001, 5, None),
                                              (1 << 16, 200_000, 8, np.uint16), (1 << 20, 150_001, 4, np.uint32),
-                                             (3, 5000, 7, None), (256, 100, 8, None)])
+                                             (3, 5000, 7, None), (256, 100, 8, None),
+                                             # 4096 superblocks exactly: the superblock scan's grid has a
+                                             # surplus CTA whose tile lies past the blocks
+                                             (256, 1 << 21, 2, None)])
 def test_dd_merge_equals_direct_build(wt, sigma, n, k, dtype):
     # the merged tree of k segment trees is the tree of the whole sequence
     for kind in ("uniform", "zipf", "runs"):
