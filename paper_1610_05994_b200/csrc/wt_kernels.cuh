@@ -54,7 +54,8 @@ __device__ __forceinline__ void scan_tile(const Op& op, uint64_t count, const Lo
     // the tile's blocks as 16-byte chunks, chunk c read by thread c % SCAN_THREADS
     // (a warp reads 512 consecutive bytes per load); 4 consecutive lanes
     // hold one block: two shuffles sum it, its first lane stores the count
-    __shared__ uint32_t s_cnt[SCAN_TILE];
+    __shared__ __align__(16) uint32_t s_cnt[SCAN_TILE];
+    static_assert(SCAN_ITEMS % 4 == 0, "16-byte item loads");
     constexpr uint32_t CH = 4 * SCAN_TILE / SCAN_THREADS;  // chunks per thread
     const uint4* src = reinterpret_cast<const uint4*>(op.bits) + 4 * tile * SCAN_TILE;
     const uint64_t t0 = tile * SCAN_TILE;  // (a surplus CTA's tile lies past count: no chunks)
@@ -76,9 +77,15 @@ __device__ __forceinline__ void scan_tile(const Op& op, uint64_t count, const Lo
       }
     }
     __syncthreads();
+    uint32_t cv[SCAN_ITEMS];  // the thread's items as 16-byte shared loads
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; k += 4) {
+      const uint4 q = *reinterpret_cast<const uint4*>(&s_cnt[threadIdx.x * SCAN_ITEMS + k]);
+      cv[k] = q.x, cv[k + 1] = q.y, cv[k + 2] = q.z, cv[k + 3] = q.w;
+    }
 #pragma unroll
     for (int k = 0; k < SCAN_ITEMS; ++k) {
-      v[k] = (base + k < count) ? s_cnt[threadIdx.x * SCAN_ITEMS + k] : 0;
+      v[k] = (base + k < count) ? cv[k] : 0;
       tsum += v[k];
     }
   } else {
