@@ -5,19 +5,22 @@
 A step = one whole build (pass over S, scans, node tables, every level pass) of
 one config's sequence, through the C ABI (wt_build_async), inputs resident in
 HBM.  Default workload = BASELINE configs[1] (cfg2, DNA-like, n=2^30 uint8,
-sigma=4).  Prints ONE JSON line on rank 0.
+sigma=4).  Prints ONE JSON line on rank 0.  The same run also times the three
+north-star configs (cfg3-5, n = 2^28) device-side and reports them under
+"north_star_configs" (build Gsym/s and per-kernel-kind fractions of the HBM
+roofline).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl ours|reference]
 
-Multi-GPU (torchrun, one process per GPU): every rank builds its own copy of
-the config (independent problems, no data-path collective) -> "scaling":
-"weak"; value = symbols of all ranks / max-over-ranks time.
+Multi-GPU (one process per GPU; `--gpus N` without torchrun re-launches itself
+under torch.distributed.run): see DESIGN.md §8 for the N > 1 step.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,9 +36,12 @@ import wt_inputs  # noqa: E402
 METRIC = "wavelet tree build Gsymbols/s (HBM GB/s vs roofline in 'roofline')"
 UNIT = "Gsymbols/s"
 DTYPE = {1: "u8", 2: "u16", 4: "u32"}
+# kernel kinds whose per-launch HBM fraction is a roofline statement (the scans
+# move a few MB and are latency-bound)
+STREAMING_KINDS = ("prologue", "level", "pair", "last_level", "final_scan")
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
@@ -45,12 +51,14 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=9)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg3-5 device-timed lines")
+    ap.add_argument("--extra-steps", type=int, default=10)
     ap.add_argument("--out", default=None, help="also write the JSON line (plus per-kernel detail) here")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
-    """Bytes the levelwise method itself must move per launch."""
+    """Bytes the levelwise method itself must move per launch (DESIGN.md §6 table)."""
     nsb = (n + 511) // 512 + 1
     bitmap = 4 * 16 * ((n + 511) // 512)
     if kind == "level":      # read T_l, write T_{l+1}, bitmap words, superblocks
@@ -59,13 +67,11 @@ def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
         return n * w + bitmap + 8 * nsb
     if kind == "pair":        # level L-2 fused with L-1: read T_{L-2}, both bitmaps, superblocks of L-2
         return n * w + 2 * bitmap + 8 * nsb
-    if kind == "sb_scan":     # superblocks of level L-1 from the block counts
-        return 4 * (nsb - 1) + 8 * nsb
     if kind == "prologue":    # read S once (range check, level-0 tile ones)
         return n * w
     if kind == "scan":        # node_offsets: read 2^L uint32 leaf counts, write 2^L + 1 uint64
         return 4 * (1 << L) + 8 * ((1 << L) + 1)
-    if kind in ("prep", "tile_scan"):  # tile prefixes (read agg, write pre), node tables, zeroed counts; avg per launch
+    if kind == "prep":        # tile prefixes (read agg, write pre), node tables, zeroed counts; avg per launch
         tile = {1: 2048, 2: 1024, 4: 512}[w]
         tiles = (n + tile - 1) // tile
         levels = max(L - 1, 1)
@@ -147,44 +153,71 @@ def cpu_model():
     return "unknown"
 
 
+def config_of(cfg: int, world: int = 1) -> dict:
+    """The `config` object of the JSON line -- identical for both arms."""
+    c = wt_inputs.CONFIGS[cfg]
+    w = np.dtype(c["dtype"]).itemsize
+    L = max(0, (c["sigma"] - 1).bit_length())
+    return {"workload": f"{c['name']} (BASELINE configs[{cfg - 1}])", "n": c["n"], "sigma": c["sigma"],
+            "width": w, "levels": L,
+            "l2": "inputs exceed L2 (n*w >= 256 MiB > 126 MB), no flush" if c["n"] * w > (200 << 20)
+            else "inputs fit in L2 (latency config), no flush",
+            "parallelism": "replicas" if world > 1 else "1 GPU"}
+
+
 def oracle_time(cfg: int, n_sample: int, reps: int):
-    """Time the CPU oracle (as it stands, one thread) on a prefix sample of the config."""
+    """Time the CPU oracle (as it stands: single-threaded C, Alg. 1) on the first
+    n_sample symbols of the config, pinned to ONE host core (os.sched_setaffinity),
+    `reps` repetitions.  Returns (n, seconds per repetition, core)."""
     import oracle
     S, sigma = wt_inputs.generate(cfg, n_sample)
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        oracle.build(S, sigma)
-        ts.append(time.perf_counter() - t0)
-    return S.size, ts
+    oracle.lib()
+    old = os.sched_getaffinity(0)
+    core = max(old)                      # one core of those this process may use
+    os.sched_setaffinity(0, {core})
+    try:
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            oracle.build(S, sigma)
+            ts.append(time.perf_counter() - t0)
+    finally:
+        os.sched_setaffinity(0, old)
+    return S.size, ts, core
 
 
+# bounded samples (~3 s of single-core oracle work per repetition)
 ORACLE_SAMPLE = {1: 1 << 20, 2: 1 << 28, 3: 1 << 26, 4: 1 << 24, 5: 1 << 23}
 
 
-def run_reference(args, rank):
-    """--impl reference: the CPU oracle is this tier's reference arm."""
+def cpu_baseline_of(cfg: int, n: int, ts, core, reps_note: str) -> dict:
+    c = wt_inputs.CONFIGS[cfg]
+    t = statistics.median(ts)
+    return {"value": n / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {n} of the {c['n']} symbols of {c['name']} (a bounded prefix; throughput = "
+                      f"prefix symbols / time), oracle (Alg. 1 sequential, gcc -O2, 1 thread pinned to host "
+                      f"core {core} by sched_setaffinity), {reps_note} ({t:.2f} s each)",
+            "sample_n": n, "host": cpu_model(), "host_cores": os.cpu_count()}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle is this tier's reference arm (rank 0 only)."""
     if rank != 0:
         return
-    cfg = wt_inputs.CONFIGS[args.config]
     n_s = ORACLE_SAMPLE[args.config] // 4
-    steps = args.steps or 3
-    for _ in range(args.warmup if args.warmup < 2 else 1):
+    steps = args.steps or 5
+    for _ in range(min(args.warmup, 1)):
         oracle_time(args.config, n_s, 1)
-    n, ts = oracle_time(args.config, n_s, steps)
+    n, ts, core = oracle_time(args.config, n_s, steps)
     t = statistics.median(ts)
     val = n / t / 1e9
-    w = np.dtype(cfg["dtype"]).itemsize
+    w = np.dtype(wt_inputs.CONFIGS[args.config]["dtype"]).itemsize
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": DTYPE[w], "data": "synthetic",
-        "config": {"workload": f"{cfg['name']} (BASELINE configs[{args.config - 1}])", "n": cfg["n"],
-                   "sigma": cfg["sigma"], "width": w},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"first {n} symbols of the config's sequence, oracle (Alg. 1 sequential, "
-                                   f"gcc -O2, 1 thread), median of {steps}",
-                         "host": cpu_model(), "host_cores": os.cpu_count()},
+        "config": config_of(args.config, world),
+        "cpu_baseline": cpu_baseline_of(args.config, n, ts, core, f"median of {steps}"),
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -203,8 +236,166 @@ def max_over_ranks(ms: float, world: int, device) -> float:
 
 
 def job_throughput(n_per_rank: int, world: int, ms_per_step: float) -> float:
-    """Whole-job Gsymbols/s: every rank builds its own replica of n symbols (weak scaling)."""
+    """Whole-job Gsymbols/s: every rank processes n symbols per step (weak scaling)."""
     return world * n_per_rank / (ms_per_step * 1e-3) / 1e9
+
+
+def time_builds(wt, d_seq, sigma, stream, steps, warmup, profile=True):
+    """Device-time `steps` builds back to back (CUDA events on the build stream),
+    then the same builds with a library-recorded event pair around every launch
+    (per-kernel durations on the launching stream).  Returns a dict."""
+    import torch
+    n = d_seq.numel()
+    w = wt.width_of(d_seq)
+    dev = d_seq.device
+    tree = wt.alloc_tree(n, sigma, w, dev)
+    ws = wt.alloc_workspace(n, sigma, w, dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    plan = wt.launch_plan(n, sigma, w)
+
+    def step():
+        wt.build_async(d_seq, sigma, tree=tree, workspace=ws, status=status, stream=stream)
+
+    for _ in range(warmup):
+        step()
+    stream.synchronize()
+    assert int(status.item()) == wt.WT_OK
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for _ in range(steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    res = {"ms_per_step": t0.elapsed_time(t1) / steps, "plan": plan, "tree": tree, "ws": ws, "status": status,
+           "step": step}
+    if not profile:
+        return res
+    nl = len(plan)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nl)] for _ in range(steps)]
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    p0.record(stream)
+    for k in range(steps):
+        wt.set_profile_events(evs[k])
+        step()
+    p1.record(stream)
+    wt.set_profile_events(None)
+    torch.cuda.synchronize()
+    per_launch = [[evs[k][2 * i].elapsed_time(evs[k][2 * i + 1]) for k in range(steps)] for i in range(nl)]
+    res["profiled_ms_per_step"] = p0.elapsed_time(p1) / steps
+    res["per_launch_ms"] = [sum(x) / steps for x in per_launch]
+    return res
+
+
+def kernel_table(res, n, w, L, peak):
+    """Per kernel kind: launches, time share of the step, algorithmic GB/s and the
+    min / mean / max per-launch fraction of the HBM roofline."""
+    plan, pl, ms = res["plan"], res["per_launch_ms"], res["ms_per_step"]
+    kinds = {}
+    for kd, t in zip(plan, pl):
+        kinds.setdefault(kd, []).append(t)
+    out = {}
+    for kd, ts in kinds.items():
+        ab = algorithmic_bytes(kd, n, w, L)
+        fr = [ab / (t * 1e-3) / 1e9 / peak for t in ts if t > 0]
+        e = {"launches_per_step": len(ts), "ms_per_step": sum(ts), "share": sum(ts) / ms,
+             "per_launch_ms": {"min": min(ts), "mean": sum(ts) / len(ts), "max": max(ts)},
+             "algorithmic_GBps": ab * len(ts) / (sum(ts) * 1e-3) / 1e9}
+        if kd in STREAMING_KINDS and fr:
+            e["roofline_frac"] = {"min": min(fr), "mean": sum(fr) / len(fr), "max": max(fr)}
+        out[kd] = e
+    return out
+
+
+def north_star_line(wt, cfg, stream, dev, steps, warmup, peak):
+    """Device-timed build of one north-star config (cfg3-5): Gsym/s plus the
+    per-kind roofline fractions (the level-partition kernels' target is >= 0.6)."""
+    import torch
+    S, sigma = wt_inputs.generate(cfg)
+    n, w = S.size, S.dtype.itemsize
+    d_seq = torch.from_numpy(S.view(np.int32) if w == 4 else S).to(dev)
+    del S
+    L = wt.sizes(n, sigma, w).levels
+    res = time_builds(wt, d_seq, sigma, stream, steps, warmup)
+    kt = kernel_table(res, n, w, L, peak)
+    lvl = [k for k in ("level", "pair", "last_level") if k in kt]
+    line = {"workload": config_of(cfg)["workload"], "n": n, "sigma": sigma, "width": w, "levels": L,
+            "steps": steps, "ms_per_step": res["ms_per_step"], "value": n / (res["ms_per_step"] * 1e-3) / 1e9,
+            "unit": UNIT, "level_partition_frac_min": min(kt[k]["roofline_frac"]["min"] for k in lvl),
+            "kernels": kt}
+    del d_seq, res
+    torch.cuda.empty_cache()
+    return line
+
+
+def e2e_throughput(wt, h_seq, sigma, dev, steps, world):
+    """End to end through the public host API: every step is the H2D of S from
+    pinned memory, the build, and the D2H of the whole tree and its status word
+    (wt_build_from_host_async).  Three builds are in flight on three streams with
+    their own workspaces, so one build's copies overlap the others' compute: the
+    value is the pipelined whole-job throughput of back-to-back host-to-host
+    builds (PCIe-bound), not one call's latency, which is reported beside it."""
+    import torch
+    n, w = h_seq.numel(), wt.width_of(h_seq)
+    h_pinned = h_seq.pin_memory()
+    INFLIGHT = 3
+    streams = [torch.cuda.Stream(device=dev) for _ in range(INFLIGHT)]
+    h_trees = [wt.alloc_host_tree(n, sigma, w) for _ in range(INFLIGHT)]
+    wss = [wt.alloc_workspace(n, sigma, w, dev, host=True) for _ in range(INFLIGHT)]
+    stats = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(INFLIGHT)]
+    for i in range(INFLIGHT):  # warm-up, every slot
+        wt.build_from_host_async(h_pinned, sigma, h_trees[i], wss[i], stats[i], stream=streams[i])
+    torch.cuda.synchronize()
+    # one call alone: H2D -> build -> D2H latency
+    l0 = torch.cuda.Event(enable_timing=True)
+    l1 = torch.cuda.Event(enable_timing=True)
+    l0.record(streams[0])
+    wt.build_from_host_async(h_pinned, sigma, h_trees[0], wss[0], stats[0], stream=streams[0])
+    l1.record(streams[0])
+    torch.cuda.synchronize()
+    single_ms = l0.elapsed_time(l1)
+    sz = wt.sizes(n, sigma, w)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(streams[0])
+    for s_ in streams[1:]:
+        s_.wait_event(e0)
+    for k in range(steps):
+        i = k % INFLIGHT
+        wt.build_from_host_async(h_pinned, sigma, h_trees[i], wss[i], stats[i], stream=streams[i])
+    for s_ in streams[1:]:
+        done = torch.cuda.Event()
+        done.record(s_)
+        streams[0].wait_event(done)
+    e1.record(streams[0])
+    torch.cuda.synchronize()
+    e_ms = max_over_ranks(e0.elapsed_time(e1) / steps, world, dev)
+    # correctness guard on the e2e results: status words and C[2^L] = n
+    assert all(int(x.item()) == wt.WT_OK for x in stats)
+    assert all(int(t.node_offsets[-1].item()) == n for t in h_trees)
+    return {"value": job_throughput(n, world, e_ms), "unit": UNIT, "ms_per_step": e_ms,
+            "h2d_bytes_per_step": n * w,
+            "d2h_bytes_per_step": int(sz.bitmap_bytes + sz.superblock_bytes + sz.node_offset_bytes + 4),
+            "pipelined": True, "single_build_ms": single_ms,
+            "single_build_value": n / (single_ms * 1e-3) / 1e9,
+            "api": f"wt_build_from_host_async (pinned host buffers; {INFLIGHT} builds in flight on "
+                   f"{INFLIGHT} streams; single_build_* = one call alone)"}
+
+
+def relaunch_under_torchrun(args):
+    """`--gpus N` (N > 1) without torchrun: start N ranks ourselves."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -212,8 +403,13 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                         f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus")
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, rank, world)
         return
 
     import torch
@@ -226,66 +422,42 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    cfg = wt_inputs.CONFIGS[args.config]
-    S, sigma = wt_inputs.generate(args.config)
+    cfg = args.config
+    S, sigma = wt_inputs.generate(cfg)
     n = S.size
     w = S.dtype.itemsize
     L = wt.sizes(n, sigma, w).levels
     h_seq = torch.from_numpy(S.view(np.int32) if w == 4 else S)
     d_seq = h_seq.to(dev)
     stream = torch.cuda.Stream(device=dev)
-    tree = wt.alloc_tree(n, sigma, w, dev)
-    ws = wt.alloc_workspace(n, sigma, w, dev)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
-    plan = wt.launch_plan(n, sigma, w)
-    steps = args.steps or {1: 2000, 2: 200, 3: 200, 4: 60, 5: 25}[args.config]
+    steps = args.steps or {1: 2000, 2: 200, 3: 200, 4: 60, 5: 25}[cfg]
     warmup = max(3, args.warmup)
-
-    def step():
-        wt.build_async(d_seq, sigma, tree=tree, workspace=ws, status=status, stream=stream)
-
-    with torch.cuda.stream(stream):
-        for _ in range(warmup):
-            step()
-    stream.synchronize()
-    assert int(status.item()) == wt.WT_OK
+    peak, peak_src = measured_peaks()
 
     # timed region 1 (the reported value): K builds back to back, no instrumentation
-    nl = len(plan)
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     with sampler:
         if world > 1:
             dist.barrier()
-        torch.cuda.synchronize()
-        t_start.record(stream)
-        for k in range(steps):
-            step()
-        t_end.record(stream)
-        torch.cuda.synchronize()
+        res = time_builds(wt, d_seq, sigma, stream, steps, warmup, profile=False)
         if world > 1:
             dist.barrier()
-    elapsed_ms = max_over_ranks(t_start.elapsed_time(t_end), world, dev)
-    ms_per_step = elapsed_ms / steps
+    ms_per_step = max_over_ranks(res["ms_per_step"], world, dev)
     value = job_throughput(n, world, ms_per_step)
-
-    # timed region 2 (the per-kernel breakdown and roofline): the same K builds
-    # with a CUDA event pair recorded by the library around every launch, on
-    # the build stream (event records add small gaps, so the value above is
-    # taken without them)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nl)] for _ in range(steps)]
-    p_start = torch.cuda.Event(enable_timing=True)
-    p_end = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    p_start.record(stream)
-    for k in range(steps):
-        wt.set_profile_events(evs[k])
-        step()
-    p_end.record(stream)
-    wt.set_profile_events(None)
-    torch.cuda.synchronize()
-    profiled_ms_per_step = p_start.elapsed_time(p_end) / steps
+    # timed region 2 (per-kernel breakdown and roofline): the same builds with an
+    # event pair recorded by the library around every launch, on the build stream
+    prof = time_builds(wt, d_seq, sigma, stream, steps, 1, profile=True)
+    plan = prof["plan"]
+    kt = kernel_table(prof, n, w, L, peak)
+    dom = max(kt, key=lambda k: kt[k]["ms_per_step"])
+    avg_launch_ms = kt[dom]["ms_per_step"] / kt[dom]["launches_per_step"]
+    ab = algorithmic_bytes(dom, n, w, L)
+    achieved = ab / (avg_launch_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cfg}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(dom)
 
     # the same build captured once in a CUDA graph and replayed (launch gaps
     # removed); reported beside the direct-launch value, not instead of it
@@ -294,7 +466,7 @@ def main():
         try:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
-                step()
+                prof["step"]()
             g.replay()
             torch.cuda.synchronize()
             g0 = torch.cuda.Event(enable_timing=True)
@@ -307,116 +479,54 @@ def main():
             torch.cuda.synchronize()
             gms = g0.elapsed_time(g1) / steps
             graph = {"ms_per_step": gms, "value": job_throughput(n, world, gms), "unit": UNIT}
-            assert int(status.item()) == wt.WT_OK
+            assert int(prof["status"].item()) == wt.WT_OK
+            del g
         except Exception as e:  # report, do not fail the bench line
             graph = {"error": str(e)[:200]}
+    del res, prof
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
 
-    # per-kernel durations (same stream as the launches)
-    per_kind: dict[str, list[float]] = {}
-    per_launch = [0.0] * nl
-    for k in range(steps):
-        for i in range(nl):
-            d = evs[k][2 * i].elapsed_time(evs[k][2 * i + 1])
-            per_launch[i] += d / steps
-            per_kind.setdefault(plan[i], []).append(d)
-    kind_total = {kd: sum(v) / steps for kd, v in per_kind.items()}
-    dom = max(kind_total, key=kind_total.get)
-    launches_of = {kd: plan.count(kd) for kd in kind_total}
-    avg_launch_ms = kind_total[dom] / launches_of[dom]
-    ab = algorithmic_bytes(dom, n, w, L)
-    achieved = ab / (avg_launch_ms * 1e-3) / 1e9
-    peak, peak_src = measured_peaks()
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.config}.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get(dom)
-    kernels = {kd: {"launches_per_step": launches_of[kd], "ms_per_step": kind_total[kd],
-                    "share": kind_total[kd] / ms_per_step,
-                    "algorithmic_GBps": algorithmic_bytes(kd, n, w, L) * launches_of[kd] /
-                    (kind_total[kd] * 1e-3) / 1e9}
-               for kd in kind_total}
-
-    # end-to-end through the public host API: every step is H2D of S from pinned
-    # memory, the build, and D2H of the whole tree (wt_build_from_host_async).
-    # INFLIGHT builds are in flight on as many streams with their own workspaces,
-    # so one build's copies overlap the others' compute (H2D and D2H use separate
-    # copy engines); a build's H2D -> build -> D2H chain is ~2-3x one copy.
     e2e = None
     if args.e2e_steps > 0:
-        h_pinned = h_seq.pin_memory()
-        del ws
-        torch.cuda.empty_cache()
-        INFLIGHT = 3
-        streams = [torch.cuda.Stream(device=dev) for _ in range(INFLIGHT)]
-        h_trees = [wt.alloc_host_tree(n, sigma, w) for _ in range(INFLIGHT)]
-        wss = [wt.alloc_workspace(n, sigma, w, dev, host=True) for _ in range(INFLIGHT)]
-        stats = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(INFLIGHT)]
-        for i in range(INFLIGHT):  # warm-up, every slot
-            wt.build_from_host_async(h_pinned, sigma, h_trees[i], wss[i], stats[i], stream=streams[i])
-        sz = wt.sizes(n, sigma, w)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(streams[0])
-        for s_ in streams[1:]:
-            s_.wait_event(e0)
-        for k in range(args.e2e_steps):
-            i = k % INFLIGHT
-            wt.build_from_host_async(h_pinned, sigma, h_trees[i], wss[i], stats[i], stream=streams[i])
-        for s_ in streams[1:]:
-            done = torch.cuda.Event()
-            done.record(s_)
-            streams[0].wait_event(done)
-        e1.record(streams[0])
-        torch.cuda.synchronize()
-        e_ms = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, world, dev)
-        e2e = {"value": job_throughput(n, world, e_ms), "unit": UNIT, "ms_per_step": e_ms,
-               "h2d_bytes_per_step": n * w,
-               "d2h_bytes_per_step": int(sz.bitmap_bytes + sz.superblock_bytes + sz.node_offset_bytes + 4),
-               "api": f"wt_build_from_host_async (pinned host buffers; {INFLIGHT} builds in flight on "
-                      f"{INFLIGHT} streams)"}
-        # correctness guard on the e2e results: status words and C[2^L] = n
-        assert all(int(x.item()) == wt.WT_OK for x in stats)
-        assert all(int(t.node_offsets[-1].item()) == n for t in h_trees)
+        e2e = e2e_throughput(wt, h_seq, sigma, dev, args.e2e_steps, world)
+    del d_seq
+    torch.cuda.empty_cache()
+
+    # the north-star configs (n = 2^28), device-timed, on rank 0 of a 1-GPU run
+    extra = None
+    if rank == 0 and world == 1 and not args.no_extra and cfg == 2:
+        extra = {}
+        for c in (3, 4, 5):
+            extra[f"cfg{c}"] = north_star_line(wt, c, stream, dev, args.extra_steps, 3, peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_s = min(ORACLE_SAMPLE[args.config], n)
-        ns, ts = oracle_time(args.config, n_s, 3)
-        cpu = {"value": ns / statistics.median(ts) / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"first {ns} symbols of {cfg['name']}, oracle (Alg. 1 sequential, gcc -O2, 1 thread), "
-                         f"median of 3 ({statistics.median(ts):.2f} s each)",
-               "host": cpu_model(), "host_cores": os.cpu_count()}
+        ns, ts, core = oracle_time(cfg, min(ORACLE_SAMPLE[cfg], n), 5)
+        cpu = cpu_baseline_of(cfg, ns, ts, core, "median of 5")
 
     clocks = sampler.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": DTYPE[w], "data": "synthetic",
-        "config": {"workload": f"{cfg['name']} (BASELINE configs[{args.config - 1}])", "n": n, "sigma": sigma,
-                   "width": w, "levels": L, "per_rank": "independent replica of the config",
-                   "l2": "inputs exceed L2 (n*w >= 256 MiB > 126 MB), no flush" if n * w > (200 << 20)
-                   else "inputs fit in L2 (latency config), no flush",
-                   "parallelism": f"replicas x{world}"},
-        "profiled_ms_per_step": profiled_ms_per_step,
+        "config": config_of(cfg, world),
         "graph": graph,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": ab, "avg_launch_ms": avg_launch_ms},
         "e2e": e2e,
-        "gpu_launches": steps * nl,
+        "gpu_launches": steps * len(plan),
         "clocks": clocks,
         "cpu_baseline": cpu,
-        "kernels": kernels,
+        "kernels": kt,
+        "north_star_configs": extra,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
         if args.out:
             with open(args.out, "w") as f:
-                json.dump(dict(line, per_launch_ms=per_launch, plan=plan), f, indent=1)
+                json.dump(dict(line, plan=plan), f, indent=1)
     if world > 1:
         dist.destroy_process_group()
 

@@ -130,6 +130,25 @@ def _stream_ptr(stream) -> int:
     return s.cuda_stream
 
 
+def _keep_for(stream, *tensors):
+    """Tensors allocated here on torch's current stream but used by kernels enqueued
+    on another `stream`: tell the caching allocator, so their memory is not handed out
+    again before that stream's work completes (torch Tensor.record_stream)."""
+    if stream is None:
+        return
+    for t in tensors:
+        if t is not None and t.is_cuda and t.numel():
+            t.record_stream(stream)
+
+
+def _sync(stream):
+    (stream if stream is not None else torch.cuda.current_stream()).synchronize()
+
+
+def _status_tensor(device):
+    return torch.zeros(1, dtype=torch.int32, device=device)
+
+
 def sizes(n: int, sigma: int, width: int) -> WtSizes:
     out = WtSizes()
     _check(_lib.wt_sizes(n, sigma, width, ctypes.byref(out)), "wt_sizes")
@@ -217,13 +236,17 @@ def build_async(seq: torch.Tensor, sigma: int, tree: WaveletTree | None = None,
     `status` (int32 device tensor, optional) receives WT_OK / WT_ERR_SYMBOL_RANGE."""
     if not seq.is_cuda:
         raise ValueError("seq must be a CUDA tensor (use build_from_host for host data)")
+    seq_in = seq
     seq = seq.contiguous()
     w = width_of(seq)
     n = seq.numel()
+    own_tree, own_ws = tree is None, workspace is None
     if tree is None:
         tree = alloc_tree(n, sigma, w, seq.device)
     if workspace is None:
         workspace = alloc_workspace(n, sigma, w, seq.device)
+    _keep_for(stream, seq if seq is not seq_in else None, workspace if own_ws else None,
+              *((tree.bitmaps, tree.superblocks, tree.node_offsets) if own_tree else ()))
     ct = tree._ctree()
     st = _lib.wt_build_async(seq.data_ptr() if n else None, n, sigma, w, ctypes.byref(ct),
                              workspace.data_ptr(), workspace.numel(),
@@ -315,8 +338,6 @@ def build_from_host_async(h_seq: torch.Tensor, sigma: int, h_tree: HostTree, wor
     return h_tree
 
 
-def _status_tensor(device):
-    return torch.zeros(1, dtype=torch.int32, device=device)
 
 
 def access(tree: WaveletTree, pos: torch.Tensor, stream=None, status: torch.Tensor | None = None) -> torch.Tensor:
@@ -429,6 +450,7 @@ def build_matrix(seq: torch.Tensor, sigma: int, workspace: torch.Tensor | None =
     st = _lib.wt_matrix_build_async(seq.data_ptr() if n else None, n, sigma, w, ctypes.byref(cm),
                                     workspace.data_ptr(), workspace.numel(), status.data_ptr(), _stream_ptr(stream))
     _check(st, "wt_matrix_build_async")
+    _sync(stream)  # the status word is written on `stream`, which need not be torch's current one
     if int(status.item()) != WT_OK:
         raise WtError(int(status.item()), "wt_matrix_build_async: a symbol is >= sigma")
     return mx
@@ -468,7 +490,8 @@ def remap_alphabet(seq: torch.Tensor, sigma: int, stream=None):
     n = seq.numel()
     dev = seq.device
     out = torch.empty_like(seq)
-    alphabet = torch.empty((max(sigma, 1),), dtype=torch.int32, device=dev)
+    # at most min(sigma, n) distinct values can occur (sigma may be 2^32)
+    alphabet = torch.empty((max(min(sigma, n), 1),), dtype=torch.int32, device=dev)
     sig = torch.zeros(1, dtype=torch.int64, device=dev)
     status = _status_tensor(dev)
     ws = torch.empty((max(int(_lib.wt_remap_workspace_bytes(sigma)), 256),), dtype=torch.uint8, device=dev)
@@ -476,6 +499,7 @@ def remap_alphabet(seq: torch.Tensor, sigma: int, stream=None):
                                 alphabet.data_ptr(), sig.data_ptr(), ws.data_ptr(), ws.numel(), status.data_ptr(),
                                 _stream_ptr(stream))
     _check(st, "wt_remap_alphabet")
+    _sync(stream)
     if int(status.item()) != WT_OK:
         raise WtError(int(status.item()), "wt_remap_alphabet: a symbol is >= sigma")
     s2 = int(sig.item())

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "wt.h"
@@ -41,35 +42,49 @@ uint64_t level_tile(uint32_t width) {
   }
 }
 
-int g_num_sms = 0;
+// Per-device launch facts (a process may drive several GPUs): the SM count
+// and, per level-kernel instantiation, the dynamic shared-memory opt-in and
+// the resident CTAs per SM.  Filled once per device under a mutex.
+constexpr int MAX_DEVICES = 64;
+std::mutex g_dev_mu;
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAX_DEVICES) dev = 0;
+  return dev;
+}
+
 int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || g_num_sms <= 0)
-      g_num_sms = 148;
-  }
-  return g_num_sms;
+  static int sms[MAX_DEVICES] = {};
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  if (sms[dev] == 0 &&
+      (cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms[dev] <= 0))
+    sms[dev] = 148;
+  return sms[dev];
 }
 
 // opt in to > 48 KiB dynamic shared memory once per level-kernel instantiation
-// and size the persistent grid: every resident CTA slot of every SM.
+// and device, and size the persistent grid: every resident CTA slot of every SM.
 template <typename T, int SC>
 cudaError_t level_kernel_setup(int* blocks_per_sm) {
-  static int bps = 0;
-  static cudaError_t once = [] {
+  static int bps[MAX_DEVICES] = {};
+  static cudaError_t err[MAX_DEVICES] = {};
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  if (bps[dev] == 0) {
     cudaError_t e = cudaFuncSetAttribute(wt::k_level<T, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)wt::level_smem_bytes<T>());
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, wt::k_level<T, SC>, wt::LV_THREADS,
-                                                      wt::level_smem_bytes<T>());
-    if (bps < 1) bps = 1;
-    return e;
-  }();
-  *blocks_per_sm = bps;
-  return once;
+    int b = 0;
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, wt::k_level<T, SC>, wt::LV_THREADS,
+                                                        wt::level_smem_bytes<T>());
+    err[dev] = e;
+    bps[dev] = b < 1 ? 1 : b;
+  }
+  *blocks_per_sm = bps[dev];
+  return err[dev];
 }
-
 
 constexpr int MAX_LOOKBACK_LAUNCHES = 128;
 

@@ -1,24 +1,19 @@
-// wt_kernels.cuh -- the hot path of the levelwise wavelet-tree build (sm_100a).
-//
-// Steps (PAPER.md = P:n):
-//   a1 k_hist_*      H[c] = #{j : S[j] = c} plus the symbol-range flag.  Alg. 1
-//                    counts per level (lines 5-6); by Prop. 1
-//                     every level's counters are a coarsening of H,
-//                    so one pass over S serves all levels.
-//   a2 k_scan        C = exclusive_scan(H) (line 7), in place in the
-//                    caller's node_offsets; then the per-level node tables.
-//   a3 k_level<.,1>  level l < L-1: stable segmented bit-partition of T_l:
-//                    bitmap words by ballot, rank by warp/block scan +
-//                    decoupled look-back, superblocks, scatter to T_{l+1}.
-//   a4 k_level<.,0>  level L-1: bitmap + superblocks only.
+// wt_kernels.cuh -- the build's scan kernels and the query / merge / remap
+// kernels (sm_100a).  The launch sequence of a build (PAPER.md = P:n):
+//   a1 k_prologue     (wt_prologue.cuh) one pass over S: symbol-range flag and the
+//                     level-0 ones of every level tile.  No histogram of S is
+//                     taken: Alg. 1's per-level counters (lines 5-6)
+//                     are node sizes (Prop. 1), counted two levels
+//                     ahead by the level passes ("progressive counting").
+//   a2 k_prep         per level: decoupled-look-back scans (this file) of the
+//                     per-tile ones (tile prefixes) and of the node sizes (node
+//                     tables); the final one writes C (line 7, P:541-543,
+//                     exclusive) and the last level's superblocks.
+//   a3/a5 k_level     (wt_level.cuh) the per-level stable segmented bit-partition
+//                     of T_l; the pass of level L-2 is fused with level L-1.
 #pragma once
 #include "wt_device.cuh"
-
-namespace wt {
-
-}  // namespace wt
-
-#include "wt_hist.cuh"
+#include "wt_prologue.cuh"
 
 namespace wt {
 
@@ -218,7 +213,7 @@ struct ScanOfBits<OpBitsPopZ> {
 // levels for sigma' distinct values).  A presence bitmap over [0, sigma), a
 // scan of its word popcounts, then every symbol is replaced by its rank.
 template <typename T>
-__global__ void k_remap_mark(const T* __restrict__ seq, uint64_t n, uint64_t sigma, uint32_t* __restrict__ present,
+__global__ void k_remap_mark(const T* __restrict__ seq, uint64_t n, uint64_t sigma, uint32_t* present,
                              int32_t* __restrict__ flag) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t s = (uint64_t)seq[j];
@@ -228,7 +223,9 @@ __global__ void k_remap_mark(const T* __restrict__ seq, uint64_t n, uint64_t sig
     }
     const uint32_t bit = 1u << (s & 31);
     uint32_t* w = present + (s >> 5);
-    if (!(__ldg(w) & bit)) atomicOr(w, bit);  // (the read skips the atomic for repeats)
+    // (a coherent relaxed read -- other threads OR into `present` during this
+    // kernel, so no read-only-cache load -- skips the atomic for repeats)
+    if (!(ld_relaxed_u32(w) & bit)) atomicOr(w, bit);
   }
 }
 struct OpPopPrefix {  // rank of the first value of word w = set bits of the words before w

@@ -299,7 +299,8 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
     const uint32_t mypre = prep & 0xffffu, hpre = prep >> 16;
     const uint32_t tot = totp & 0xffffu, nseg = (totp >> 16) + 1;
     if ((i0 & 511u) == 0 && T0 + i0 < n32) sb[(T0 + i0) >> 9] = P + mypre;
-    if (lane == 0 && T0 + TILE >= n32) sb[nsb - 1] = P + tot;
+    // (the last tile by index: T0 + TILE can wrap to 0 when n is within a tile of 2^32)
+    if (lane == 0 && tile + 1 == ntiles) sb[nsb - 1] = P + tot;
     if (!SCATTER) {
       __syncwarp();  // every read of this buffer is done
       if (lane == 0) issue(it + NB);

@@ -1,4 +1,4 @@
-// wt_hist.cuh -- a1: the one pass over S before the level passes.
+// wt_prologue.cuh -- a1: the one pass over S before the level passes.
 //
 // Alg. 1 counts symbols per level node (lines 5-6) before each
 // level's sweep.  Here no full histogram of S is taken: by Proposition 1
