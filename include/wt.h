@@ -89,9 +89,16 @@ typedef struct {
 /*
  * wt_sizes: sizes of every output and of the workspace for a build of n
  * symbols of `width` bytes over [0, sigma).  Pure host arithmetic.
+ * n may exceed 2^32: a build of more than seg_max = 2^31 symbols is
+ * SEGMENTED -- S is cut into k = ceil(n / 2^31) contiguous segments, each built
+ * by the direct launch sequence (all of its in-kernel positions 32-bit), and
+ * the k segment trees are merged into the output with 64-bit positions (the
+ * paper's domain decomposition; its datasets reach
+ * n = 1.46e10).  workspace_bytes then includes the k segment trees
+ * and one segment's build workspace.  (WT_SEG_MAX, read per call, lowers the
+ * segment length for tests: a multiple of 4096 in [4096, 2^31].)
  * Errors: WT_ERR_ARG if width not in {1,2,4}, sigma == 0,
- * sigma > 2^(8*width), L > 30, n >= 2^32 (node counts are 32-bit), or
- * out == NULL.
+ * sigma > 2^(8*width), L > 30, n > 32 * seg_max, or out == NULL.
  */
 wt_status wt_sizes(uint64_t n, uint64_t sigma, uint32_t width, wt_sizes_t* out);
 
@@ -193,7 +200,8 @@ wt_status wt_select(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uin
  * (L * n / 8 bytes); like the paper's rank/select structures it is not part
  * of the tree construction.  d_samples: caller-owned device memory of
  * wt_select_index_entries(n, sigma) uint32.  Asynchronous.
- * Errors: WT_ERR_ARG (NULL pointers, bad sigma), WT_ERR_CUDA.
+ * Errors: WT_ERR_ARG (NULL pointers, bad sigma, n >= 2^32: the samples are
+ * 32-bit positions), WT_ERR_CUDA.
  */
 uint64_t wt_select_index_entries(uint64_t n, uint64_t sigma);
 wt_status wt_select_index(const wt_tree_t* tree, uint64_t n, uint64_t sigma, uint32_t* d_samples,
@@ -254,20 +262,75 @@ wt_status wt_remap_alphabet(const void* d_seq, uint64_t n, uint64_t sigma, uint3
                             size_t workspace_bytes, int32_t* d_status, wt_stream_t stream);
 
 /*
- * Domain-decomposition merge (NEXT-3 on one GPU; the paper's dd, P:633-687,
- * 773-822): the trees of k <= 8 contiguous segments of S (built with
- * wt_build_async over the same sigma; segs[g] device pointers, seg_n[g]
- * their lengths) are merged into the tree of the whole sequence: node v of
- * every level holds segment 0's run of v, then segment 1's, ...; C is the sum
- * of the segments' node offsets; superblocks are recomputed.  This is the
- * merge step a multi-GPU or out-of-core build needs (segments built where the
- * data is, then concatenated).  d_scratch: wt_dd_merge_scratch_bytes(n) bytes
- * of device memory, n = sum seg_n.  Asynchronous.
- * Errors: WT_ERR_ARG (k = 0 or > 8, NULL pointers, n >= 2^32), WT_ERR_WORKSPACE.
+ * Domain decomposition (NEXT-3; the paper's dd).  S is cut
+ * into k <= 32 contiguous segments, each built on its own (the partial trees of
+ * createPartialBA) -- on one GPU, or one segment per GPU -- and the
+ * tree of the whole sequence is their merge (mergeBA): C is the sum
+ * of the segments' node offsets, and node v of every level holds segment 0's
+ * run of v, then segment 1's, ... (the per-level prefix over segments of
+ * Alg. 2 lines 7-8).  All positions are 64-bit (n may be >= 2^32).
+ *
+ * wt_dd_merge: the whole merge on one device.  segs[g]: device trees of
+ * seg_n[g] symbols over the same sigma; out: a tree of n = sum seg_n symbols.
+ * d_scratch: wt_dd_merge_scratch_bytes(n).  Asynchronous.
+ * Errors: WT_ERR_ARG (k = 0 or > 32, NULL pointers), WT_ERR_WORKSPACE.
  */
 size_t wt_dd_merge_scratch_bytes(uint64_t n);
 wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, uint64_t sigma,
                       const wt_tree_t* out, void* d_scratch, size_t scratch_bytes, wt_stream_t stream);
+
+/*
+ * The merge's building blocks, for a merge whose output is split into `parts`
+ * (one per GPU: each rank merges and owns one part):
+ *
+ * wt_dd_part_blocks: part p of a merged tree of n symbols owns the 512-bit
+ *   blocks [*block_begin, *block_end) -- bitmap words [16 b, 16 e), merged
+ *   positions [min(n, 512 b), min(n, 512 e)), superblock entries [b, e]
+ *   (e - b + 1 entries; the last equals the next part's first).  Parts get
+ *   ceil(ceil(n/512) / parts) blocks each, the trailing ones fewer (or none).
+ * wt_dd_offsets: d_offsets[i] = sum_g d_seg_offsets[g][i], i <= 2^L (the
+ *   merged node offsets C).  d_seg_offsets: HOST array of k device pointers.
+ * wt_dd_plan (host arithmetic on HOST arrays h_seg_offsets[g][0..2^L]) and
+ * wt_dd_plan_async (the same arithmetic in a kernel, DEVICE arrays; n = the
+ *   merged length): for level l < L, part p < parts, segment g < k,
+ *     plan[((l * parts + p) * k + g) * 2 + 0] = lo, [... + 1] = hi
+ *   where [lo, hi) are the positions of segment g's level-l bitmap whose
+ *   merged positions fall in part p (a contiguous range: inside a segment the
+ *   nodes are in order, and so are they in the merge).  lo counts the
+ *   segment-g bits whose merged position is before the part: by node offsets
+ *   alone (binary search for the node holding the part's first position).
+ * wt_dd_merge_level: level `level` of the merge over merged words
+ *   [word_begin, word_end) into d_out[0 .. word_end - word_begin).  Segment g's
+ *   local bit q of that level is bit (q - src_base[g]) of the words at
+ *   d_src_bits[g] (HOST arrays of k entries; src_base multiples of 32, NULL =
+ *   all 0); the merge reads exactly the bits the plan assigns to the range,
+ *   i.e. words [lo/32, ceil(hi/32)) relative to src_base.  d_seg_offsets,
+ *   d_offsets as above.  Words past n are written as zeros.
+ * wt_superblocks: superblocks of nblocks 512-bit blocks of d_bits plus the
+ *   final total: d_sb[t] = base + ones in blocks [0, t), t <= nblocks.  One
+ *   decoupled-look-back scan; d_scratch: wt_superblocks_scratch_bytes(nblocks).
+ * wt_rank1: d_out[j] = ones of level d_level[j] before position d_pos[j]
+ *   (d_pos[j] <= n) of a finished tree (the base of a part's superblocks is the
+ *   sum over segments of rank1 at the plan's lo).
+ * All asynchronous on `stream` except wt_dd_plan and wt_dd_part_blocks.
+ * Errors: WT_ERR_ARG (k = 0 or > 32, NULL pointers, bad ranges), WT_ERR_WORKSPACE.
+ */
+void wt_dd_part_blocks(uint64_t n, uint64_t parts, uint64_t part, uint64_t* block_begin, uint64_t* block_end);
+wt_status wt_dd_offsets(uint32_t k, const uint64_t* const* d_seg_offsets, uint64_t sigma, uint64_t* d_offsets,
+                        wt_stream_t stream);
+wt_status wt_dd_plan(uint32_t k, const uint64_t* const* h_seg_offsets, uint64_t sigma, uint64_t parts,
+                     uint64_t* h_plan);
+wt_status wt_dd_plan_async(uint32_t k, const uint64_t* const* d_seg_offsets, uint64_t sigma, uint64_t n,
+                           uint64_t parts, uint64_t* d_plan, wt_stream_t stream);
+wt_status wt_dd_merge_level(uint32_t k, const uint64_t* const* d_seg_offsets, const uint64_t* d_offsets,
+                            uint64_t sigma, uint64_t n, uint32_t level, const uint32_t* const* d_src_bits,
+                            const uint64_t* src_base, uint64_t word_begin, uint64_t word_end, uint32_t* d_out,
+                            wt_stream_t stream);
+size_t wt_superblocks_scratch_bytes(uint64_t nblocks);
+wt_status wt_superblocks(const uint32_t* d_bits, uint64_t nblocks, uint64_t base, uint64_t* d_sb, void* d_scratch,
+                         size_t scratch_bytes, wt_stream_t stream);
+wt_status wt_rank1(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint32_t* d_level, const uint64_t* d_pos,
+                   uint64_t m, uint64_t* d_out, wt_stream_t stream);
 
 /* Kernel launches one wt_build_async(n, sigma, width) enqueues, and their kinds
  * (kinds may be NULL): 1 pass over S (prologue), 2 scan of node_offsets
@@ -278,6 +341,9 @@ wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, 
  * and the zeroing of the node counts the pass fills -- and of B_{L-1} before
  * pass 8), 12 final scans (superblocks of level L-1 straight from its bitmap,
  * node_offsets).
+ * A segmented build (n > seg_max) lists each segment's launches, then
+ * 13 the merged node offsets, per level 14 the level merge and 15 its
+ * superblock scan, and 16 the OR of the segments' range flags.
  * Kinds 3, 6, 7, 9, 10 are retired (folded into 11 and 12). */
 uint32_t wt_launch_plan(uint64_t n, uint64_t sigma, uint32_t width, uint32_t* kinds, uint32_t cap);
 

@@ -31,7 +31,8 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 WT_OK, WT_ERR_ARG, WT_ERR_SYMBOL_RANGE, WT_ERR_INDEX, WT_ERR_CUDA, WT_ERR_WORKSPACE = range(6)
 KIND_NAMES = {1: "prologue", 2: "scan", 3: "tables", 4: "level", 5: "last_level", 6: "tile_scan", 7: "memset",
-              8: "pair", 9: "sb_scan", 10: "block_pop", 11: "prep", 12: "final_scan"}
+              8: "pair", 9: "sb_scan", 10: "block_pop", 11: "prep", 12: "final_scan", 13: "dd_offsets",
+              14: "dd_merge", 15: "dd_superblocks", 16: "flags"}
 
 
 class WtSizes(ctypes.Structure):
@@ -73,6 +74,16 @@ _lib.wt_matrix_rank.argtypes = [ctypes.POINTER(WtMatrix), _u64, _u64, _vp, _vp, 
 _lib.wt_dd_merge_scratch_bytes.argtypes = [_u64]
 _lib.wt_dd_merge_scratch_bytes.restype = _sz
 _lib.wt_dd_merge.argtypes = [_u32, _vp, _vp, _u64, ctypes.POINTER(WtTree), _vp, _sz, _vp]
+_lib.wt_dd_part_blocks.argtypes = [_u64, _u64, _u64, _vp, _vp]
+_lib.wt_dd_part_blocks.restype = None
+_lib.wt_dd_offsets.argtypes = [_u32, _vp, _u64, _vp, _vp]
+_lib.wt_dd_plan.argtypes = [_u32, _vp, _u64, _u64, _vp]
+_lib.wt_dd_plan_async.argtypes = [_u32, _vp, _u64, _u64, _u64, _vp, _vp]
+_lib.wt_dd_merge_level.argtypes = [_u32, _vp, _vp, _u64, _u64, _u32, _vp, _vp, _u64, _u64, _vp, _vp]
+_lib.wt_superblocks_scratch_bytes.argtypes = [_u64]
+_lib.wt_superblocks_scratch_bytes.restype = _sz
+_lib.wt_superblocks.argtypes = [_vp, _u64, _u64, _vp, _vp, _sz, _vp]
+_lib.wt_rank1.argtypes = [ctypes.POINTER(WtTree), _u64, _u64, _vp, _vp, _u64, _vp, _vp]
 _lib.wt_remap_workspace_bytes.argtypes = [_u64]
 _lib.wt_remap_workspace_bytes.restype = _sz
 _lib.wt_remap_alphabet.argtypes = [_vp, _u64, _u64, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _vp]
@@ -93,13 +104,16 @@ _lib.wt_last_error.restype = ctypes.c_char_p
 for _f in (_lib.wt_sizes, _lib.wt_build_async, _lib.wt_build, _lib.wt_build_from_host,
            _lib.wt_build_from_host_async, _lib.wt_access, _lib.wt_rank, _lib.wt_select, _lib.wt_select_index,
            _lib.wt_select_indexed, _lib.wt_matrix_build_async, _lib.wt_matrix_access, _lib.wt_matrix_rank,
-           _lib.wt_remap_alphabet, _lib.wt_dd_merge):
+           _lib.wt_remap_alphabet, _lib.wt_dd_merge, _lib.wt_dd_offsets, _lib.wt_dd_plan, _lib.wt_dd_plan_async,
+           _lib.wt_dd_merge_level, _lib.wt_superblocks, _lib.wt_rank1):
     _f.restype = ctypes.c_int
 
 EXPORTS = ["wt_sizes", "wt_build_async", "wt_build", "wt_build_from_host", "wt_build_from_host_async",
            "wt_access", "wt_rank", "wt_select_index_entries", "wt_select_index", "wt_select_indexed",
            "wt_matrix_build_async", "wt_matrix_access", "wt_matrix_rank", "wt_remap_workspace_bytes",
-           "wt_remap_alphabet", "wt_dd_merge_scratch_bytes", "wt_dd_merge",
+           "wt_remap_alphabet", "wt_dd_merge_scratch_bytes", "wt_dd_merge", "wt_dd_part_blocks", "wt_dd_offsets",
+           "wt_dd_plan", "wt_dd_plan_async", "wt_dd_merge_level", "wt_superblocks_scratch_bytes", "wt_superblocks",
+           "wt_rank1",
            "wt_select", "wt_launch_plan", "wt_debug_offsets", "wt_set_profile_events", "wt_status_string",
            "wt_last_error"]
 
@@ -509,12 +523,19 @@ def remap_alphabet(seq: torch.Tensor, sigma: int, stream=None):
 # ---------------------------------------------------------------- domain decomposition (NEXT-3)
 
 
+DD_MAX_SEGMENTS = 32
+
+
+def _ptr_array(ptrs):
+    return (ctypes.c_void_p * len(ptrs))(*ptrs)
+
+
 def dd_merge(segments: list, sigma: int, stream=None) -> WaveletTree:
-    """wt_dd_merge: the tree of the concatenation of k <= 8 segment trees (each a
+    """wt_dd_merge: the tree of the concatenation of k <= 32 segment trees (each a
     WaveletTree over the same sigma, on the same device)."""
     k = len(segments)
-    if not 1 <= k <= 8:
-        raise ValueError("1..8 segments")
+    if not 1 <= k <= DD_MAX_SEGMENTS:
+        raise ValueError(f"1..{DD_MAX_SEGMENTS} segments")
     n = sum(t.n for t in segments)
     dev = segments[0].node_offsets.device
     w = 4  # (the tree layout does not depend on the symbol width; 4 admits every sigma)
@@ -526,7 +547,7 @@ def dd_merge(segments: list, sigma: int, stream=None) -> WaveletTree:
     st = _lib.wt_dd_merge(k, ctypes.cast(arr, _vp), ctypes.cast(ns, _vp), sigma, ctypes.byref(ct),
                           scratch.data_ptr(), scratch.numel(), _stream_ptr(stream))
     _check(st, "wt_dd_merge")
-    torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+    _sync(stream)
     return out
 
 
@@ -543,3 +564,88 @@ def build_dd(seq: torch.Tensor, sigma: int, k: int) -> WaveletTree:
     segs = [build(seq[cuts[i]:cuts[i + 1]], sigma) for i in range(k)]
     return dd_merge(segs, sigma)
 
+
+# ---------------------------------------------------------------- dd building blocks (multi-GPU merge)
+
+
+def dd_part_blocks(n: int, parts: int, part: int) -> tuple[int, int]:
+    """wt_dd_part_blocks: the 512-bit blocks [b, e) part `part` of `parts` owns."""
+    b, e = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    _lib.wt_dd_part_blocks(n, parts, part, ctypes.byref(b), ctypes.byref(e))
+    return int(b.value), int(e.value)
+
+
+def dd_plan_host(seg_offsets: list, sigma: int, parts: int):
+    """wt_dd_plan on host arrays: seg_offsets[g] = segment g's node offsets (numpy
+    uint64 or int64, 2^L + 1 entries).  Returns an int64 numpy array of shape
+    (L, parts, k, 2): the source range [lo, hi) of segment g's level-l bits that
+    land in part p."""
+    import numpy as np
+    k = len(seg_offsets)
+    L = sizes(1, sigma, 4).levels
+    arrs = [np.ascontiguousarray(np.asarray(c).view(np.uint64)) for c in seg_offsets]
+    ptrs = _ptr_array([a.ctypes.data for a in arrs])
+    plan = np.zeros((L, parts, k, 2), np.uint64)
+    _check(_lib.wt_dd_plan(k, ctypes.cast(ptrs, _vp), sigma, parts, plan.ctypes.data if plan.size else None),
+           "wt_dd_plan")
+    return plan.astype(np.int64)
+
+
+def dd_plan_device(seg_offsets: list, sigma: int, n: int, parts: int, stream=None) -> torch.Tensor:
+    """wt_dd_plan_async: the same plan from device node offsets (a device int64
+    tensor of shape (L, parts, k, 2))."""
+    k = len(seg_offsets)
+    L = sizes(1, sigma, 4).levels
+    dev = seg_offsets[0].device
+    plan = torch.empty((L, parts, k, 2), dtype=torch.int64, device=dev)
+    ptrs = _ptr_array([c.data_ptr() for c in seg_offsets])
+    _check(_lib.wt_dd_plan_async(k, ctypes.cast(ptrs, _vp), sigma, n, parts,
+                                 plan.data_ptr() if plan.numel() else None, _stream_ptr(stream)),
+           "wt_dd_plan_async")
+    return plan
+
+
+def dd_offsets(seg_offsets: list, sigma: int, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """wt_dd_offsets: out = sum of the segments' node offsets (device tensors)."""
+    ptrs = _ptr_array([c.data_ptr() for c in seg_offsets])
+    _check(_lib.wt_dd_offsets(len(seg_offsets), ctypes.cast(ptrs, _vp), sigma, out.data_ptr(), _stream_ptr(stream)),
+           "wt_dd_offsets")
+    return out
+
+
+def dd_merge_level(seg_offsets: list, offsets: torch.Tensor, sigma: int, n: int, level: int, src_bits: list,
+                   src_base: list, word_begin: int, word_end: int, out: torch.Tensor, stream=None):
+    """wt_dd_merge_level: merged words [word_begin, word_end) of `level` into `out`
+    from the segments' source words (src_bits[g]: device tensor whose word j holds
+    segment g's level bits [src_base[g] + 32 j, +32))."""
+    k = len(seg_offsets)
+    offs = _ptr_array([c.data_ptr() for c in seg_offsets])
+    bits = _ptr_array([b.data_ptr() if b.numel() else 0 for b in src_bits])
+    base = (ctypes.c_uint64 * k)(*[int(x) for x in src_base])
+    _check(_lib.wt_dd_merge_level(k, ctypes.cast(offs, _vp), offsets.data_ptr(), sigma, n, level,
+                                  ctypes.cast(bits, _vp), ctypes.cast(base, _vp), word_begin, word_end,
+                                  out.data_ptr() if out.numel() else None, _stream_ptr(stream)),
+           "wt_dd_merge_level")
+
+
+def superblocks(bits: torch.Tensor, nblocks: int, base: int, out: torch.Tensor, stream=None):
+    """wt_superblocks: out[t] = base + ones in the first t 512-bit blocks of `bits`, t <= nblocks."""
+    dev = out.device
+    scratch = torch.empty((max(int(_lib.wt_superblocks_scratch_bytes(nblocks)), 256),), dtype=torch.uint8,
+                          device=dev)
+    _keep_for(stream, scratch)
+    _check(_lib.wt_superblocks(bits.data_ptr() if nblocks else None, nblocks, base, out.data_ptr(),
+                               scratch.data_ptr(), scratch.numel(), _stream_ptr(stream)), "wt_superblocks")
+
+
+def rank1(tree: WaveletTree, level: torch.Tensor, pos: torch.Tensor, stream=None) -> torch.Tensor:
+    """wt_rank1: ones of level[j] before pos[j] in a finished tree."""
+    level = level.to(torch.int32).contiguous()
+    pos = pos.to(torch.int64).contiguous()
+    m = pos.numel()
+    out = torch.empty(m, dtype=torch.int64, device=pos.device)
+    ct = tree._ctree()
+    _check(_lib.wt_rank1(ctypes.byref(ct), tree.n, tree.sigma, level.data_ptr() if m else None,
+                         pos.data_ptr() if m else None, m, out.data_ptr() if m else None, _stream_ptr(stream)),
+           "wt_rank1")
+    return out

@@ -106,9 +106,86 @@ struct Carve {
   size_t off_pre = 0, off_tab = 0, off_cnt = 0, off_bufA = 0, off_bufB = 0, total = 0;
   // host-API extras (after total)
   size_t off_seq = 0, off_bits = 0, off_sb = 0, off_c = 0, host_total = 0;
+  // segmented build (n > seg_max(): S is cut into k segments, each built with
+  // the direct launch sequence into its own tree, then merged -- the paper's
+  // dd on one GPU; keeps every in-kernel position of the level
+  // passes 32-bit while the tree holds n >= 2^32 symbols)
+  bool seg = false;
+  uint32_t k = 0;
+  uint64_t seg_len = 0;
+  size_t off_flags = 0, off_sc_counters = 0, off_sc_status = 0, off_sc_value = 0, seg_ctrl = 0;
+  size_t off_tree[wt::DD_MAX_SEGMENTS] = {}, off_segws = 0;
+  uint64_t sc_tiles = 0;
 };
 
+// Longest segment of a segmented build (a multiple of 4096 symbols, < 2^32).
+// WT_SEG_MAX overrides it (tests exercise the segmented path at small n).
+uint64_t seg_max() {
+  const char* v = std::getenv("WT_SEG_MAX");
+  if (v && *v) {
+    const uint64_t x = std::strtoull(v, nullptr, 10) / 4096 * 4096;
+    if (x >= 4096 && x <= (1ull << 31)) return x;
+  }
+  return 1ull << 31;
+}
+// per-level sizes of a tree of n symbols
+uint64_t words_of(uint64_t n) { return 16 * ((n + 511) / 512); }
+uint64_t nsb_of(uint64_t n) { return (n + 511) / 512 + 1; }
+size_t tree_bytes(uint64_t n, uint32_t L) {
+  return align_up((size_t)L * words_of(n) * 4) + align_up((size_t)L * nsb_of(n) * 8) +
+         align_up(((1ull << L) + 1) * 8);
+}
+// superblock scans over nblocks blocks: look-back tiles
+uint64_t sb_scan_tiles(uint64_t nblocks) {
+  return std::max<uint64_t>(1, (nblocks + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+}
+
+Carve carve_direct(uint64_t n, uint64_t sigma, uint32_t width);
+
 Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
+  const uint64_t sm = seg_max();
+  if (n <= sm) return carve_direct(n, sigma, width);
+  Carve c;
+  c.seg = true;
+  c.L = levels_of(sigma);
+  c.words = words_of(n);
+  c.nsb = nsb_of(n);
+  c.c_len = (1ull << c.L) + 1;
+  c.seg_len = sm;
+  c.k = (uint32_t)((n + sm - 1) / sm);
+  c.sc_tiles = sb_scan_tiles(c.nsb - 1);
+  size_t o = 0;
+  c.off_flag = o;
+  o += ALIGN;
+  c.off_flags = o;
+  o += align_up(wt::DD_MAX_SEGMENTS * sizeof(int32_t));
+  c.off_sc_counters = o;
+  o += align_up(64 * sizeof(uint32_t));
+  c.off_sc_status = o;
+  o += align_up(c.sc_tiles * sizeof(uint32_t));
+  c.seg_ctrl = o;  // [0, seg_ctrl) zeroed once per build
+  c.off_sc_value = o;
+  o += align_up(2 * c.sc_tiles * sizeof(uint64_t));
+  for (uint32_t g = 0; g < c.k; ++g) {
+    c.off_tree[g] = o;
+    o += tree_bytes(std::min(sm, n - (uint64_t)g * sm), c.L);
+  }
+  c.off_segws = o;
+  o += carve_direct(sm, sigma, width).total;
+  c.total = o;
+  c.off_seq = o;
+  o += align_up(n * width);
+  c.off_bits = o;
+  o += align_up((size_t)c.L * c.words * 4);
+  c.off_sb = o;
+  o += align_up((size_t)c.L * c.nsb * 8);
+  c.off_c = o;
+  o += align_up(c.c_len * 8);
+  c.host_total = o;
+  return c;
+}
+
+Carve carve_direct(uint64_t n, uint64_t sigma, uint32_t width) {
   Carve c;
   c.L = levels_of(sigma);
   c.words = 16 * ((n + 511) / 512);
@@ -170,7 +247,7 @@ wt_status check_args(uint64_t n, uint64_t sigma, uint32_t width) {
   if (sigma == 0) return fail(WT_ERR_ARG, "sigma must be >= 1");
   if (sigma > (1ull << (8 * width))) return fail(WT_ERR_ARG, "sigma exceeds the symbol width");
   if (levels_of(sigma) > 30) return fail(WT_ERR_ARG, "more than 30 levels");
-  if (n >= (1ull << 32)) return fail(WT_ERR_ARG, "n must be < 2^32 (32-bit node counts)");
+  if (n > (uint64_t)wt::DD_MAX_SEGMENTS * seg_max()) return fail(WT_ERR_ARG, "n exceeds 32 segments of seg_max()");
   return WT_OK;
 }
 
@@ -240,14 +317,15 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), uint32_t grid, uint32_t block, si
 
 enum Kind : uint32_t {
   K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7, K_PAIR = 8, K_SBSCAN = 9,
-  K_PREP = 11, K_FINAL = 12
+  K_PREP = 11, K_FINAL = 12, K_DD_OFFSETS = 13, K_DD_MERGE = 14, K_DD_SB = 15, K_FLAGS = 16
 };
 
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
 template <typename T>
 wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out, char* ws, const Carve& c,
-                  cudaStream_t stream, uint32_t* kinds, uint32_t cap, uint32_t* count,
+                  Launcher& lk, uint32_t* kinds, uint32_t cap, uint32_t* count,
                   unsigned long long* mzeros = nullptr) {
+  const cudaStream_t stream = lk.s;
   // mzeros != nullptr: the wavelet matrix (NEXT-4): every level one global
   // node, per-level zeros to mzeros[l], no node offsets
   const bool matrix = mzeros != nullptr;
@@ -272,7 +350,6 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   T* buf[2] = {reinterpret_cast<T*>(ws + c.off_bufA), reinterpret_cast<T*>(ws + c.off_bufB)};
   unsigned long long* C = (dry || matrix) ? nullptr : reinterpret_cast<unsigned long long*>(out->node_offsets);
   const uint32_t L = c.L;
-  Launcher lk{stream};
   cudaError_t e;
 
   if (!dry) {
@@ -463,15 +540,128 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   return WT_OK;
 }
 
-wt_status dispatch(const void* seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* out, char* ws,
-                   const Carve& c, cudaStream_t stream, uint32_t* kinds, uint32_t cap, uint32_t* count,
-                   unsigned long long* mzeros = nullptr) {
+wt_status dispatch_direct(const void* seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* out,
+                          char* ws, const Carve& c, Launcher& lk, uint32_t* kinds, uint32_t cap, uint32_t* count,
+                          unsigned long long* mzeros = nullptr) {
   switch (width) {
-    case 1: return enqueue<uint8_t>((const uint8_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count, mzeros);
-    case 2: return enqueue<uint16_t>((const uint16_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count, mzeros);
+    case 1: return enqueue<uint8_t>((const uint8_t*)seq, n, sigma, out, ws, c, lk, kinds, cap, count, mzeros);
+    case 2: return enqueue<uint16_t>((const uint16_t*)seq, n, sigma, out, ws, c, lk, kinds, cap, count, mzeros);
     default:
-      return enqueue<uint32_t>((const uint32_t*)seq, n, sigma, out, ws, c, stream, kinds, cap, count, mzeros);
+      return enqueue<uint32_t>((const uint32_t*)seq, n, sigma, out, ws, c, lk, kinds, cap, count, mzeros);
   }
+}
+
+// One level of a dd merge over the word range [w_begin, w_end) of the merged
+// level bitmap (into out[0 ..)), and the segments' node offsets / sources.
+cudaError_t launch_merge_level(const wt::DdOffsets& sg, const wt::DdLevelSrc& src, uint32_t l,
+                               const unsigned long long* C, uint64_t n, uint64_t w_begin, uint64_t w_end,
+                               uint32_t* out, cudaStream_t s) {
+  if (w_end <= w_begin) return cudaSuccess;
+  const uint64_t threads = (w_end - w_begin + wt::DD_WPT - 1) / wt::DD_WPT;
+  wt::k_dd_merge_level<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(sg, src, l, C, n, w_begin, w_end, out);
+  return cudaGetLastError();
+}
+
+// superblocks of nblocks 512-bit blocks of `bits` (plus the final total), each
+// offset by `base`: one decoupled-look-back scan launch (counter + status
+// zeroed by the caller, epoch distinguishes launches sharing them)
+cudaError_t launch_superblocks(const uint32_t* bits, uint64_t nblocks, uint64_t base, unsigned long long* sb,
+                               const wt::LookbackState& lb, uint32_t* counter, uint32_t epoch, const int32_t* noflag,
+                               cudaStream_t s) {
+  if (nblocks == 0) {  // one entry: the base
+    wt::k_set_u64<<<1, 32, 0, s>>>(sb, base);
+    return cudaGetLastError();
+  }
+  const uint32_t tiles = (uint32_t)((nblocks + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+  wt::k_scan<wt::OpBitsPop><<<tiles, wt::SCAN_THREADS, 0, s>>>(wt::OpBitsPop{bits, sb, nblocks, base}, nblocks, lb,
+                                                               counter, epoch, noflag);
+  return cudaGetLastError();
+}
+
+// A segmented build (c.seg): every segment with the direct launch sequence
+// into its own tree (the segment workspace reused), the segments' range flags
+// kept, then the merge: C = sum of the segments' C, every level's node runs
+// concatenated (k_dd_merge_level), superblocks rescanned, flags OR-ed.
+wt_status dispatch_segmented(const void* seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* out,
+                             char* ws, const Carve& c, Launcher& lk, uint32_t* kinds, uint32_t cap,
+                             uint32_t* count) {
+  const bool dry = (seq == nullptr && out == nullptr);
+  const cudaStream_t s = lk.s;
+  uint32_t nk = 0;
+  auto note = [&](uint32_t kind) {
+    if (kinds && nk < cap) kinds[nk] = kind;
+    ++nk;
+  };
+  cudaError_t e;
+  int32_t* flags = dry ? nullptr : reinterpret_cast<int32_t*>(ws + c.off_flags);
+  if (!dry && (e = cudaMemsetAsync(ws, 0, c.seg_ctrl, s)) != cudaSuccess) return fail_cuda(e, "memset seg ctrl");
+  wt::DdOffsets sg{};
+  sg.k = c.k;
+  sg.L = c.L;
+  wt_tree_t segt[wt::DD_MAX_SEGMENTS];
+  uint64_t segn[wt::DD_MAX_SEGMENTS];
+  for (uint32_t g = 0; g < c.k; ++g) {
+    segn[g] = std::min(c.seg_len, n - (uint64_t)g * c.seg_len);
+    char* t = ws + c.off_tree[g];
+    segt[g].bitmaps = reinterpret_cast<uint32_t*>(t);
+    segt[g].superblocks = reinterpret_cast<uint64_t*>(t + align_up((size_t)c.L * words_of(segn[g]) * 4));
+    segt[g].node_offsets = reinterpret_cast<uint64_t*>(t + align_up((size_t)c.L * words_of(segn[g]) * 4) +
+                                                       align_up((size_t)c.L * nsb_of(segn[g]) * 8));
+    sg.C[g] = reinterpret_cast<const unsigned long long*>(segt[g].node_offsets);
+    const Carve cg = carve_direct(segn[g], sigma, width);
+    const void* sq = dry ? nullptr : static_cast<const char*>(seq) + (uint64_t)g * c.seg_len * width;
+    uint32_t sub = 0;
+    wt_status st = dispatch_direct(sq, segn[g], sigma, width, dry ? nullptr : &segt[g], ws + c.off_segws, cg, lk,
+                                   kinds ? kinds + std::min(nk, cap) : nullptr, cap > nk ? cap - nk : 0, &sub);
+    if (st != WT_OK) return st;
+    nk += sub;
+    if (!dry && (e = cudaMemcpyAsync(flags + g, ws + c.off_segws + cg.off_flag, 4, cudaMemcpyDeviceToDevice, s)) !=
+                    cudaSuccess)
+      return fail_cuda(e, "segment flag");
+  }
+  unsigned long long* C = dry ? nullptr : reinterpret_cast<unsigned long long*>(out->node_offsets);
+  note(K_DD_OFFSETS);
+  if (!dry) {
+    if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    wt::k_dd_sum_offsets<<<(uint32_t)std::min<uint64_t>((c.c_len + 255) / 256, 4ull * num_sms()), 256, 0, s>>>(
+        sg, c.c_len, C);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_dd_sum_offsets");
+    if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+  }
+  const wt::LookbackState lb{reinterpret_cast<uint32_t*>(ws + c.off_sc_status),
+                             reinterpret_cast<uint64_t*>(ws + c.off_sc_value), c.sc_tiles};
+  uint32_t* counters = reinterpret_cast<uint32_t*>(ws + c.off_sc_counters);
+  const int32_t* noflag = reinterpret_cast<const int32_t*>(ws + c.off_sc_counters + 63 * sizeof(uint32_t));
+  for (uint32_t l = 0; l < c.L; ++l) {
+    note(K_DD_MERGE);
+    note(K_DD_SB);
+    if (dry) continue;
+    wt::DdLevelSrc src{};
+    for (uint32_t g = 0; g < c.k; ++g) src.bits[g] = segt[g].bitmaps + (uint64_t)l * words_of(segn[g]);
+    uint32_t* ob = out->bitmaps + (uint64_t)l * c.words;
+    if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    if ((e = launch_merge_level(sg, src, l, C, n, 0, c.words, ob, s)) != cudaSuccess)
+      return fail_cuda(e, "k_dd_merge_level");
+    if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    unsigned long long* sbl = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
+    if ((e = launch_superblocks(ob, c.nsb - 1, 0, sbl, lb, counters + l, l + 1, noflag, s)) != cudaSuccess)
+      return fail_cuda(e, "superblock scan");
+    if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+  }
+  note(K_FLAGS);
+  if (!dry) {
+    wt::k_or_flags<<<1, 32, 0, s>>>(flags, c.k, reinterpret_cast<int32_t*>(ws + c.off_flag));
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_or_flags");
+  }
+  if (count) *count = nk;
+  return WT_OK;
+}
+
+wt_status dispatch(const void* seq, uint64_t n, uint64_t sigma, uint32_t width, const wt_tree_t* out, char* ws,
+                   const Carve& c, Launcher& lk, uint32_t* kinds, uint32_t cap, uint32_t* count) {
+  if (c.seg) return dispatch_segmented(seq, n, sigma, width, out, ws, c, lk, kinds, cap, count);
+  return dispatch_direct(seq, n, sigma, width, out, ws, c, lk, kinds, cap, count);
 }
 
 wt::TreeView view_of(const wt_tree_t* t, uint64_t n, uint64_t sigma) {
@@ -523,7 +713,8 @@ wt_status wt_build_async(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t
     return fail(WT_ERR_ARG, "workspace must be 256-byte aligned");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char* ws = static_cast<char*>(d_workspace);
-  st = dispatch(d_seq, n, sigma, width, out, ws, c, s, nullptr, 0, nullptr);
+  Launcher lk{s};
+  st = dispatch(d_seq, n, sigma, width, out, ws, c, lk, nullptr, 0, nullptr);
   if (st != WT_OK) return st;
   if (d_status) {
     cudaError_t e = cudaMemcpyAsync(d_status, ws + c.off_flag, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
@@ -544,6 +735,7 @@ wt_status wt_matrix_build_async(const void* d_seq, uint64_t n, uint64_t sigma, u
   if (n > 0 && !d_seq) return fail(WT_ERR_ARG, "d_seq is NULL");
   if (n > 0 && (reinterpret_cast<uintptr_t>(d_seq) & 15)) return fail(WT_ERR_ARG, "d_seq must be 16-byte aligned");
   const Carve c = carve(n, sigma, width);
+  if (c.seg) return fail(WT_ERR_ARG, "the wavelet matrix takes n <= seg_max() (2^31)");
   if (!d_workspace || workspace_bytes < c.total) return fail(WT_ERR_WORKSPACE, "workspace too small");
   if (reinterpret_cast<uintptr_t>(d_workspace) & (ALIGN - 1))
     return fail(WT_ERR_ARG, "workspace must be 256-byte aligned");
@@ -552,7 +744,8 @@ wt_status wt_matrix_build_async(const void* d_seq, uint64_t n, uint64_t sigma, u
   wt_tree_t t{out->bitmaps, out->superblocks, nullptr};
   unsigned long long dummy = 0;  // (L = 0: no zeros array; the pointer only marks the matrix mode)
   unsigned long long* z = L ? reinterpret_cast<unsigned long long*>(out->zeros) : &dummy;
-  st = dispatch(d_seq, n, sigma, width, &t, ws, c, s, nullptr, 0, nullptr, z);
+  Launcher lk{s};
+  st = dispatch_direct(d_seq, n, sigma, width, &t, ws, c, lk, nullptr, 0, nullptr, z);
   if (st != WT_OK) return st;
   if (d_status) {
     cudaError_t e = cudaMemcpyAsync(d_status, ws + c.off_flag, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
@@ -625,7 +818,8 @@ wt_status wt_build_from_host_async(const void* h_seq, uint64_t n, uint64_t sigma
   cudaError_t e;
   if (n && (e = cudaMemcpyAsync(ws + c.off_seq, h_seq, n * width, cudaMemcpyHostToDevice, s)) != cudaSuccess)
     return fail_cuda(e, "H2D sequence");
-  st = dispatch(ws + c.off_seq, n, sigma, width, &dtree, ws, c, s, nullptr, 0, nullptr);
+  Launcher lk{s};
+  st = dispatch(ws + c.off_seq, n, sigma, width, &dtree, ws, c, lk, nullptr, 0, nullptr);
   if (st != WT_OK) return st;
   const size_t bb = (size_t)c.L * c.words * 4, sbb = (size_t)c.L * c.nsb * 8, cb = c.c_len * 8;
   if (bb && (e = cudaMemcpyAsync(h_out->bitmaps, dtree.bitmaps, bb, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
@@ -788,10 +982,136 @@ wt_status wt_remap_alphabet(const void* d_seq, uint64_t n, uint64_t sigma, uint3
 }
 
 // ---------------------------------------------------------------- domain decomposition merge (NEXT-3)
-size_t wt_dd_merge_scratch_bytes(uint64_t n) {
-  const uint64_t nsb = (n + 511) / 512 + 1, tiles = std::max<uint64_t>(1, (nsb + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
-  return 3 * ALIGN + align_up(tiles * 4) + align_up(2 * tiles * 8);
+namespace {
+wt_status dd_offsets_of(uint32_t k, const uint64_t* const* seg_offsets, uint64_t sigma, wt::DdOffsets* sg) {
+  if (k == 0 || k > (uint32_t)wt::DD_MAX_SEGMENTS || !seg_offsets) return fail(WT_ERR_ARG, "k must be 1..32");
+  if (sigma == 0 || levels_of(sigma) > 30) return fail(WT_ERR_ARG, "bad sigma");
+  *sg = wt::DdOffsets{};
+  sg->k = k;
+  sg->L = levels_of(sigma);
+  for (uint32_t g = 0; g < k; ++g) {
+    if (!seg_offsets[g]) return fail(WT_ERR_ARG, "NULL segment node offsets");
+    sg->C[g] = reinterpret_cast<const unsigned long long*>(seg_offsets[g]);
+  }
+  return WT_OK;
 }
+struct HostCg {  // host accessor of the segments' node offsets
+  const uint64_t* const* C;
+  __host__ __device__ uint64_t operator()(uint32_t h, uint64_t i) const { return C[h][i]; }
+};
+}  // namespace
+
+void wt_dd_part_blocks(uint64_t n, uint64_t parts, uint64_t part, uint64_t* block_begin, uint64_t* block_end) {
+  uint64_t a = 0, b = 0;
+  if (parts > 0 && part < parts) wt::dd_part_blocks(n, parts, part, &a, &b);
+  if (block_begin) *block_begin = a;
+  if (block_end) *block_end = b;
+}
+
+wt_status wt_dd_plan(uint32_t k, const uint64_t* const* h_seg_offsets, uint64_t sigma, uint64_t parts,
+                     uint64_t* h_plan) {
+  g_last_error.clear();
+  wt::DdOffsets sg;
+  wt_status st = dd_offsets_of(k, h_seg_offsets, sigma, &sg);
+  if (st != WT_OK) return st;
+  if (parts == 0 || !h_plan) return fail(WT_ERR_ARG, "parts = 0 or NULL plan");
+  const uint32_t L = sg.L;
+  const HostCg cg{h_seg_offsets};
+  uint64_t n = 0;
+  for (uint32_t g = 0; g < k; ++g) n += h_seg_offsets[g][1ull << L];
+  for (uint32_t l = 0; l < L; ++l)
+    for (uint64_t p = 0; p < parts; ++p) {
+      uint64_t b_lo, b_hi;
+      wt::dd_part_blocks(n, parts, p, &b_lo, &b_hi);
+      const uint64_t q_lo = std::min(n, 512 * b_lo), q_hi = std::min(n, 512 * b_hi);
+      for (uint32_t g = 0; g < k; ++g) {
+        uint64_t* e = h_plan + ((l * parts + p) * k + g) * 2;
+        e[0] = wt::dd_src_before(cg, k, L, l, g, q_lo);
+        e[1] = wt::dd_src_before(cg, k, L, l, g, q_hi);
+      }
+    }
+  return WT_OK;
+}
+
+wt_status wt_dd_plan_async(uint32_t k, const uint64_t* const* d_seg_offsets, uint64_t sigma, uint64_t n,
+                           uint64_t parts, uint64_t* d_plan, wt_stream_t stream) {
+  g_last_error.clear();
+  wt::DdOffsets sg;
+  wt_status st = dd_offsets_of(k, d_seg_offsets, sigma, &sg);
+  if (st != WT_OK) return st;
+  if (parts == 0 || !d_plan) return fail(WT_ERR_ARG, "parts = 0 or NULL plan");
+  const uint64_t t = (uint64_t)sg.L * parts * k;
+  if (t == 0) return WT_OK;
+  wt::k_dd_plan<<<(uint32_t)((t + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      sg, n, parts, reinterpret_cast<unsigned long long*>(d_plan));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_dd_plan");
+}
+
+wt_status wt_dd_offsets(uint32_t k, const uint64_t* const* d_seg_offsets, uint64_t sigma, uint64_t* d_offsets,
+                        wt_stream_t stream) {
+  g_last_error.clear();
+  wt::DdOffsets sg;
+  wt_status st = dd_offsets_of(k, d_seg_offsets, sigma, &sg);
+  if (st != WT_OK) return st;
+  if (!d_offsets) return fail(WT_ERR_ARG, "NULL output");
+  const uint64_t clen = (1ull << sg.L) + 1;
+  wt::k_dd_sum_offsets<<<(uint32_t)std::min<uint64_t>((clen + 255) / 256, 4ull * num_sms()), 256, 0,
+                         reinterpret_cast<cudaStream_t>(stream)>>>(
+      sg, clen, reinterpret_cast<unsigned long long*>(d_offsets));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_dd_sum_offsets");
+}
+
+wt_status wt_dd_merge_level(uint32_t k, const uint64_t* const* d_seg_offsets, const uint64_t* d_offsets,
+                            uint64_t sigma, uint64_t n, uint32_t level, const uint32_t* const* d_src_bits,
+                            const uint64_t* src_base, uint64_t word_begin, uint64_t word_end, uint32_t* d_out,
+                            wt_stream_t stream) {
+  g_last_error.clear();
+  wt::DdOffsets sg;
+  wt_status st = dd_offsets_of(k, d_seg_offsets, sigma, &sg);
+  if (st != WT_OK) return st;
+  if (level >= sg.L) return fail(WT_ERR_ARG, "level >= L");
+  if (!d_offsets || !d_src_bits || word_end > words_of(n) || word_begin > word_end)
+    return fail(WT_ERR_ARG, "bad merge arguments");
+  if (word_end > word_begin && !d_out) return fail(WT_ERR_ARG, "NULL output");
+  wt::DdLevelSrc src{};
+  for (uint32_t g = 0; g < k; ++g) {
+    src.bits[g] = d_src_bits[g];
+    src.base[g] = src_base ? src_base[g] : 0;
+    if (src.base[g] & 31) return fail(WT_ERR_ARG, "source base must be a multiple of 32");
+  }
+  cudaError_t e = launch_merge_level(sg, src, level, reinterpret_cast<const unsigned long long*>(d_offsets), n,
+                                     word_begin, word_end, d_out, reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_dd_merge_level");
+}
+
+size_t wt_superblocks_scratch_bytes(uint64_t nblocks) {
+  const uint64_t tiles = sb_scan_tiles(nblocks);
+  return 2 * ALIGN + align_up(tiles * 4) + align_up(2 * tiles * 8);
+}
+
+wt_status wt_superblocks(const uint32_t* d_bits, uint64_t nblocks, uint64_t base, uint64_t* d_sb, void* d_scratch,
+                         size_t scratch_bytes, wt_stream_t stream) {
+  g_last_error.clear();
+  if (!d_sb || (nblocks && !d_bits)) return fail(WT_ERR_ARG, "NULL pointer");
+  if (!d_scratch || scratch_bytes < wt_superblocks_scratch_bytes(nblocks))
+    return fail(WT_ERR_WORKSPACE, "scratch too small");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* sc = static_cast<char*>(d_scratch);
+  const uint64_t tiles = sb_scan_tiles(nblocks);
+  // [0, ALIGN): ticket counter, then a zero word as the (unused) range flag
+  const size_t off_status = 2 * ALIGN, off_value = off_status + align_up(tiles * 4);
+  cudaError_t e = cudaMemsetAsync(sc, 0, off_value, s);
+  if (e != cudaSuccess) return fail_cuda(e, "memset scratch");
+  const wt::LookbackState lb{reinterpret_cast<uint32_t*>(sc + off_status), reinterpret_cast<uint64_t*>(sc + off_value),
+                             tiles};
+  e = launch_superblocks(d_bits, nblocks, base, reinterpret_cast<unsigned long long*>(d_sb), lb,
+                         reinterpret_cast<uint32_t*>(sc), 1, reinterpret_cast<const int32_t*>(sc + ALIGN), s);
+  return e == cudaSuccess ? WT_OK : fail_cuda(e, "superblock scan");
+}
+
+size_t wt_dd_merge_scratch_bytes(uint64_t n) { return wt_superblocks_scratch_bytes((n + 511) / 512); }
 
 wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, uint64_t sigma,
                       const wt_tree_t* out, void* d_scratch, size_t scratch_bytes, wt_stream_t stream) {
@@ -801,55 +1121,42 @@ wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, 
   if (sigma == 0 || levels_of(sigma) > 30) return fail(WT_ERR_ARG, "bad sigma");
   const uint32_t L = levels_of(sigma);
   uint64_t n = 0;
-  wt::DdSegments sg{};
-  sg.k = k;
-  sg.L = L;
+  const uint64_t* offs[wt::DD_MAX_SEGMENTS];
   for (uint32_t g = 0; g < k; ++g) {
     if (!segs[g].node_offsets || (L && seg_n[g] && !segs[g].bitmaps)) return fail(WT_ERR_ARG, "NULL segment tree");
-    sg.bits[g] = segs[g].bitmaps;
-    sg.C[g] = reinterpret_cast<const unsigned long long*>(segs[g].node_offsets);
-    sg.n[g] = seg_n[g];
-    sg.W[g] = 16 * ((seg_n[g] + 511) / 512);
+    offs[g] = segs[g].node_offsets;
     n += seg_n[g];
   }
-  if (n >= (1ull << 32)) return fail(WT_ERR_ARG, "n must be < 2^32");
   if (L && (!out->bitmaps || !out->superblocks)) return fail(WT_ERR_ARG, "NULL output");
   if (!d_scratch || scratch_bytes < wt_dd_merge_scratch_bytes(n)) return fail(WT_ERR_WORKSPACE, "scratch too small");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  unsigned long long* C = reinterpret_cast<unsigned long long*>(out->node_offsets);
-  const uint64_t clen = (1ull << L) + 1;
-  cudaError_t e;
-  wt::k_dd_sum_offsets<<<(uint32_t)std::min<uint64_t>((clen + 255) / 256, 4ull * num_sms()), 256, 0, s>>>(sg, clen, C);
-  if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_dd_sum_offsets");
-  if (L == 0) return WT_OK;
-  const uint64_t W = 16 * ((n + 511) / 512), nsb = (n + 511) / 512 + 1;
-  // scratch: flag, ticket counters (one per level), look-back status/values
-  char* sc = static_cast<char*>(d_scratch);
-  const uint64_t tiles = std::max<uint64_t>(1, (nsb + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
-  int32_t* flag = reinterpret_cast<int32_t*>(sc);
-  uint32_t* counters = reinterpret_cast<uint32_t*>(sc + ALIGN);  // (32 levels * 4 B fit in ALIGN * 2)
-  const size_t off_status = 3 * ALIGN, off_value = off_status + align_up(tiles * 4);
-  if ((e = cudaMemsetAsync(sc, 0, off_value, s)) != cudaSuccess) return fail_cuda(e, "memset scratch");
-  const wt::LookbackState lb{reinterpret_cast<uint32_t*>(sc + off_status), reinterpret_cast<uint64_t*>(sc + off_value),
-                             tiles};
+  wt_status st = wt_dd_offsets(k, offs, sigma, out->node_offsets, stream);
+  if (st != WT_OK) return st;
+  const uint64_t W = words_of(n), nsb = nsb_of(n);
   for (uint32_t l = 0; l < L; ++l) {
-    if (W) {
-      const uint64_t threads = (W + wt::DD_WPT - 1) / wt::DD_WPT;
-      wt::k_dd_merge_level<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(sg, l, C, n, W,
-                                                                          out->bitmaps + (uint64_t)l * W);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_dd_merge_level");
-    }
-    const uint32_t* lb_bits = out->bitmaps + (uint64_t)l * W;
-    unsigned long long* sbl = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * nsb;
-    if (nsb > 1) {
-      wt::k_scan<wt::OpBitsPop><<<(uint32_t)tiles, wt::SCAN_THREADS, 0, s>>>(wt::OpBitsPop{lb_bits, sbl, nsb - 1},
-                                                                         nsb - 1, lb, counters + l, l + 1, flag);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(dd superblocks)");
-    } else if ((e = cudaMemsetAsync(sbl, 0, 8, s)) != cudaSuccess) {
-      return fail_cuda(e, "memset sb");
-    }
+    const uint32_t* src[wt::DD_MAX_SEGMENTS];
+    for (uint32_t g = 0; g < k; ++g) src[g] = segs[g].bitmaps + (uint64_t)l * words_of(seg_n[g]);
+    if ((st = wt_dd_merge_level(k, offs, out->node_offsets, sigma, n, l, src, nullptr, 0, W,
+                                out->bitmaps + (uint64_t)l * W, stream)) != WT_OK)
+      return st;
+    if ((st = wt_superblocks(out->bitmaps + (uint64_t)l * W, nsb - 1, 0, out->superblocks + (uint64_t)l * nsb,
+                             d_scratch, scratch_bytes, stream)) != WT_OK)
+      return st;
   }
   return WT_OK;
+}
+
+wt_status wt_rank1(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint32_t* d_level, const uint64_t* d_pos,
+                   uint64_t m, uint64_t* d_out, wt_stream_t stream) {
+  g_last_error.clear();
+  wt_status st = query_args(tree, n, sigma);
+  if (st != WT_OK) return st;
+  if (m == 0) return WT_OK;
+  if (!d_level || !d_pos || !d_out) return fail(WT_ERR_ARG, "NULL query pointer");
+  wt::k_rank1<<<(uint32_t)((m + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      tree->bitmaps, reinterpret_cast<const unsigned long long*>(tree->superblocks), words_of(n), nsb_of(n), d_level,
+      reinterpret_cast<const unsigned long long*>(d_pos), m, reinterpret_cast<unsigned long long*>(d_out));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_rank1");
 }
 
 uint64_t wt_select_index_entries(uint64_t n, uint64_t sigma) {
@@ -863,6 +1170,7 @@ wt_status wt_select_index(const wt_tree_t* tree, uint64_t n, uint64_t sigma, uin
   wt_status st = query_args(tree, n, sigma);
   if (st != WT_OK) return st;
   const uint32_t L = levels_of(sigma);
+  if (n >= (1ull << 32)) return fail(WT_ERR_ARG, "the select index stores 32-bit positions (n < 2^32)");
   if (L == 0) return WT_OK;
   if (!d_samples) return fail(WT_ERR_ARG, "NULL samples pointer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -888,6 +1196,7 @@ wt_status wt_select_indexed(const wt_tree_t* tree, uint64_t n, uint64_t sigma, c
   if (st != WT_OK) return st;
   if (m == 0) return WT_OK;
   if (!d_c || !d_j || !d_out || (levels_of(sigma) > 0 && !d_samples)) return fail(WT_ERR_ARG, "NULL pointer");
+  if (n >= (1ull << 32)) return fail(WT_ERR_ARG, "the select index stores 32-bit positions (n < 2^32)");
   const uint32_t grid = (uint32_t)((m + 255) / 256);
   wt::k_select<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       view_of(tree, n, sigma), sigma, d_c, d_j, m, reinterpret_cast<unsigned long long*>(d_out), d_status,
@@ -900,7 +1209,8 @@ uint32_t wt_launch_plan(uint64_t n, uint64_t sigma, uint32_t width, uint32_t* ki
   if (check_args(n, sigma, width) != WT_OK) return 0;
   const Carve c = carve(n, sigma, width);
   uint32_t count = 0;
-  dispatch(nullptr, n, sigma, width, nullptr, nullptr, c, nullptr, kinds, cap, &count);
+  Launcher lk{nullptr};
+  dispatch(nullptr, n, sigma, width, nullptr, nullptr, c, lk, kinds, cap, &count);
   return count;
 }
 

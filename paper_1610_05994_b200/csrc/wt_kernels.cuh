@@ -177,10 +177,11 @@ struct OpBitsPop {
   const uint32_t* bits;
   unsigned long long* sb;
   uint64_t nblocks;
+  uint64_t base;  // ones before block 0 (a part of a merged level: the ones of the earlier parts)
   __device__ uint64_t load(uint64_t) const { return 0; }  // (unused: ScanOfBits)
   __device__ void store(uint64_t i, uint64_t excl, uint64_t val) const {
-    sb[i] = excl;
-    if (i + 1 == nblocks) sb[nblocks] = excl + val;
+    sb[i] = base + excl;
+    if (i + 1 == nblocks) sb[nblocks] = base + excl + val;
   }
 };
 template <>
@@ -347,6 +348,17 @@ __device__ __forceinline__ uint64_t rank1(const uint32_t* __restrict__ B,
   return r;
 }
 
+// out[k] = ones of level lv[k] before position pos[k] (pos <= n): bit-level
+// rank of a finished tree (superblock + word popcounts).
+__global__ void k_rank1(const uint32_t* __restrict__ bitmaps, const unsigned long long* __restrict__ sb, uint64_t W,
+                        uint64_t NSB, const uint32_t* __restrict__ lv, const unsigned long long* __restrict__ pos,
+                        uint64_t m, unsigned long long* __restrict__ out) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const uint64_t l = lv[k];
+  out[k] = rank1(bitmaps + l * W, sb + l * NSB, pos[k]);
+}
+
 struct TreeView {
   const uint32_t* bitmaps;
   const unsigned long long* sb;
@@ -459,27 +471,98 @@ __global__ void k_matrix_rank(TreeView t, const unsigned long long* __restrict__
 // concatenated: node v of level l in the merged tree holds segment 0's run of
 // node v, then segment 1's, ... (stability across segments).  With Cg the
 // segments' node offsets and C = sum_g Cg, segment g's run of node v goes to
-//   C[v << (L-l)] + sum_{g' < g} (Cg'[(v+1) << (L-l)] - Cg'[v << (L-l)]).
-// Destination-driven: one thread per DD_WPT consecutive words of the merged
-// level bitmap.  It finds the node v holding its first position (binary search
-// over C's level-l node starts) and the segment run inside v, then walks the
-// runs (v, 0), (v, 1), ..., (v + 1, 0), ... in merged order, funnel-shifting
-// up to 32 source bits at a time into the word it assembles; every word is
-// written once with a plain store (no zero fill, no atomics), words past n are
-// written as zeros.
-constexpr int DD_MAX_SEGMENTS = 8;
-struct DdSegments {
-  const uint32_t* bits[DD_MAX_SEGMENTS];  // level-major bitmaps of each segment
+//   C[v << (L-l)] + sum_{g' < g} (Cg'[(v+1) << (L-l)] - Cg'[v << (L-l)])
+// (the paper's per-level prefix over segments, Alg. 2 lines 7-8).
+// All positions are 64-bit: the merged tree may hold n >= 2^32 symbols.
+constexpr int DD_MAX_SEGMENTS = 32;
+struct DdOffsets {  // the segments' node offsets (device, 2^L + 1 each)
   const unsigned long long* C[DD_MAX_SEGMENTS];
-  uint64_t n[DD_MAX_SEGMENTS], W[DD_MAX_SEGMENTS];
   uint32_t k, L;
 };
+// One level's source bits: segment g's local bit p (of that level) is bit
+// (p - base[g]) of the words at bits[g]; base[g] is a multiple of 32.  (The
+// whole level bitmap of a segment tree: base 0.  A multi-GPU merge: the word
+// range of the segment's bitmap received from its rank.)
+struct DdLevelSrc {
+  const uint32_t* bits[DD_MAX_SEGMENTS];
+  unsigned long long base[DD_MAX_SEGMENTS];
+};
+
+// Number of segment-g bits of level l whose merged position is < p, for
+// p in [0, n]: the node v holding p (the last v with node start <= p), the
+// bits of g in nodes < v, plus g's part of node v before p.  `cg(h, i)` reads
+// segment h's node offset i.  Shared by the host plan (wt_dd_plan) and the
+// device plan kernel -- the same arithmetic on both sides.
+template <class CG>
+__host__ __device__ inline uint64_t dd_src_before(const CG& cg, uint32_t k, uint32_t L, uint32_t l, uint32_t g,
+                                                  uint64_t p) {
+  const uint32_t sh = L - l;
+  auto cum = [&](uint64_t i) {
+    uint64_t s = 0;
+    for (uint32_t h = 0; h < k; ++h) s += cg(h, i);
+    return s;
+  };
+  if (p >= cum(1ull << L)) return cg(g, 1ull << L);
+  uint64_t lo = 0, hi = 1ull << l;  // cum(lo << sh) <= p < cum(hi << sh)
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (cum(mid << sh) <= p) lo = mid;
+    else hi = mid;
+  }
+  uint64_t off = p - cum(lo << sh), before = 0;
+  for (uint32_t h = 0; h < g; ++h) before += cg(h, (lo + 1) << sh) - cg(h, lo << sh);
+  const uint64_t a = cg(g, lo << sh), sz = cg(g, (lo + 1) << sh) - a;
+  const uint64_t in = off > before ? off - before : 0;
+  return a + (in < sz ? in : sz);
+}
+
+// The merged tree's blocks are split into `parts` contiguous ranges of whole
+// 512-bit blocks (one per rank in a multi-GPU merge): part p owns blocks
+// [b_lo, b_hi), i.e. bitmap words [16 b_lo, 16 b_hi) and merged positions
+// [min(n, 512 b_lo), min(n, 512 b_hi)).
+__host__ __device__ inline void dd_part_blocks(uint64_t n, uint64_t parts, uint64_t p, uint64_t* b_lo,
+                                               uint64_t* b_hi) {
+  const uint64_t nblk = (n + 511) / 512, per = (nblk + parts - 1) / parts;
+  *b_lo = p * per < nblk ? p * per : nblk;
+  *b_hi = (p + 1) * per < nblk ? (p + 1) * per : nblk;
+}
+
+struct DevCg {  // device accessor of the segments' node offsets
+  const DdOffsets* sg;
+  __device__ uint64_t operator()(uint32_t h, uint64_t i) const { return sg->C[h][i]; }
+};
+// plan[((l * parts + p) * k + g) * 2 + {0, 1}] = the source range [lo, hi) of
+// segment g's level-l bits that land in part p: one thread per (l, p, g).
+__global__ void k_dd_plan(DdOffsets sg, uint64_t n, uint64_t parts, unsigned long long* __restrict__ plan) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t k = sg.k;
+  if (t >= (uint64_t)sg.L * parts * k) return;
+  const uint32_t g = (uint32_t)(t % k);
+  const uint64_t p = (t / k) % parts;
+  const uint32_t l = (uint32_t)(t / (k * parts));
+  uint64_t b_lo, b_hi;
+  dd_part_blocks(n, parts, p, &b_lo, &b_hi);
+  const uint64_t q_lo = min(n, 512 * b_lo), q_hi = min(n, 512 * b_hi);
+  const DevCg cg{&sg};
+  plan[2 * t] = dd_src_before(cg, sg.k, sg.L, l, g, q_lo);
+  plan[2 * t + 1] = dd_src_before(cg, sg.k, sg.L, l, g, q_hi);
+}
+
+// Destination-driven merge of one level: one thread per DD_WPT consecutive
+// words of the merged bitmap, within the word range [w_begin, w_end) (a part;
+// out[w - w_begin] receives merged word w).  The thread finds the node v
+// holding its first position (binary search over C's level-l node starts) and
+// the segment run inside v, then walks the runs (v, 0), (v, 1), ..., (v + 1, 0),
+// ... in merged order, funnel-shifting up to 32 source bits at a time into the
+// word it assembles; every word is written once with a plain store (no zero
+// fill, no atomics: the paper's concat of bit runs, done from the
+// destination side), words past n as zeros.
 constexpr uint32_t DD_WPT = 8;  // merged words per thread
-__global__ void k_dd_merge_level(DdSegments sg, uint32_t l, const unsigned long long* __restrict__ C, uint64_t n,
-                                 uint64_t W, uint32_t* __restrict__ out_bits) {
-  const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * DD_WPT;
-  if (w0 >= W) return;
-  const uint64_t w1 = min(w0 + DD_WPT, W);
+__global__ void k_dd_merge_level(DdOffsets sg, DdLevelSrc src, uint32_t l, const unsigned long long* __restrict__ C,
+                                 uint64_t n, uint64_t w_begin, uint64_t w_end, uint32_t* __restrict__ out) {
+  const uint64_t w0 = w_begin + ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * DD_WPT;
+  if (w0 >= w_end) return;
+  const uint64_t w1 = min(w0 + DD_WPT, w_end);
   const uint64_t qend = min(32 * w1, n);
   const uint32_t sh = sg.L - l;  // node v of level l spans leaves [v << sh, (v + 1) << sh)
   const uint64_t nodes = 1ull << l;
@@ -512,10 +595,11 @@ __global__ void k_dd_merge_level(DdSegments sg, uint32_t l, const unsigned long 
     for (;;) {
       const uint32_t d = (uint32_t)(q & 31);
       const uint32_t len = (uint32_t)min(min(rem, qend - q), (uint64_t)(32 - d));
-      const uint32_t* src = sg.bits[h] + (uint64_t)l * sg.W[h];
+      const uint32_t* s = src.bits[h];
+      const uint64_t sw = (sp - src.base[h]) >> 5;
       const uint32_t o = (uint32_t)(sp & 31);
-      const uint32_t lo_w = src[sp >> 5];
-      const uint32_t hi_w = (o + len > 32) ? src[(sp >> 5) + 1] : 0u;
+      const uint32_t lo_w = s[sw];
+      const uint32_t hi_w = (o + len > 32) ? s[sw + 1] : 0u;
       uint32_t x = __funnelshift_r(lo_w, hi_w, o);
       if (len < 32) x &= (1u << len) - 1u;
       acc |= x << d;
@@ -523,7 +607,7 @@ __global__ void k_dd_merge_level(DdSegments sg, uint32_t l, const unsigned long 
       sp += len;
       rem -= len;
       if ((q & 31) == 0) {
-        out_bits[(q >> 5) - 1] = acc;
+        out[(q >> 5) - 1 - w_begin] = acc;
         acc = 0;
       }
       if (q >= qend) break;
@@ -541,17 +625,30 @@ __global__ void k_dd_merge_level(DdSegments sg, uint32_t l, const unsigned long 
         if (g == sg.k) enter(v + 1);
       }
     }
-    if (q & 31) out_bits[q >> 5] = acc;  // q == n: the last, partial word
+    if (q & 31) out[(q >> 5) - w_begin] = acc;  // q == n: the last, partial word
   }
-  for (uint64_t w = max(w0, (n + 31) >> 5); w < w1; ++w) out_bits[w] = 0;  // padding past n
+  for (uint64_t w = max(w0, (n + 31) >> 5); w < w1; ++w) out[w - w_begin] = 0;  // padding past n
 }
 
 // C = sum over the segments' node offsets
-__global__ void k_dd_sum_offsets(DdSegments sg, uint64_t count, unsigned long long* __restrict__ C) {
+__global__ void k_dd_sum_offsets(DdOffsets sg, uint64_t count, unsigned long long* __restrict__ C) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
     unsigned long long s = 0;
     for (uint32_t g = 0; g < sg.k; ++g) s += sg.C[g][i];
     C[i] = s;
+  }
+}
+
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *p = v;
+}
+
+// the OR of k status words (the segments of a segmented build) into *flag
+__global__ void k_or_flags(const int32_t* __restrict__ flags, uint32_t k, int32_t* __restrict__ flag) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int32_t f = 0;
+    for (uint32_t g = 0; g < k; ++g) f |= flags[g];
+    *flag = f;
   }
 }
 

@@ -61,7 +61,7 @@ def test_sizes(wt):
 
 
 @pytest.mark.parametrize("n,sigma,width", [(10, 4, 3), (10, 0, 1), (10, 257, 1), (10, 1 << 17, 2),
-                                           (10, (1 << 31), 4), (1 << 32, 256, 1)])
+                                           (10, (1 << 31), 4), ((1 << 36) + 1, 256, 1)])
 def test_sizes_rejects_bad_args(wt, n, sigma, width):
     with pytest.raises(wt.WtError) as e:
         wt.sizes(n, sigma, width)
