@@ -341,9 +341,10 @@ wt_status wt_rank1(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint
  * and the zeroing of the node counts the pass fills -- and of B_{L-1} before
  * pass 8), 12 final scans (superblocks of level L-1 straight from its bitmap,
  * node_offsets).
- * A segmented build (n > seg_max) lists each segment's launches, then
- * 13 the merged node offsets, per level 14 the level merge and 15 its
- * superblock scan, and 16 the OR of the segments' range flags.
+ * A segmented build (n > seg_max) lists each segment's launches followed by
+ * 16 (its range flag OR-ed into the build's), then 13 the merged node
+ * offsets and, per level, 14 the level merge and 15 its superblock scan
+ * (the merge kernels do nothing once a range flag is set).
  * Kinds 3, 6, 7, 9, 10 are retired (folded into 11 and 12). */
 uint32_t wt_launch_plan(uint64_t n, uint64_t sigma, uint32_t width, uint32_t* kinds, uint32_t cap);
 

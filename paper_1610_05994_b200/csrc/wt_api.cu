@@ -113,7 +113,7 @@ struct Carve {
   bool seg = false;
   uint32_t k = 0;
   uint64_t seg_len = 0;
-  size_t off_flags = 0, off_sc_counters = 0, off_sc_status = 0, off_sc_value = 0, seg_ctrl = 0;
+  size_t off_sc_counters = 0, off_sc_status = 0, off_sc_value = 0, seg_ctrl = 0;
   size_t off_tree[wt::DD_MAX_SEGMENTS] = {}, off_segws = 0;
   uint64_t sc_tiles = 0;
 };
@@ -157,8 +157,6 @@ Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
   size_t o = 0;
   c.off_flag = o;
   o += ALIGN;
-  c.off_flags = o;
-  o += align_up(wt::DD_MAX_SEGMENTS * sizeof(int32_t));
   c.off_sc_counters = o;
   o += align_up(64 * sizeof(uint32_t));
   c.off_sc_status = o;
@@ -555,10 +553,11 @@ wt_status dispatch_direct(const void* seq, uint64_t n, uint64_t sigma, uint32_t 
 // level bitmap (into out[0 ..)), and the segments' node offsets / sources.
 cudaError_t launch_merge_level(const wt::DdOffsets& sg, const wt::DdLevelSrc& src, uint32_t l,
                                const unsigned long long* C, uint64_t n, uint64_t w_begin, uint64_t w_end,
-                               uint32_t* out, cudaStream_t s) {
+                               uint32_t* out, cudaStream_t s, const int32_t* flag = nullptr) {
   if (w_end <= w_begin) return cudaSuccess;
   const uint64_t threads = (w_end - w_begin + wt::DD_WPT - 1) / wt::DD_WPT;
-  wt::k_dd_merge_level<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(sg, src, l, C, n, w_begin, w_end, out);
+  wt::k_dd_merge_level<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(sg, src, l, C, n, w_begin, w_end, out,
+                                                                         flag);
   return cudaGetLastError();
 }
 
@@ -593,7 +592,7 @@ wt_status dispatch_segmented(const void* seq, uint64_t n, uint64_t sigma, uint32
     ++nk;
   };
   cudaError_t e;
-  int32_t* flags = dry ? nullptr : reinterpret_cast<int32_t*>(ws + c.off_flags);
+  int32_t* const flag = reinterpret_cast<int32_t*>(ws + c.off_flag);  // OR of the segments' range flags
   if (!dry && (e = cudaMemsetAsync(ws, 0, c.seg_ctrl, s)) != cudaSuccess) return fail_cuda(e, "memset seg ctrl");
   wt::DdOffsets sg{};
   sg.k = c.k;
@@ -615,23 +614,24 @@ wt_status dispatch_segmented(const void* seq, uint64_t n, uint64_t sigma, uint32
                                    kinds ? kinds + std::min(nk, cap) : nullptr, cap > nk ? cap - nk : 0, &sub);
     if (st != WT_OK) return st;
     nk += sub;
-    if (!dry && (e = cudaMemcpyAsync(flags + g, ws + c.off_segws + cg.off_flag, 4, cudaMemcpyDeviceToDevice, s)) !=
-                    cudaSuccess)
-      return fail_cuda(e, "segment flag");
+    note(K_FLAGS);
+    if (!dry) {
+      wt::k_or_flag<<<1, 32, 0, s>>>(reinterpret_cast<const int32_t*>(ws + c.off_segws + cg.off_flag), flag);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_or_flag");
+    }
   }
   unsigned long long* C = dry ? nullptr : reinterpret_cast<unsigned long long*>(out->node_offsets);
   note(K_DD_OFFSETS);
   if (!dry) {
     if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
     wt::k_dd_sum_offsets<<<(uint32_t)std::min<uint64_t>((c.c_len + 255) / 256, 4ull * num_sms()), 256, 0, s>>>(
-        sg, c.c_len, C);
+        sg, c.c_len, C, flag);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_dd_sum_offsets");
     if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
   }
   const wt::LookbackState lb{reinterpret_cast<uint32_t*>(ws + c.off_sc_status),
                              reinterpret_cast<uint64_t*>(ws + c.off_sc_value), c.sc_tiles};
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + c.off_sc_counters);
-  const int32_t* noflag = reinterpret_cast<const int32_t*>(ws + c.off_sc_counters + 63 * sizeof(uint32_t));
   for (uint32_t l = 0; l < c.L; ++l) {
     note(K_DD_MERGE);
     note(K_DD_SB);
@@ -640,19 +640,14 @@ wt_status dispatch_segmented(const void* seq, uint64_t n, uint64_t sigma, uint32
     for (uint32_t g = 0; g < c.k; ++g) src.bits[g] = segt[g].bitmaps + (uint64_t)l * words_of(segn[g]);
     uint32_t* ob = out->bitmaps + (uint64_t)l * c.words;
     if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-    if ((e = launch_merge_level(sg, src, l, C, n, 0, c.words, ob, s)) != cudaSuccess)
+    if ((e = launch_merge_level(sg, src, l, C, n, 0, c.words, ob, s, flag)) != cudaSuccess)
       return fail_cuda(e, "k_dd_merge_level");
     if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
     if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
     unsigned long long* sbl = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
-    if ((e = launch_superblocks(ob, c.nsb - 1, 0, sbl, lb, counters + l, l + 1, noflag, s)) != cudaSuccess)
+    if ((e = launch_superblocks(ob, c.nsb - 1, 0, sbl, lb, counters + l, l + 1, flag, s)) != cudaSuccess)
       return fail_cuda(e, "superblock scan");
     if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-  }
-  note(K_FLAGS);
-  if (!dry) {
-    wt::k_or_flags<<<1, 32, 0, s>>>(flags, c.k, reinterpret_cast<int32_t*>(ws + c.off_flag));
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_or_flags");
   }
   if (count) *count = nk;
   return WT_OK;
@@ -1058,7 +1053,7 @@ wt_status wt_dd_offsets(uint32_t k, const uint64_t* const* d_seg_offsets, uint64
   const uint64_t clen = (1ull << sg.L) + 1;
   wt::k_dd_sum_offsets<<<(uint32_t)std::min<uint64_t>((clen + 255) / 256, 4ull * num_sms()), 256, 0,
                          reinterpret_cast<cudaStream_t>(stream)>>>(
-      sg, clen, reinterpret_cast<unsigned long long*>(d_offsets));
+      sg, clen, reinterpret_cast<unsigned long long*>(d_offsets), nullptr);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? WT_OK : fail_cuda(e, "k_dd_sum_offsets");
 }

@@ -558,8 +558,12 @@ __global__ void k_dd_plan(DdOffsets sg, uint64_t n, uint64_t parts, unsigned lon
 // fill, no atomics: the paper's concat of bit runs, done from the
 // destination side), words past n as zeros.
 constexpr uint32_t DD_WPT = 8;  // merged words per thread
+// (flag, optional: a segmented build's range flag; set = the segment trees are
+// unspecified, nothing is merged)
 __global__ void k_dd_merge_level(DdOffsets sg, DdLevelSrc src, uint32_t l, const unsigned long long* __restrict__ C,
-                                 uint64_t n, uint64_t w_begin, uint64_t w_end, uint32_t* __restrict__ out) {
+                                 uint64_t n, uint64_t w_begin, uint64_t w_end, uint32_t* __restrict__ out,
+                                 const int32_t* __restrict__ flag) {
+  if (flag && *flag) return;
   const uint64_t w0 = w_begin + ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * DD_WPT;
   if (w0 >= w_end) return;
   const uint64_t w1 = min(w0 + DD_WPT, w_end);
@@ -631,7 +635,9 @@ __global__ void k_dd_merge_level(DdOffsets sg, DdLevelSrc src, uint32_t l, const
 }
 
 // C = sum over the segments' node offsets
-__global__ void k_dd_sum_offsets(DdOffsets sg, uint64_t count, unsigned long long* __restrict__ C) {
+__global__ void k_dd_sum_offsets(DdOffsets sg, uint64_t count, unsigned long long* __restrict__ C,
+                                 const int32_t* __restrict__ flag) {
+  if (flag && *flag) return;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
     unsigned long long s = 0;
     for (uint32_t g = 0; g < sg.k; ++g) s += sg.C[g][i];
@@ -643,13 +649,9 @@ __global__ void k_set_u64(unsigned long long* p, unsigned long long v) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *p = v;
 }
 
-// the OR of k status words (the segments of a segmented build) into *flag
-__global__ void k_or_flags(const int32_t* __restrict__ flags, uint32_t k, int32_t* __restrict__ flag) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int32_t f = 0;
-    for (uint32_t g = 0; g < k; ++g) f |= flags[g];
-    *flag = f;
-  }
+// *flag |= *seg_flag (a segmented build accumulates its segments' range flags)
+__global__ void k_or_flag(const int32_t* __restrict__ seg_flag, int32_t* __restrict__ flag) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *flag |= *seg_flag;
 }
 
 // Select index (NEXT-1; createRankSelect's select half):

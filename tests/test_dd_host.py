@@ -67,5 +67,5 @@ def test_segmented_sizes_and_plan(wt):
     assert s.workspace_bytes > 2 * n // 8   # three segment trees of two levels
     plan = wt.launch_plan(n, 4, 1)
     seg = ["prologue", "prep", "pair", "final_scan"]
-    assert plan == seg * 3 + ["dd_offsets"] + ["dd_merge", "dd_superblocks"] * 2 + ["flags"]
+    assert plan == (seg + ["flags"]) * 3 + ["dd_offsets"] + ["dd_merge", "dd_superblocks"] * 2
     assert wt.launch_plan(1 << 20, 4, 1) == seg

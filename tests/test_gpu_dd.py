@@ -58,7 +58,7 @@ def small_segments():
 @pytest.mark.parametrize("sigma,n,dtype,kind", [(4, 100_003, None, "uniform"), (256, 50_000, None, "zipf"),
                                                 (1 << 16, 40_961, np.uint16, "runs"),
                                                 (1 << 20, 30_011, np.uint32, "zipf"), (2, 24_577, None, "uniform"),
-                                                (1, 20_000, None, "uniform"), (230, 12_288, None, "sorted")])
+                                                (1, 20_000, None, "uniform"), (230, 12_289, None, "sorted")])
 def test_segmented_build_small(wt, small_segments, sigma, n, dtype, kind):
     S = wt_inputs.random_case(n + sigma, n, sigma, kind, dtype=dtype)
     assert n > small_segments
