@@ -162,7 +162,7 @@ def config_of(cfg: int, world: int = 1) -> dict:
             "width": w, "levels": L,
             "l2": "inputs exceed L2 (n*w >= 256 MiB > 126 MB), no flush" if c["n"] * w > (200 << 20)
             else "inputs fit in L2 (latency config), no flush",
-            "parallelism": "replicas" if world > 1 else "1 GPU"}
+            "parallelism": f"dd x{world}" if world > 1 else "1 GPU"}
 
 
 def oracle_time(cfg: int, n_sample: int, reps: int):
@@ -388,6 +388,97 @@ def e2e_throughput(wt, h_seq, sigma, dev, steps, world):
                    f"{INFLIGHT} streams; single_build_* = one call alone)"}
 
 
+def run_dd(args, wt, rank, world, local, dev):
+    """N > 1: the multi-GPU domain decomposition.
+    Every rank holds one contiguous segment of the job's sequence -- the config's
+    n symbols (its seeded sequence; the job's sequence is the G segments in rank
+    order, G*n symbols) -- and a step is one whole distributed build
+    (paper_1610_05994_b200.dist.build_distributed): the rank's segment build,
+    all-gather of node offsets, plan, NCCL send/recv of the bit words, merge of
+    the rank's part of every level, superblock rescan.  Weak scaling: value =
+    G*n / the slowest rank's device time."""
+    import torch
+    import torch.distributed as dist
+    from paper_1610_05994_b200.dist import build_distributed
+    cfg = args.config
+    S, sigma = wt_inputs.generate(cfg)
+    n, w = S.size, S.dtype.itemsize
+    h_seq = torch.from_numpy(S.view(np.int32) if w == 4 else S)
+    d_seq = h_seq.to(dev)
+    steps = args.steps or {1: 200, 2: 50, 3: 50, 4: 20, 5: 10}[cfg]
+    warmup = max(3, args.warmup)
+    peak, peak_src = measured_peaks()
+    for _ in range(warmup):
+        part = build_distributed(d_seq, sigma)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    with sampler:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            part = build_distributed(d_seq, sigma)
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, world, dev)
+    # the rank's local segment build alone (its kernels and roofline)
+    stream = torch.cuda.Stream(device=dev)
+    L = wt.sizes(n, sigma, w).levels
+    prof = time_builds(wt, d_seq, sigma, stream, min(steps, 20), 1, profile=True)
+    kt = kernel_table(prof, n, w, L, peak)
+    dom = max(kt, key=lambda k: kt[k]["ms_per_step"])
+    avg_launch_ms = kt[dom]["ms_per_step"] / kt[dom]["launches_per_step"]
+    ab = algorithmic_bytes(dom, n, w, L)
+    local_ms = max_over_ranks(prof["ms_per_step"], world, dev)
+    # end to end: H2D of the rank's segment from pinned memory, the distributed
+    # build, D2H of the rank's part of the tree
+    h_pinned = h_seq.pin_memory()
+    h_bits = torch.empty(part.bitmaps.shape, dtype=part.bitmaps.dtype, pin_memory=True)
+    h_sb = torch.empty(part.superblocks.shape, dtype=part.superblocks.dtype, pin_memory=True)
+    e_steps = max(1, min(args.e2e_steps, 5))
+    dist.barrier()
+    torch.cuda.synchronize()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(e_steps):
+        d_in = h_pinned.to(dev, non_blocking=True)
+        part = build_distributed(d_in, sigma)
+        h_bits.copy_(part.bitmaps, non_blocking=True)
+        h_sb.copy_(part.superblocks, non_blocking=True)
+    f1.record()
+    torch.cuda.synchronize()
+    e_ms = max_over_ranks(f0.elapsed_time(f1) / e_steps, world, dev)
+    line = {
+        "metric": METRIC, "value": job_throughput(n, world, ms), "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": DTYPE[w], "data": "synthetic",
+        "config": dict(config_of(cfg, world), parallelism=f"dd x{world} (one segment of n per rank, merged tree "
+                                                            f"of {world}*n symbols sharded by position)"),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": ab / (avg_launch_ms * 1e-3) / 1e9, "peak": peak,
+                     "unit": "GB/s", "frac": ab / (avg_launch_ms * 1e-3) / 1e9 / peak, "traffic": None,
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": ab, "avg_launch_ms": avg_launch_ms,
+                     "scope": "the rank's local segment build"},
+        "dd": {"local_build_ms": local_ms, "exchange_merge_ms": ms - local_ms},
+        "e2e": {"value": job_throughput(n, world, e_ms), "unit": UNIT, "ms_per_step": e_ms,
+                "h2d_bytes_per_step": n * w,
+                "d2h_bytes_per_step": int(h_bits.numel() * 4 + h_sb.numel() * 8),
+                "api": "per rank: H2D of its segment, dist.build_distributed, D2H of its part"},
+        "gpu_launches": None,
+        "clocks": sampler.summary(),
+        "cpu_baseline": None,
+        "kernels": kt,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+        if args.out:
+            with open(args.out, "w") as f:
+                json.dump(line, f, indent=1)
+
+
 def relaunch_under_torchrun(args):
     """`--gpus N` (N > 1) without torchrun: start N ranks ourselves."""
     with socket.socket() as s:
@@ -423,6 +514,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     cfg = args.config
+    if world > 1:
+        run_dd(args, wt, rank, world, local, dev)
+        dist.destroy_process_group()
+        return
     S, sigma = wt_inputs.generate(cfg)
     n = S.size
     w = S.dtype.itemsize
