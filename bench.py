@@ -38,7 +38,7 @@ UNIT = "Gsymbols/s"
 DTYPE = {1: "u8", 2: "u16", 4: "u32"}
 # kernel kinds whose per-launch HBM fraction is a roofline statement (the scans
 # move a few MB and are latency-bound)
-STREAMING_KINDS = ("prologue", "level", "pair", "last_level", "final_scan", "l2_pass", "l2_shift")
+STREAMING_KINDS = ("prologue", "level", "pair", "last_level", "final_scan")
 
 
 def parse(argv=None):
@@ -80,10 +80,6 @@ def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
         return 8 * tiles + (tables + zero) // levels
     if kind == "final_scan":  # last-level superblocks from its bitmap, C from the leaf counts
         return bitmap + 8 * nsb + 4 * (1 << L) + 8 * ((1 << L) + 1)
-    if kind == "l2_pass":     # L = 2 in one pass: read S, write B_0, both runs of B_1 (n bits), SB_0
-        return n * w + 2 * bitmap + 8 * nsb
-    if kind == "l2_shift":    # the ones' run moved behind the zeros': read + write ~O/8 (O ~ n/2 on cfg2)
-        return 2 * ((n // 2 + 7) // 8)
     return 0
 
 

@@ -34,20 +34,6 @@ uint32_t levels_of(uint64_t sigma) {
   return L;
 }
 
-// WT_NO_L2=1 (read per call): build L = 2 trees with the general sequence
-// (pass over S, fused pair pass) instead of the one-pass kernel (A/B, tests)
-bool l2_enabled() {
-  const char* v = std::getenv("WT_NO_L2");
-  return !(v && *v && *v != '0');
-}
-uint64_t l2_tile(uint32_t width) {
-  switch (width) {
-    case 1: return wt::L2Tile<uint8_t>::TS;
-    case 2: return wt::L2Tile<uint16_t>::TS;
-    default: return wt::L2Tile<uint32_t>::TS;
-  }
-}
-
 uint64_t level_tile(uint32_t width) {
   switch (width) {
     case 1: return wt::LvTile<uint8_t>::TILE;
@@ -118,11 +104,6 @@ struct Carve {
   size_t off_flag = 0, off_counters = 0, off_ones0 = 0, off_status = 0, off_value = 0, off_agg = 0, ctrl_bytes = 0;
   size_t off_status2 = 0, off_value2 = 0;  // a second look-back state (two scans per k_prep launch)
   size_t off_pre = 0, off_tab = 0, off_cnt = 0, off_bufA = 0, off_bufB = 0, total = 0;
-  // the one-pass L = 2 build (wt_l2.cuh): leaf counts (in the control block),
-  // the ones' run of level 1, per-tile side words
-  bool l2 = false;
-  uint64_t l2_tiles = 0;
-  size_t off_l2cnt = 0, off_l2ost = 0, off_l2side = 0;
   // host-API extras (after total)
   size_t off_seq = 0, off_bits = 0, off_sb = 0, off_c = 0, host_total = 0;
   // segmented build (n > seg_max(): S is cut into k segments, each built with
@@ -214,10 +195,7 @@ Carve carve_direct(uint64_t n, uint64_t sigma, uint32_t width) {
   c.cnt_entries = c.L >= 2 ? (1ull << c.L) : 0;
   const uint64_t pre_tiles = (c.ntiles + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
   const uint64_t sb_tiles = (c.nsb + wt::SCAN_TILE - 1) / wt::SCAN_TILE;  // last level's superblock scan
-  c.l2 = c.L == 2 && l2_enabled();
-  c.l2_tiles = c.l2 ? (n + l2_tile(width) - 1) / l2_tile(width) : 0;
-  c.status_entries = std::max<uint64_t>(std::max<uint64_t>(1, c.l2_tiles),
-                                        std::max(std::max(pre_tiles, scan_tiles), sb_tiles));
+  c.status_entries = std::max<uint64_t>(1, std::max(std::max(pre_tiles, scan_tiles), sb_tiles));
   size_t o = 0;
   c.off_flag = o;
   o += ALIGN;
@@ -231,8 +209,6 @@ Carve carve_direct(uint64_t n, uint64_t sigma, uint32_t width) {
   o += align_up(c.status_entries * sizeof(uint32_t));
   c.off_agg = o;
   o += align_up((size_t)c.L * c.ntiles * sizeof(uint32_t));
-  c.off_l2cnt = o;
-  o += ALIGN;
   c.ctrl_bytes = o;
   c.off_value = o;  // look-back values: written before their status, never read stale
   o += align_up(2 * c.status_entries * sizeof(uint64_t));
@@ -250,10 +226,6 @@ Carve carve_direct(uint64_t n, uint64_t sigma, uint32_t width) {
   if (c.L >= 3) o += seq_bytes;  // T_1, T_3, ...
   c.off_bufB = o;
   if (c.L >= 4) o += seq_bytes;  // T_2, T_4, ...
-  c.off_l2ost = o;
-  if (c.l2) o += align_up(((n + 31) / 32 + 2) * 4);
-  c.off_l2side = o;
-  if (c.l2) o += align_up(2 * c.l2_tiles * 4);
   c.total = o;
   c.off_seq = o;
   o += seq_bytes;
@@ -343,8 +315,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), uint32_t grid, uint32_t block, si
 
 enum Kind : uint32_t {
   K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7, K_PAIR = 8, K_SBSCAN = 9,
-  K_PREP = 11, K_FINAL = 12, K_DD_OFFSETS = 13, K_DD_MERGE = 14, K_DD_SB = 15, K_FLAGS = 16, K_L2 = 17,
-  K_L2_SIDE = 18, K_L2_SHIFT = 19
+  K_PREP = 11, K_FINAL = 12, K_DD_OFFSETS = 13, K_DD_MERGE = 14, K_DD_SB = 15, K_FLAGS = 16
 };
 
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
@@ -413,10 +384,9 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   };
   wt_status st;
 
-  const bool one_pass_l2 = c.l2 && !matrix;
   // a1: the pass over S: range check, level-0 tile ones agg0, ones0
-  if (!one_pass_l2) note(K_PRO);
-  if (!dry && !one_pass_l2) {
+  note(K_PRO);
+  if (!dry) {
     if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
     const uint64_t tiles = (n + wt::LvTile<T>::TILE - 1) / wt::LvTile<T>::TILE;  // one warp per tile
     const uint32_t grid = (uint32_t)std::max<uint64_t>(
@@ -447,67 +417,6 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     return WT_OK;
   };
   const wt::ZeroFill nozero{nullptr, 0, nullptr, 0};
-
-  if (c.l2 && !matrix) {
-    // L = 2 in one pass over S (wt_l2.cuh): B_0, SB_0, B_1's zeros' run and the
-    // ones' run (to the workspace), leaf counts; then the side words, the ones'
-    // run moved to bit Z of B_1, and the final scan (SB_1 from B_1, C)
-    constexpr uint64_t TS = wt::L2Tile<T>::TS;
-    wt::L2Args la{};
-    if (!dry) {
-      la.B0 = out->bitmaps;
-      la.B1 = out->bitmaps + c.words;
-      la.ost = reinterpret_cast<uint32_t*>(ws + c.off_l2ost);
-      la.SB0 = reinterpret_cast<unsigned long long*>(out->superblocks);
-      la.side = reinterpret_cast<uint32_t*>(ws + c.off_l2side);
-      la.cnt = reinterpret_cast<unsigned long long*>(ws + c.off_l2cnt);
-      la.ticket = counters;
-      la.flag = flag;
-      la.lb = status;
-      la.n = n;
-      la.sigma = sigma;
-      la.ntiles = c.l2_tiles;
-      la.nsb = c.nsb;
-    }
-    note(K_L2);
-    if (!dry) {
-      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      wt::k_l2<T><<<(uint32_t)c.l2_tiles, wt::L2_THREADS, 0, stream>>>(seq, la);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_l2");
-      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-    }
-    note(K_L2_SIDE);
-    if (!dry) {
-      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      e = launch_pdl(wt::k_l2_side<(int)TS>, (uint32_t)((c.l2_tiles + 255) / 256), 256, 0, stream,
-                     (const uint32_t*)la.side, (const unsigned long long*)la.SB0, c.l2_tiles, la.B1, la.ost,
-                     (const int32_t*)flag);
-      if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_l2_side");
-      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-    }
-    note(K_L2_SHIFT);
-    if (!dry) {
-      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      const uint64_t pairs = (c.words + 1) / 2;  // (an upper bound: words from Z/32 on)
-      e = launch_pdl(wt::k_l2_shift, (uint32_t)std::max<uint64_t>(1, (pairs + 255) / 256), 256, 0, stream,
-                     (const uint32_t*)la.ost, (const unsigned long long*)la.SB0, n, c.nsb, c.words, la.B1,
-                     (const int32_t*)flag);
-      if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_l2_shift");
-      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
-    }
-    epoch = 2;    // (the pass used epoch 1 of the status words and ticket counter 0)
-    counter = 1;
-    unsigned long long* const sb1 =
-        dry ? nullptr : reinterpret_cast<unsigned long long*>(out->superblocks) + c.nsb;
-    if ((st = prep(K_FINAL, wt::OpBitsPop{dry ? nullptr : la.B1, sb1, c.nsb - 1, 0}, c.nsb - 1,
-                   wt::OpLeafC{dry ? nullptr : reinterpret_cast<const uint32_t*>(ws + c.off_l2cnt), C, 4, n,
-                               nullptr},
-                   4, wt::ZeroFill{nullptr, 0, nullptr, 0}, "k_prep(final)")) != WT_OK)
-      return st;
-    if (count) *count = nk;
-    return WT_OK;
-  }
-
 
   if (L == 0 && matrix) {  // no levels, nothing but the range check
     if (count) *count = nk;

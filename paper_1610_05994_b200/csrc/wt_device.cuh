@@ -57,16 +57,13 @@ __device__ __forceinline__ void lb_publish(LookbackState lb, uint64_t tile, uint
 // returns the exclusive prefix of all earlier tiles and publishes the
 // inclusive prefix.  Tile ids must be handed out in launch order by an atomic
 // counter (forward progress: every earlier tile is owned by a resident CTA).
-// published = true: the caller already published `aggregate` for `tile`
-// (ST_AGG, or ST_PREFIX for tile 0) and did other work before looking back.
-__device__ __forceinline__ uint64_t lookback(LookbackState lb, uint64_t tile, uint64_t aggregate, uint32_t epoch,
-                                             bool published = false) {
+__device__ __forceinline__ uint64_t lookback(LookbackState lb, uint64_t tile, uint64_t aggregate, uint32_t epoch) {
   const uint32_t lane = threadIdx.x & 31;
   if (tile == 0) {
-    if (lane == 0 && !published) lb_publish(lb, 0, ST_PREFIX, epoch, aggregate);
+    if (lane == 0) lb_publish(lb, 0, ST_PREFIX, epoch, aggregate);
     return 0;
   }
-  if (lane == 0 && !published) lb_publish(lb, tile, ST_AGG, epoch, aggregate);
+  if (lane == 0) lb_publish(lb, tile, ST_AGG, epoch, aggregate);
   uint64_t exclusive = 0;
   int64_t base = (int64_t)tile - 1;
   while (true) {

@@ -14,7 +14,6 @@
 #pragma once
 #include "wt_device.cuh"
 #include "wt_prologue.cuh"
-#include "wt_l2.cuh"
 
 namespace wt {
 

@@ -51,8 +51,7 @@ def test_sizes(wt):
     # two ping-pong permuted copies of the sequence at most (T_1..T_{L-2}), plus
     # node tables, two 2^L uint32 node-count buffers, per-tile and per-block counts
     assert 2 * (1 << 30) <= s.workspace_bytes < 2 * (1 << 30) + 450 * (1 << 20)
-    # L=2: one pass over S, no permuted copy; the ones' run of level 1 (n/8 bytes) in the workspace
-    assert wt.sizes(1 << 20, 4, 1).workspace_bytes < (1 << 20) // 8 + (1 << 16)
+    assert wt.sizes(1 << 20, 4, 1).workspace_bytes < 1 << 20   # L=2: the fused pass writes no permuted copy
     assert wt.sizes(1 << 20, 8, 1).workspace_bytes > 1 << 20   # L=3: T_1
     assert s.host_workspace_bytes > s.workspace_bytes + (1 << 30)
     assert wt.sizes(5, 1, 1).levels == 0
@@ -96,9 +95,7 @@ def test_launch_plan(wt):
     lv = ["prep", "level"]
     pair = ["prep", "pair", "final_scan"]
     assert wt.launch_plan(1 << 20, 256, 1) == ["prologue"] + lv * 6 + pair
-    # L=2: the one-pass kernel (B_0, SB_0, both runs of B_1), the runs' shared
-    # words, the ones' run moved behind the zeros', the final scan
-    assert wt.launch_plan(1 << 20, 4, 1) == ["l2_pass", "l2_side", "l2_shift", "final_scan"]
+    assert wt.launch_plan(1 << 20, 4, 1) == ["prologue"] + pair
     assert wt.launch_plan(1 << 20, 8, 1) == ["prologue"] + lv + pair
     assert wt.launch_plan(100, 2, 1) == ["prologue", "prep", "last_level"]
     assert wt.launch_plan(100, 1, 1) == ["prologue", "scan"]

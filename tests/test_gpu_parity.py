@@ -460,18 +460,19 @@ def test_dd_fig2_segments(wt):
 
 
 
-# ------------------------------------------------------------ L = 2 in one pass (wt_l2.cuh)
+# ------------------------------------------------------------ L = 2 edges
 
 
-L2_TILE = {1: 32768, 2: 16384, 4: 8192}   # symbols per tile of the one-pass L = 2 kernel
+L2_EDGE = {1: 32768, 2: 16384, 4: 8192}   # 32 KiB of symbols: several level tiles
 
 
 @pytest.mark.parametrize("width", [1, 2, 4])
-def test_l2_one_pass_edges(wt, width):
-    # tile boundaries of the one-pass kernel, runs of one value (a level-0 half
-    # empty: Z = 0 or O = 0), and the range check in full and ragged tiles
+def test_l2_edges(wt, width):
+    # two-level trees (sigma 3 / 4: the fused final pair reads S itself) across
+    # many level tiles, runs of one value (a level-0 half empty: Z = 0 or O = 0),
+    # and the range check in full and ragged tiles
     dtype = {1: np.uint8, 2: np.uint16, 4: np.uint32}[width]
-    ts = L2_TILE[width]
+    ts = L2_EDGE[width]
     for n in [1, 31, 33, 511, 513, ts - 1, ts, ts + 1, 2 * ts + 511, 3 * ts + 777, 5 * ts]:
         for sigma in (3, 4):
             S = wt_inputs.random_case(n + sigma, n, sigma, "uniform", dtype=dtype)
@@ -482,7 +483,7 @@ def test_l2_one_pass_edges(wt, width):
         check_case(wt, S, 4, f"l2 pattern {fill}")
     rng = np.random.default_rng(width)
     S = rng.integers(0, 4, 3 * ts + 5).astype(dtype)
-    S[rng.integers(0, S.size, 3000)] = 0          # zeros-heavy region, small one-runs per tile
+    S[rng.integers(0, S.size, 3000)] = 0          # zeros-heavy region
     S[ts: 2 * ts] = 3
     check_case(wt, S, 4, "l2 mixed runs")
     for pos in (0, ts - 1, ts, S.size - 1):
@@ -491,18 +492,3 @@ def test_l2_one_pass_edges(wt, width):
         with pytest.raises(wt.WtError) as e:
             wt.build(to_dev(bad), 4)
         assert e.value.status == wt.WT_ERR_SYMBOL_RANGE
-
-
-@pytest.fixture
-def no_l2():
-    os.environ["WT_NO_L2"] = "1"
-    yield
-    del os.environ["WT_NO_L2"]
-
-
-@pytest.mark.parametrize("sigma,n,dtype", [(4, 300_001, np.uint8), (3, 100_000, np.uint16), (4, 70_001, np.uint32)])
-def test_l2_general_sequence(wt, no_l2, sigma, n, dtype):
-    # WT_NO_L2=1: L = 2 through the general sequence (pass over S, fused pair pass)
-    assert wt.launch_plan(n, sigma, np.dtype(dtype).itemsize)[0] == "prologue"
-    S = wt_inputs.random_case(n, n, sigma, "zipf", dtype=dtype)
-    check_case(wt, S, sigma, f"general l2 n={n}")
