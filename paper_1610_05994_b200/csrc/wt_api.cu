@@ -7,6 +7,8 @@
 #include <mutex>
 #include <string>
 
+#include <cudaTypedefs.h>
+
 #include "wt.h"
 #include "wt_kernels.cuh"
 
@@ -290,6 +292,51 @@ bool pdl_enabled() {
 // The final pair pass writes B_{L-1}'s runs with global OR-reductions when it
 // reads S itself (L = 2, where the pass is ALU-bound);
 // WT_PAIR_RED=0/1 forces it off/on (A/B).
+// The specialised pass for two-level trees of 1-byte symbols (k_pair2);
+// WT_NO_PAIR2=1 (read per call) uses the general fused pair instead (A/B, tests).
+bool pair2_enabled() {
+  const char* v = std::getenv("WT_NO_PAIR2");
+  return !(v && *v && *v != '0');
+}
+cudaError_t pair2_setup(int* blocks_per_sm) {
+  static int bps[MAX_DEVICES] = {};
+  static cudaError_t err[MAX_DEVICES] = {};
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  if (bps[dev] == 0) {
+    int b = 0;
+    cudaError_t e = cudaFuncSetAttribute(wt::k_pair2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)wt::p2_smem_bytes());
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, wt::k_pair2, 32 * wt::P2_WARPS, wt::p2_smem_bytes());
+    err[dev] = e;
+    bps[dev] = b < 1 ? 1 : b;
+  }
+  *blocks_per_sm = bps[dev];
+  return err[dev];
+}
+// S as a 2-D tensor of rows of 128 bytes (floor(n / 128) rows; the kernel
+// copies the partial last row itself), boxes of one 2048-byte tile, 128-byte
+// swizzle.  cuTensorMapEncodeTiled comes from the driver through the
+// runtime's entry-point query (no -lcuda).
+bool rows128_tensor_map(CUtensorMap* map, const void* seq, uint64_t bytes, uint32_t box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode || bytes < 128) return false;
+  const cuuint64_t dims[2] = {128, bytes / 128};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(seq), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 int pair_red_override() {
   static const int v = [] {
     const char* s = std::getenv("WT_PAIR_RED");
@@ -315,7 +362,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), uint32_t grid, uint32_t block, si
 
 enum Kind : uint32_t {
   K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7, K_PAIR = 8, K_SBSCAN = 9,
-  K_PREP = 11, K_FINAL = 12, K_DD_OFFSETS = 13, K_DD_MERGE = 14, K_DD_SB = 15, K_FLAGS = 16
+  K_PREP = 11, K_FINAL = 12, K_DD_OFFSETS = 13, K_DD_MERGE = 14, K_DD_SB = 15, K_FLAGS = 16, K_P2C = 17
 };
 
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
@@ -442,9 +489,28 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   const uint32_t grid_sc = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_sc * (uint64_t)num_sms());
   const uint32_t grid_last = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_last * (uint64_t)num_sms());
   const uint32_t grid_pair = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_pair * (uint64_t)num_sms());
+  // two levels of 1-byte symbols: the specialised pass (wt_pair2.cuh) replaces the fused pair
+  const bool pair2 = (L == 2 && !matrix && sizeof(T) == 1 && n >= 128 && pair2_enabled());
   auto level = [&](uint32_t l, int mode) -> wt_status {
     note(mode == 0 ? K_LAST : mode == 2 ? K_PAIR : K_LEVEL);
     if (dry) return WT_OK;
+    if (mode == 2 && pair2) {
+      int bps = 1;
+      if ((e = pair2_setup(&bps)) != cudaSuccess) return fail_cuda(e, "k_pair2 setup");
+      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      const uint32_t grid = (uint32_t)std::min<uint64_t>((c.ntiles + wt::P2_WARPS - 1) / wt::P2_WARPS,
+                                                         (uint64_t)bps * num_sms());
+      CUtensorMap tmap;
+      if (!rows128_tensor_map(&tmap, seq, n, wt::P2_TILE / 128)) return fail(WT_ERR_CUDA, "cuTensorMapEncodeTiled");
+      e = launch_pdl(wt::k_pair2, grid, (uint32_t)(32 * wt::P2_WARPS), wt::p2_smem_bytes(), stream,
+                     reinterpret_cast<const uint8_t*>(seq), n, (uint32_t)c.ntiles, (const uint32_t*)pre,
+                     (const unsigned long long*)ones0, out->bitmaps,
+                     reinterpret_cast<unsigned long long*>(out->superblocks), c.nsb, out->bitmaps + c.words,
+                     (const int32_t*)flag, tmap);
+      if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_pair2");
+      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      return WT_OK;
+    }
     const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
     T* o = mode == 0 ? nullptr : mode == 2 ? reinterpret_cast<T*>(out->bitmaps + (uint64_t)(L - 1) * c.words)
                                            : buf[l & 1];
@@ -528,6 +594,20 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       if ((st = prep(K_FINAL, wt::OpBitsPopZ{lastbits, sbl, c.nsb - 1, mzeros + (L - 1), n}, c.nsb - 1, wt::OpNone{},
                      0, nozero, "k_prep(final)")) != WT_OK)
         return st;
+    } else if (pair2) {
+      // B_1's superblocks, then C from them (k_pair2 counts no leaves)
+      if ((st = prep(K_FINAL, wt::OpBitsPop{lastbits, sbl, c.nsb - 1}, c.nsb - 1, wt::OpNone{}, 0, nozero,
+                     "k_prep(final)")) != WT_OK)
+        return st;
+      note(K_P2C);
+      if (!dry) {
+        if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+        e = launch_pdl(wt::k_pair2_offsets, 1u, 32u, (size_t)0, stream, (const uint32_t*)lastbits,
+                       (const unsigned long long*)sbl, c.nsb, (const unsigned long long*)ones0, n, C,
+                       (const int32_t*)flag);
+        if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_pair2_offsets");
+        if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      }
     } else if ((st = prep(K_FINAL, wt::OpBitsPop{lastbits, sbl, c.nsb - 1}, c.nsb - 1,
                           wt::OpLeafC{dry ? nullptr : cnt[(L - 2) & 1], C, 1ull << L, n, nullptr}, 1ull << L, nozero,
                           "k_prep(final)")) != WT_OK) {

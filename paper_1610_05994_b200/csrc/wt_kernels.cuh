@@ -14,6 +14,7 @@
 #pragma once
 #include "wt_device.cuh"
 #include "wt_prologue.cuh"
+#include "wt_pair2.cuh"
 
 namespace wt {
 

@@ -1,0 +1,234 @@
+// wt_pair2.cuh -- the level pass of a two-level tree of 1-byte symbols
+// (sigma 3 or 4: the DNA-like workload, the paper's rna.* datasets,
+// P:889-895), specialised.
+//
+// With L = 2 (Alg. 1; Prop. 1) level 0 is one node, so
+//   B_0 = bit 1 of every symbol, in S order;
+//   B_1 = bit 0 of the symbols whose bit 1 is 0, in S order (positions
+//         [0, Z), Z = the zeros of level 0), then bit 0 of those whose bit 1 is
+//         1 (positions [Z, n)).
+// The pass over S before it (k_prologue) counted every tile's level-0 ones and
+// their total (so Z = n - ones0), and a scan turned them into the tile
+// prefixes pre[t].  So every tile is independent: its zeros' bits go to B_1 at
+// T0 - pre[t], its ones' bits at Z + pre[t].
+//
+// This is the general fused pair (k_level<., 2>) with everything L = 2 does
+// not need taken out -- node tables, segments, the TMA ring, progressive
+// counting: a warp takes 2048-symbol tiles round-robin (the level pass's
+// tiles, whose prefixes the scan produced) through its own ring of TMA
+// buffers, every lane 64 consecutive symbols.  The lane's symbols are compacted 4 at a time: one
+// multiply gathers their 8 bits into a byte, a 256-entry table gives their
+// level-0 bits and their zeros' and ones' bit-0 strings, whose appends are
+// multiply-adds.  Each lane's two strings (<= 64 bits) are stored straight to
+// B_1: words wholly inside the lane's run plain, the run's first and last
+// words (shared with neighbouring lanes and tiles: the paper's atomic
+// boundary words) OR-ed into the zero-filled level.
+#pragma once
+#include <cuda.h>
+
+#include "wt_device.cuh"
+#include "wt_ptx.cuh"
+
+namespace wt {
+
+constexpr int P2_TILE = 2048;  // = LvTile<uint8_t>::TILE (the tile prefixes' granularity)
+constexpr int P2_MINB = 32;    // warps (CTAs) per SM the register budget is sized for (every slot: latency hiding)
+
+// 256-entry table, index = the (bit 0, bit 1) pairs of 4 symbols (bit 2j =
+// bit 0 of symbol j, bit 2j+1 = its bit 1):
+//   .x = [3:0] bit 0 of the symbols with bit 1 = 0, in order (the zeros' string)
+//        [11:8] bit 0 of the symbols with bit 1 = 1 (the ones' string)
+//        [19:16] bit 1 of the four symbols (their level-0 bits)
+//   .y = [7:0] 2^(their zeros), [15:8] 2^(their ones): the strings' position multipliers
+__device__ __forceinline__ uint2 p2_lut_entry(uint32_t idx) {
+  uint32_t zb = 0, nz = 0, ob = 0, no = 0, m1 = 0;
+  for (uint32_t j = 0; j < 4; ++j) {
+    const uint32_t b0 = (idx >> (2 * j)) & 1u, b1 = (idx >> (2 * j + 1)) & 1u;
+    m1 |= b1 << j;
+    if (b1) ob |= b0 << no++;
+    else zb |= b0 << nz++;
+  }
+  return make_uint2(zb | (ob << 8) | (m1 << 16), (1u << nz) | ((1u << no) << 8));
+}
+
+// 32 consecutive symbols (8 words), the first `valid` real: level-0 word m,
+// zeros' string Z, ones' string O.
+__device__ __forceinline__ void p2_quarter(const uint32_t* w, uint32_t valid, const uint2* lut, uint32_t& m,
+                                           uint32_t& Z, uint32_t& O) {
+  m = Z = O = 0;
+  if (valid == 32) {
+    uint32_t pz = 1, po = 1;
+#pragma unroll
+    for (int wi = 0; wi < 8; ++wi) {
+      // byte j's two bits to 24 + 2j: x * (2^24 + 2^18 + 2^12 + 2^6) (symbols < 4: the
+      // pass over S checked the range; no carries reach the top byte)
+      const uint2 e = lut[(w[wi] * 0x01041040u) >> 24];
+      m |= ((e.x >> 16) & 15u) << (4 * wi);
+      Z += (e.x & 15u) * pz;
+      O += ((e.x >> 8) & 15u) * po;
+      pz *= e.y & 0xffu;
+      po *= e.y >> 8;
+    }
+    return;
+  }
+  uint32_t nz = 0, no = 0;
+  uint32_t ww[8];  // (a copy: the dynamic index below must not pull the caller's registers into memory)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) ww[k] = w[k];
+  for (uint32_t j = 0; j < valid; ++j) {
+    const uint32_t s = (ww[j >> 2] >> (8 * (j & 3))) & 0xffu;
+    const uint32_t b1 = (s >> 1) & 1u, b0 = s & 1u;
+    m |= b1 << j;
+    if (b1) O |= b0 << no++;
+    else Z |= b0 << nz++;
+  }
+}
+
+// nb <= 64 bits of v (v[0] low) at global bit position pos of `bits`: the
+// words wholly inside [pos, pos + nb) stored, the partial first / last OR-ed
+__device__ __forceinline__ void p2_put(uint32_t* bits, uint64_t pos, const uint32_t (&v)[2], uint32_t nb) {
+  if (nb == 0) return;
+  const uint64_t j = pos >> 5;
+  const uint32_t off = (uint32_t)(pos & 31u), end = off + nb;  // bit range [off, end) of words j, j+1, j+2
+  const uint32_t w0 = v[0] << off;
+  const uint32_t w1 = __funnelshift_lc(v[0], v[1], off);
+  const uint32_t w2 = __funnelshift_lc(v[1], 0u, off);
+  if (off == 0 && end >= 32) bits[j] = w0;
+  else atomicOr(&bits[j], w0);
+  if (end > 32) {
+    if (end >= 64) bits[j + 1] = w1;
+    else atomicOr(&bits[j + 1], w1);
+  }
+  if (end > 64) {
+    if (end == 96) bits[j + 2] = w2;
+    else atomicOr(&bits[j + 2], w2);
+  }
+}
+
+constexpr int P2_WARPS = 4;   // independent warps per CTA (they share the table)
+constexpr int P2_NB = 3;      // per-warp ring of input tiles
+
+struct P2Smem {
+  alignas(1024) uint4 ring[P2_WARPS][P2_NB][P2_TILE / 16];  // 16 rows of 128 bytes per tile, 128-byte swizzle
+  uint2 lut[256];
+  alignas(8) unsigned long long bar[P2_WARPS][P2_NB];
+};
+constexpr size_t p2_smem_bytes() { return sizeof(P2Smem) + 1024; }
+
+// 2-D tensor-map bulk copy (rows of 128 bytes, SWIZZLE_128B) into shared memory
+__device__ __forceinline__ void p2_tma(void* dst, const void* tmap, int32_t row, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(tmap), "r"(0), "r"(row), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// B_0, SB_0 and B_1 (which must be zero on entry) of a two-level tree of n
+// 1-byte symbols.  P2_WARPS independent warps per CTA (no block barrier after
+// the table is built); tiles round-robin over all warps.  Each warp streams
+// its tiles through a ring of P2_NB buffers filled by TMA tensor copies (S as
+// rows of 128 bytes, 128-byte swizzle: lane l owns half of row l/2 and reads
+// its four 16-byte chunks from distinct banks).
+__global__ void __launch_bounds__(32 * P2_WARPS, 6)
+    k_pair2(const uint8_t* __restrict__ S, uint64_t n, uint32_t ntiles, const uint32_t* __restrict__ pre,
+            const unsigned long long* __restrict__ ones0, uint32_t* __restrict__ B0,
+            unsigned long long* __restrict__ SB0, uint64_t nsb, uint32_t* __restrict__ B1,
+            const int32_t* __restrict__ flag, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ unsigned char p2_raw[];
+  P2Smem& sm = *reinterpret_cast<P2Smem*>((reinterpret_cast<uintptr_t>(p2_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t i = threadIdx.x; i < 256; i += 32 * P2_WARPS) sm.lut[i] = p2_lut_entry(i);
+  if (lane == 0) {
+    for (int b = 0; b < P2_NB; ++b) mbar_init(&sm.bar[wid][b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t gw = blockIdx.x * P2_WARPS + wid, nw = gridDim.x * P2_WARPS;  // this warp, all warps
+  const uint64_t full_bytes = n & ~127ull;  // the tensor map's whole rows
+  auto issue = [&](uint32_t it) {           // lane 0: the warp's it-th tile into ring slot it % P2_NB
+    const uint32_t tile = gw + it * nw;
+    if (tile >= ntiles) return;
+    const int b = (int)(it % P2_NB);
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&sm.bar[wid][b], P2_TILE);  // (rows past the tensor's end are zero-filled)
+    p2_tma(sm.ring[wid][b], &tmap, (int32_t)(tile * (P2_TILE / 128)), &sm.bar[wid][b]);
+  };
+  pdl_wait();  // the tile prefixes, ones0, the zero-filled B_1 (and no range error)
+  if (*flag) return;
+  if (lane == 0)
+    for (uint32_t b = 0; b < P2_NB; ++b) issue(b);
+  const uint64_t Z = n - *ones0;  // the zeros of level 0: B_1's ones' run starts here
+  const uint32_t row = lane >> 1, swz = row & 7u;
+  for (uint32_t it = 0;; ++it) {
+    const uint32_t tile = gw + it * nw;
+    if (tile >= ntiles) break;
+    const int b = (int)(it % P2_NB);
+    const uint64_t T0 = (uint64_t)tile * P2_TILE;
+    const uint64_t p0 = T0 + 64ull * lane;
+    const uint32_t P = __ldg(&pre[tile]);  // level-0 ones before the tile (issued before the wait)
+    mbar_wait(&sm.bar[wid][b], (it / P2_NB) & 1u);
+    unsigned char* const buf = reinterpret_cast<unsigned char*>(sm.ring[wid][b]);
+    if (T0 + P2_TILE > full_bytes && full_bytes < n) {  // the partial last row: into its swizzled place
+      for (uint64_t g = full_bytes + lane; g < n; g += 32) {
+        const uint32_t off = (uint32_t)(g - T0), r = off >> 7, c = (off >> 4) & 7u;
+        buf[r * 128 + ((c ^ (r & 7u)) << 4) + (off & 15u)] = S[g];
+      }
+      __syncwarp();
+    }
+    uint32_t w[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t c = 4 * (lane & 1u) + (uint32_t)k;
+      const uint4 q = *reinterpret_cast<const uint4*>(buf + row * 128 + ((c ^ swz) << 4));
+      w[4 * k] = q.x, w[4 * k + 1] = q.y, w[4 * k + 2] = q.z, w[4 * k + 3] = q.w;
+    }
+    __syncwarp();  // every lane has read the slot: refill it
+    if (lane == 0) issue(it + P2_NB);
+    const uint32_t nvalid = p0 >= n ? 0u : (uint32_t)min((uint64_t)64, n - p0);
+    uint32_t m[2], Zs[2], Os[2];
+    p2_quarter(w, min(nvalid, 32u), sm.lut, m[0], Zs[0], Os[0]);
+    p2_quarter(w + 8, nvalid > 32 ? nvalid - 32 : 0u, sm.lut, m[1], Zs[1], Os[1]);
+    // level-0 words (the last tile's padding words: zero)
+    if (p0 < ((n + 511) & ~511ull)) *reinterpret_cast<uint2*>(B0 + p0 / 32) = make_uint2(m[0], m[1]);
+    const uint32_t o0 = (uint32_t)__popc(m[0]), o1 = (uint32_t)__popc(m[1]);
+    const uint32_t no = o0 + o1;
+    const uint32_t inc = warp_incl_scan_u32(no);
+    const uint32_t R = inc - no;  // level-0 ones before the lane, inside the tile
+    if ((lane & 7u) == 0 && p0 < n) SB0[p0 / 512] = P + R;
+    if (tile + 1 == ntiles && lane == 31) SB0[nsb - 1] = P + inc;
+    // the lane's two 64-bit strings: quarter 1's bits after quarter 0's
+    const uint32_t z0 = min(nvalid, 32u) - o0, nzl = nvalid - no;
+    const uint64_t zc = (uint64_t)Zs[0] | ((uint64_t)Zs[1] << z0), oc = (uint64_t)Os[0] | ((uint64_t)Os[1] << o0);
+    const uint32_t Zv[2] = {(uint32_t)zc, (uint32_t)(zc >> 32)};
+    const uint32_t Ov[2] = {(uint32_t)oc, (uint32_t)(oc >> 32)};
+    p2_put(B1, T0 - P + (64ull * lane - R), Zv, nzl);   // zeros before the lane: positions - ones
+    p2_put(B1, Z + P + R, Ov, no);
+  }
+  pdl_trigger();
+}
+
+// Node offsets of the two-level tree: C = [0, H0, H0+H1, H0+H1+H2, n] with
+// H0 + H1 = Z (level 0's zeros), H1 = ones of B_1 before Z (its zeros' run),
+// H3 = ones of B_1 from Z on.  Reads SB_1 (the final scan wrote it) and at
+// most 16 words of B_1.  One thread.
+__global__ void k_pair2_offsets(const uint32_t* __restrict__ B1, const unsigned long long* __restrict__ SB1,
+                                uint64_t nsb, const unsigned long long* __restrict__ ones0, uint64_t n,
+                                unsigned long long* __restrict__ C, const int32_t* __restrict__ flag) {
+  pdl_wait();
+  if (threadIdx.x != 0 || blockIdx.x != 0 || *flag) return;
+  const uint64_t Z = n - *ones0;
+  uint64_t r = SB1[Z >> 9];  // ones of B_1 before Z
+  const uint32_t* blk = B1 + 16 * (Z >> 9);
+  const uint32_t wi = (uint32_t)(Z >> 5) & 15u, bi = (uint32_t)Z & 31u;
+  for (uint32_t k = 0; k < wi; ++k) r += (uint32_t)__popc(blk[k]);
+  if (bi) r += (uint32_t)__popc(blk[wi] & ((1u << bi) - 1u));
+  const uint64_t H1 = r, H0 = Z - H1, H3 = SB1[nsb - 1] - H1;
+  C[0] = 0;
+  C[1] = H0;
+  C[2] = Z;
+  C[3] = n - H3;
+  C[4] = n;
+  pdl_trigger();
+}
+
+}  // namespace wt

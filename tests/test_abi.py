@@ -95,7 +95,9 @@ def test_launch_plan(wt):
     lv = ["prep", "level"]
     pair = ["prep", "pair", "final_scan"]
     assert wt.launch_plan(1 << 20, 256, 1) == ["prologue"] + lv * 6 + pair
-    assert wt.launch_plan(1 << 20, 4, 1) == ["prologue"] + pair
+    # two levels of 1-byte symbols: the specialised pair pass, C from B_1's superblocks
+    assert wt.launch_plan(1 << 20, 4, 1) == ["prologue"] + pair + ["pair2_offsets"]
+    assert wt.launch_plan(1 << 20, 4, 2) == ["prologue"] + pair
     assert wt.launch_plan(1 << 20, 8, 1) == ["prologue"] + lv + pair
     assert wt.launch_plan(100, 2, 1) == ["prologue", "prep", "last_level"]
     assert wt.launch_plan(100, 1, 1) == ["prologue", "scan"]

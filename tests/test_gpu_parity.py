@@ -492,3 +492,18 @@ def test_l2_edges(wt, width):
         with pytest.raises(wt.WtError) as e:
             wt.build(to_dev(bad), 4)
         assert e.value.status == wt.WT_ERR_SYMBOL_RANGE
+
+
+@pytest.fixture
+def no_pair2():
+    os.environ["WT_NO_PAIR2"] = "1"
+    yield
+    del os.environ["WT_NO_PAIR2"]
+
+
+@pytest.mark.parametrize("sigma,n", [(4, 300_001), (3, 100_000), (4, 2048 * 7 + 5)])
+def test_l2_general_pair(wt, no_pair2, sigma, n):
+    # WT_NO_PAIR2=1: two levels of 1-byte symbols through the general fused pair
+    assert "pair2_offsets" not in wt.launch_plan(n, sigma, 1)
+    S = wt_inputs.random_case(n, n, sigma, "zipf", dtype=np.uint8)
+    check_case(wt, S, sigma, f"general pair n={n}")

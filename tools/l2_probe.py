@@ -1,4 +1,4 @@
-"""Probe: a few cfg2-shaped builds (n = 2^N u8, sigma = 4) for profiling the one-pass L = 2 kernel."""
+"""Probe: cfg2-shaped builds (n = 2^N u8, sigma = 4): ms per build and per launch."""
 import sys
 import numpy as np
 import torch
@@ -23,4 +23,12 @@ for _ in range(10):
     wt.build_async(d, sigma, tree=tree, workspace=ws, status=st)
 e1.record()
 torch.cuda.synchronize()
-print(f"n=2^{N}: {e0.elapsed_time(e1) / 10:.4f} ms/build")
+plan = wt.launch_plan(S.size, sigma, 1)
+evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * len(plan))] for _ in range(10)]
+for k in range(10):
+    wt.set_profile_events(evs[k])
+    wt.build_async(d, sigma, tree=tree, workspace=ws, status=st)
+wt.set_profile_events(None)
+torch.cuda.synchronize()
+per = [sum(evs[k][2 * i].elapsed_time(evs[k][2 * i + 1]) for k in range(10)) / 10 for i in range(len(plan))]
+print(f"n=2^{N}: {e0.elapsed_time(e1) / 10:.4f} ms/build  " + " ".join(f"{p}={t:.4f}" for p, t in zip(plan, per)))
