@@ -18,6 +18,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def kind_of(name: str) -> str:
+    if "k_pair2_offsets" in name:
+        return "pair2_offsets"
+    if "k_pair2" in name:
+        return "pair"
     if "k_prep" in name:
         return "final_scan" if ("OpBitsPop" in name or "OpBlockPop" in name) else "prep"
     if "k_prologue" in name:
@@ -108,11 +112,12 @@ def main():
         lines.append(f"ncu --set full capture (level pass), cfg{cfg}:")
         for r in fc:
             lines.append("  " + json.dumps(r))
-        lvl = [r for r in fc if "k_level" in r["kernel"]]
+        lvl = [r for r in fc if "k_level" in r["kernel"] or "k_pair2" in r["kernel"]]
         if lvl:
             traffic = {}
             for r in lvl:
-                kd = "pair" if ", 2>" in r["kernel"] else "level" if ", 1>" in r["kernel"] else "last_level"
+                kd = ("pair" if (", 2>" in r["kernel"] or "k_pair2" in r["kernel"]) else
+                      "level" if ", 1>" in r["kernel"] else "last_level")
                 traffic.setdefault(kd, r["dram_read"] + r["dram_write"])
             traffic["_source"] = f"profiles/{tag}/ncu_summary_cfg{cfg}.txt"
             with open(os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cfg}.json"), "w") as f:
