@@ -21,7 +21,10 @@ namespace wt {
 // ================================================================ a2 scans
 
 constexpr int SCAN_THREADS = 512;
-constexpr int SCAN_ITEMS = 8;
+#ifndef WT_SCAN_ITEMS
+#define WT_SCAN_ITEMS 8
+#endif
+constexpr int SCAN_ITEMS = WT_SCAN_ITEMS;  // values per thread of a scan tile (experiment builds override)
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
 // Scan ops whose values are the popcounts of consecutive 512-bit blocks of a
