@@ -53,6 +53,8 @@ def parse(argv=None):
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
     ap.add_argument("--no-extra", action="store_true", help="skip the cfg3-5 device-timed lines")
     ap.add_argument("--extra-steps", type=int, default=10)
+    ap.add_argument("--dd", action="store_true",
+                    help="run the multi-GPU (domain decomposition) step even at N = 1 (its merge overhead)")
     ap.add_argument("--out", default=None, help="also write the JSON line (plus per-kernel detail) here")
     return ap.parse_args(argv)
 
@@ -510,11 +512,17 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or args.dd:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            if "MASTER_PORT" not in os.environ:
+                with socket.socket() as s:
+                    s.bind(("127.0.0.1", 0))
+                    os.environ["MASTER_PORT"] = str(s.getsockname()[1])
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
 
     cfg = args.config
-    if world > 1:
+    if world > 1 or args.dd:
         run_dd(args, wt, rank, world, local, dev)
         dist.destroy_process_group()
         return

@@ -299,6 +299,7 @@ wt_status wt_dd_merge(uint32_t k, const wt_tree_t* segs, const uint64_t* seg_n, 
  *   nodes are in order, and so are they in the merge).  lo counts the
  *   segment-g bits whose merged position is before the part: by node offsets
  *   alone (binary search for the node holding the part's first position).
+ *   The plan has L * parts * k entries; with L = 0 (sigma = 1) it may be NULL.
  * wt_dd_merge_level: level `level` of the merge over merged words
  *   [word_begin, word_end) into d_out[0 .. word_end - word_begin).  Segment g's
  *   local bit q of that level is bit (q - src_base[g]) of the words at

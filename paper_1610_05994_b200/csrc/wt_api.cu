@@ -106,6 +106,9 @@ struct Carve {
   size_t off_flag = 0, off_counters = 0, off_ones0 = 0, off_status = 0, off_value = 0, off_agg = 0, ctrl_bytes = 0;
   size_t off_status2 = 0, off_value2 = 0;  // a second look-back state (two scans per k_prep launch)
   size_t off_pre = 0, off_tab = 0, off_cnt = 0, off_bufA = 0, off_bufB = 0, total = 0;
+  // a5 interior fused groups (k_quad): per-tile class counts (zeroed with the
+  // control block), their prefixes, the level-2 node sizes for the first quad
+  size_t off_agg01 = 0, off_agg11 = 0, off_hist4 = 0, off_pre01 = 0, off_pre11 = 0;
   // host-API extras (after total)
   size_t off_seq = 0, off_bits = 0, off_sb = 0, off_c = 0, host_total = 0;
   // segmented build (n > seg_max(): S is cut into k segments, each built with
@@ -143,6 +146,22 @@ uint64_t sb_scan_tiles(uint64_t nblocks) {
 }
 
 Carve carve_direct(uint64_t n, uint64_t sigma, uint32_t width);
+
+// a5: interior fused groups of k = 2 levels (k_quad, wt_quad.cuh) at
+// l = 0, 2, ..., 2 (nquad - 1): l <= Q_MAXL (the node table of <= 64 nodes) and
+// l + 2 <= L - 2 (T_{l+2} feeds a later pass; the last two levels are the fused
+// final pair).  Opt-in (WT_QUAD=1, read per call): measured on B200 the quad
+// pass is slower than the two level passes it replaces.
+bool quad_enabled() {
+  const char* v = std::getenv("WT_QUAD");
+  return v && *v && *v != '0';
+}
+uint32_t quad_levels(uint32_t L) {
+  if (!quad_enabled() || L < 4) return 0;
+  uint32_t q = 0;
+  while (2 * q <= wt::Q_MAXL && 2 * q + 2 <= L - 2) ++q;
+  return q;
+}
 
 Carve carve(uint64_t n, uint64_t sigma, uint32_t width) {
   const uint64_t sm = seg_max();
@@ -211,6 +230,13 @@ Carve carve_direct(uint64_t n, uint64_t sigma, uint32_t width) {
   o += align_up(c.status_entries * sizeof(uint32_t));
   c.off_agg = o;
   o += align_up((size_t)c.L * c.ntiles * sizeof(uint32_t));
+  const uint32_t qrows = quad_levels(c.L) ? 2 * quad_levels(c.L) - 1 : 0;  // rows l = 0 .. 2 (nquad - 1)
+  c.off_agg01 = o;
+  o += align_up((size_t)qrows * c.ntiles * sizeof(uint32_t));
+  c.off_agg11 = o;
+  o += align_up((size_t)qrows * c.ntiles * sizeof(uint32_t));
+  c.off_hist4 = o;
+  o += ALIGN;
   c.ctrl_bytes = o;
   c.off_value = o;  // look-back values: written before their status, never read stale
   o += align_up(2 * c.status_entries * sizeof(uint64_t));
@@ -218,6 +244,10 @@ Carve carve_direct(uint64_t n, uint64_t sigma, uint32_t width) {
   o += align_up(2 * c.status_entries * sizeof(uint64_t));
   c.off_pre = o;
   o += align_up(c.ntiles * sizeof(uint32_t));
+  c.off_pre01 = o;
+  if (qrows) o += align_up(c.ntiles * sizeof(uint32_t));
+  c.off_pre11 = o;
+  if (qrows) o += align_up(c.ntiles * sizeof(uint32_t));
   c.off_tab = o;
   o += align_up(c.tab_entries * sizeof(uint2));
   c.off_cnt = o;
@@ -315,6 +345,24 @@ cudaError_t pair2_setup(int* blocks_per_sm) {
   *blocks_per_sm = bps[dev];
   return err[dev];
 }
+template <typename T>
+cudaError_t quad_setup(int* blocks_per_sm) {
+  static int bps[MAX_DEVICES] = {};
+  static cudaError_t err[MAX_DEVICES] = {};
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  if (bps[dev] == 0) {
+    int b = 0;
+    cudaError_t e = cudaFuncSetAttribute(wt::k_quad<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)wt::quad_smem_bytes<T>());
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, wt::k_quad<T>, wt::Q_THREADS, wt::quad_smem_bytes<T>());
+    err[dev] = e;
+    bps[dev] = b < 1 ? 1 : b;
+  }
+  *blocks_per_sm = bps[dev];
+  return err[dev];
+}
 // S as a 2-D tensor of rows of 128 bytes (floor(n / 128) rows; the kernel
 // copies the partial last row itself), boxes of one 2048-byte tile, 128-byte
 // swizzle.  cuTensorMapEncodeTiled comes from the driver through the
@@ -362,7 +410,8 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), uint32_t grid, uint32_t block, si
 
 enum Kind : uint32_t {
   K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7, K_PAIR = 8, K_SBSCAN = 9,
-  K_PREP = 11, K_FINAL = 12, K_DD_OFFSETS = 13, K_DD_MERGE = 14, K_DD_SB = 15, K_FLAGS = 16, K_P2C = 17
+  K_PREP = 11, K_FINAL = 12, K_DD_OFFSETS = 13, K_DD_MERGE = 14, K_DD_SB = 15, K_FLAGS = 16, K_P2C = 17,
+  K_QUAD = 18
 };
 
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
@@ -396,6 +445,13 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   unsigned long long* C = (dry || matrix) ? nullptr : reinterpret_cast<unsigned long long*>(out->node_offsets);
   const uint32_t L = c.L;
   cudaError_t e;
+  // a5: interior fused groups (k_quad) at l = 0, 2, ..., 2 (nquad - 1)
+  const uint32_t nquad = matrix ? 0u : quad_levels(L);
+  uint32_t* agg01 = reinterpret_cast<uint32_t*>(ws + c.off_agg01);
+  uint32_t* agg11 = reinterpret_cast<uint32_t*>(ws + c.off_agg11);
+  uint32_t* hist4 = reinterpret_cast<uint32_t*>(ws + c.off_hist4);
+  uint32_t* pre01 = reinterpret_cast<uint32_t*>(ws + c.off_pre01);
+  uint32_t* pre11 = reinterpret_cast<uint32_t*>(ws + c.off_pre11);
 
   if (!dry) {
     if ((e = cudaMemsetAsync(ws, 0, c.ctrl_bytes, stream)) != cudaSuccess) return fail_cuda(e, "memset ctrl");
@@ -438,7 +494,11 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     const uint64_t tiles = (n + wt::LvTile<T>::TILE - 1) / wt::LvTile<T>::TILE;  // one warp per tile
     const uint32_t grid = (uint32_t)std::max<uint64_t>(
         1, std::min<uint64_t>((tiles + wt::PRO_THREADS / 32 - 1) / (wt::PRO_THREADS / 32), 8ull * num_sms()));
-    wt::k_prologue<T><<<grid, wt::PRO_THREADS, 0, stream>>>(seq, n, sigma, L, L ? agg : nullptr, ones0, flag);
+    if (nquad)
+      wt::k_prologue<T, true><<<grid, wt::PRO_THREADS, 0, stream>>>(seq, n, sigma, L, agg, ones0, flag, agg01,
+                                                                     agg11, hist4);
+    else
+      wt::k_prologue<T><<<grid, wt::PRO_THREADS, 0, stream>>>(seq, n, sigma, L, L ? agg : nullptr, ones0, flag);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_prologue");
     if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
   }
@@ -561,7 +621,65 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   // L >= 2: passes 0..L-3 write T_{l+1}; pass L-2 is fused with level L-1
   // (writes B_{L-1} directly, no T_{L-1})
   uint32_t* const lastbits = dry ? nullptr : out->bitmaps + (uint64_t)(L - 1) * c.words;
-  for (uint32_t l = 0; l < Lrun; ++l) {
+  // The quads first.  Quad q (level l = 2q) reads T_l and the level-(l+2)
+  // node sizes (hist4 for q = 0) and writes T_{l+2} and the node sizes the
+  // next pass needs into the buffers of parity (nquad - 1 - q) + 1, so that the
+  // pass after the last quad (level 2 nquad) finds them where a level pass
+  // expects its input: T in buf[1], counts in cnt[1].
+  for (uint32_t q = 0; q < nquad && 2 * q < Lrun; ++q) {
+    const uint32_t l = 2 * q;
+    const uint32_t D = (q + 1 < nquad) ? 2u : 1u;  // node sizes for a following quad (l+4) or level pass (l+3)
+    const uint32_t po = ((nquad - 1 - q) & 1u) ? 0u : 1u;
+    const uint64_t nt = c.ntiles;
+    uint32_t* bits1 = dry ? nullptr : out->bitmaps + (uint64_t)(l + 1) * c.words;
+    wt::ZeroFill z{dry ? nullptr : reinterpret_cast<uint4*>(cnt[po]), 1ull << (l + D),
+                   reinterpret_cast<uint4*>(bits1), c.words / 4};
+    if ((st = prep(K_PREP, wt::OpTilePrefix2{agg01 + l * nt, agg11 + l * nt, pre01, pre11}, nt,
+                   wt::OpTilePrefix{agg + l * nt, pre}, nt, z, "k_prep(quad)")) != WT_OK)
+      return st;
+    note(K_QUAD);
+    if (!dry) {
+      int bps = 1;
+      if ((e = quad_setup<T>(&bps)) != cudaSuccess) return fail_cuda(e, "k_quad setup");
+      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      constexpr uint64_t QT = wt::QCfg<T>::TILE;
+      const uint64_t ntq = (n + QT - 1) / QT;
+      const uint32_t grid = (uint32_t)std::min<uint64_t>(ntq, (uint64_t)bps * num_sms());
+      wt::QuadArgs qa;
+      qa.n = (uint32_t)n;
+      qa.ntq = (uint32_t)ntq;
+      qa.sh = L - 1 - l;
+      qa.nodes = 1u << l;
+      qa.pre1 = pre;
+      qa.pre01 = pre01;
+      qa.pre11 = pre11;
+      qa.gcnt = l == 0 ? hist4 : cnt[po ^ 1u];
+      qa.bits = out->bitmaps + (uint64_t)l * c.words;
+      qa.sb = reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb;
+      qa.nsb = (uint32_t)c.nsb;
+      qa.words = (uint32_t)c.words;
+      qa.bits1 = bits1;
+      qa.agg_next = agg + (l + 2) * nt;
+      qa.agg01_next = D == 2 ? agg01 + (l + 2) * nt : nullptr;
+      qa.agg11_next = D == 2 ? agg11 + (l + 2) * nt : nullptr;
+      qa.cnt_next = cnt[po];
+      qa.D = D;
+      qa.flag = flag;
+      const T* qin = l == 0 ? seq : buf[po ^ 1u];
+      e = launch_pdl(wt::k_quad<T>, grid, wt::Q_THREADS, wt::quad_smem_bytes<T>(), stream, qin, buf[po], qa);
+      if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_quad");
+      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    }
+    // superblocks of level l+1 from the bits the quad OR-ed in
+    note(K_SBSCAN);
+    if ((st = scan(wt::OpBitsPop{bits1, dry ? nullptr
+                                            : reinterpret_cast<unsigned long long*>(out->superblocks) +
+                                                  (uint64_t)(l + 1) * c.nsb,
+                                 c.nsb - 1, 0},
+                   c.nsb - 1, "k_scan(quad sb)")) != WT_OK)
+      return st;
+  }
+  for (uint32_t l = 2 * nquad; l < Lrun; ++l) {
     const bool pair = (l + 2 == L);
     // pre_l (scan of agg_l), the node tables of level l (from the level-(l+1)
     // node sizes counted by pass l-1, or from ones0 for l = 0), and zero the
@@ -1089,8 +1207,8 @@ wt_status wt_dd_plan(uint32_t k, const uint64_t* const* h_seg_offsets, uint64_t 
   wt::DdOffsets sg;
   wt_status st = dd_offsets_of(k, h_seg_offsets, sigma, &sg);
   if (st != WT_OK) return st;
-  if (parts == 0 || !h_plan) return fail(WT_ERR_ARG, "parts = 0 or NULL plan");
   const uint32_t L = sg.L;
+  if (parts == 0 || (!h_plan && L > 0)) return fail(WT_ERR_ARG, "parts = 0 or NULL plan");
   const HostCg cg{h_seg_offsets};
   uint64_t n = 0;
   for (uint32_t g = 0; g < k; ++g) n += h_seg_offsets[g][1ull << L];
@@ -1114,7 +1232,7 @@ wt_status wt_dd_plan_async(uint32_t k, const uint64_t* const* d_seg_offsets, uin
   wt::DdOffsets sg;
   wt_status st = dd_offsets_of(k, d_seg_offsets, sigma, &sg);
   if (st != WT_OK) return st;
-  if (parts == 0 || !d_plan) return fail(WT_ERR_ARG, "parts = 0 or NULL plan");
+  if (parts == 0 || (!d_plan && sg.L > 0)) return fail(WT_ERR_ARG, "parts = 0 or NULL plan");
   const uint64_t t = (uint64_t)sg.L * parts * k;
   if (t == 0) return WT_OK;
   wt::k_dd_plan<<<(uint32_t)((t + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(

@@ -15,6 +15,7 @@
 #include "wt_device.cuh"
 #include "wt_prologue.cuh"
 #include "wt_pair2.cuh"
+#include "wt_quad.cuh"
 
 namespace wt {
 
@@ -280,6 +281,21 @@ struct OpTilePrefix {  // (n < 2^32: the prefixes fit 32 bits)
   uint32_t* pre;
   __device__ uint64_t load(uint64_t i) const { return agg[i]; }
   __device__ void store(uint64_t i, uint64_t excl, uint64_t) const { pre[i] = (uint32_t)excl; }
+};
+
+// The class-count tile prefixes of a quad pass (wt_quad.cuh): classes 01 and
+// 11 of the bit pair (l, l+1) packed in one 64-bit value (each prefix <= n <
+// 2^32, so the low half never carries into the high half).
+struct OpTilePrefix2 {
+  const uint32_t* a01;
+  const uint32_t* a11;
+  uint32_t* p01;
+  uint32_t* p11;
+  __device__ uint64_t load(uint64_t i) const { return a01[i] | ((uint64_t)a11[i] << 32); }
+  __device__ void store(uint64_t i, uint64_t excl, uint64_t) const {
+    p01[i] = (uint32_t)excl;
+    p11[i] = (uint32_t)(excl >> 32);
+  }
 };
 
 // Node tables of level l from the sizes of the level-(l+1) nodes

@@ -94,7 +94,20 @@ def test_launch_plan(wt):
     # level's superblocks (from its bitmap) and C in one launch
     lv = ["prep", "level"]
     pair = ["prep", "pair", "final_scan"]
+    # interior fused groups (a5, k = 2) at l = 0, 2, .. <= 6 while l + 2 <= L - 2:
+    # tile prefixes + zeroing, the quad pass, the superblocks of its level l+1
+    # (opt-in, WT_QUAD=1: slower than the level passes on B200)
     assert wt.launch_plan(1 << 20, 256, 1) == ["prologue"] + lv * 6 + pair
+    quad = ["prep", "quad", "sb_scan"]
+    os.environ["WT_QUAD"] = "1"
+    try:
+        assert wt.launch_plan(1 << 20, 256, 1) == ["prologue"] + quad * 3 + pair
+        assert wt.launch_plan(1 << 20, 1 << 16, 2) == ["prologue"] + quad * 4 + lv * 6 + pair
+        assert wt.launch_plan(1 << 20, 32, 1) == ["prologue"] + quad + lv + pair
+        assert wt.launch_plan(1 << 20, 16, 4) == ["prologue"] + quad + pair
+        assert wt.launch_plan(1 << 20, 8, 1) == ["prologue"] + lv + pair   # L = 3: no quad
+    finally:
+        del os.environ["WT_QUAD"]
     # two levels of 1-byte symbols: the specialised pair pass, C from B_1's superblocks
     assert wt.launch_plan(1 << 20, 4, 1) == ["prologue"] + pair + ["pair2_offsets"]
     assert wt.launch_plan(1 << 20, 4, 2) == ["prologue"] + pair

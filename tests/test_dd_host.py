@@ -25,7 +25,7 @@ def segment_trees(S, sigma, cuts):
 @pytest.mark.parametrize("sigma,n,k,parts,kind", [
     (16, 30, 3, 2, "uniform"), (4, 5000, 2, 3, "uniform"), (256, 20000, 5, 4, "zipf"),
     (1 << 12, 9000, 8, 8, "runs"), (3, 1000, 4, 7, "uniform"), (1 << 16, 3000, 3, 2, "zipf"),
-    (2, 700, 1, 1, "uniform"), (1000, 4096 + 13, 6, 5, "sorted"),
+    (2, 700, 1, 1, "uniform"), (1000, 4096 + 13, 6, 5, "sorted"), (1, 500, 3, 2, "uniform"),
 ])
 def test_plan_matches_brute_force(wt, sigma, n, k, parts, kind):
     S = wt_inputs.random_case(n * k + parts, n, sigma, kind)
