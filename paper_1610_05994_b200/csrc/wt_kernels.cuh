@@ -615,6 +615,27 @@ __global__ void k_dd_merge_level(DdOffsets sg, DdLevelSrc src, uint32_t l, const
       }
     };
     enter(0);
+    if (rem >= qend - q) {
+      // one run covers the thread's whole range (long runs: shallow levels, few
+      // segments): a funnel-shifted copy with all source loads issued first
+      const uint32_t len = (uint32_t)(qend - q), nw = (len + 31) / 32;
+      const uint32_t* sbits = src.bits[h];
+      const uint64_t sw = (sp - src.base[h]) >> 5;
+      const uint32_t o = (uint32_t)(sp & 31);
+      const uint32_t last = (o + len - 1) >> 5;  // the last source word holding a needed bit
+      uint32_t x[DD_WPT + 1];
+#pragma unroll
+      for (uint32_t i = 0; i <= DD_WPT; ++i) x[i] = i <= last ? sbits[sw + i] : 0u;
+#pragma unroll
+      for (uint32_t i = 0; i < DD_WPT; ++i) {
+        if (i < nw) {
+          uint32_t v = __funnelshift_r(x[i], x[i + 1], o);
+          if (32 * (i + 1) > len) v &= (1u << (len - 32 * i)) - 1u;
+          out[(q >> 5) + i - w_begin] = v;
+        }
+      }
+      q = qend;
+    } else {
     uint32_t acc = 0;
     for (;;) {
       const uint32_t d = (uint32_t)(q & 31);
@@ -650,6 +671,7 @@ __global__ void k_dd_merge_level(DdOffsets sg, DdLevelSrc src, uint32_t l, const
       }
     }
     if (q & 31) out[(q >> 5) - w_begin] = acc;  // q == n: the last, partial word
+    }
   }
   for (uint64_t w = max(w0, (n + 31) >> 5); w < w1; ++w) out[w - w_begin] = 0;  // padding past n
 }
