@@ -754,8 +754,8 @@ cudaError_t launch_merge_level(const wt::DdOffsets& sg, const wt::DdLevelSrc& sr
                                uint32_t* out, cudaStream_t s, const int32_t* flag = nullptr) {
   if (w_end <= w_begin) return cudaSuccess;
   const uint64_t threads = (w_end - w_begin + wt::DD_WPT - 1) / wt::DD_WPT;
-  wt::k_dd_merge_level<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(sg, src, l, C, n, w_begin, w_end, out,
-                                                                         flag);
+  wt::k_dd_merge_level<<<(uint32_t)((threads + wt::DD_THREADS - 1) / wt::DD_THREADS), wt::DD_THREADS, 0, s>>>(
+      sg, src, l, C, n, w_begin, w_end, out, flag);
   return cudaGetLastError();
 }
 

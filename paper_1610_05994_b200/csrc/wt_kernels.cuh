@@ -576,13 +576,22 @@ __global__ void k_dd_plan(DdOffsets sg, uint64_t n, uint64_t parts, unsigned lon
 // ... in merged order, funnel-shifting up to 32 source bits at a time into the
 // word it assembles; every word is written once with a plain store (no zero
 // fill, no atomics: the paper's concat of bit runs, done from the
-// destination side), words past n as zeros.
-constexpr uint32_t DD_WPT = 8;  // merged words per thread
+// destination side), words past n as zeros.  When one run covers the thread's
+// whole range (long runs: shallow levels, few segments) the words are a
+// funnel-shifted copy with all source loads issued first.  The thread's words
+// leave as two 16-byte stores (one L2 request per 4 words: per-word stores of
+// 8-word-strided threads made the merge L2-request-bound, 140 -> 49 us per
+// cfg2 level).
+constexpr uint32_t DD_WPT = 8;     // merged words per thread (two 16-byte stores)
+constexpr uint32_t DD_THREADS = 256;
 // (flag, optional: a segmented build's range flag; set = the segment trees are
 // unspecified, nothing is merged)
-__global__ void k_dd_merge_level(DdOffsets sg, DdLevelSrc src, uint32_t l, const unsigned long long* __restrict__ C,
-                                 uint64_t n, uint64_t w_begin, uint64_t w_end, uint32_t* __restrict__ out,
-                                 const int32_t* __restrict__ flag) {
+__global__ void __launch_bounds__(DD_THREADS) k_dd_merge_level(DdOffsets sg, DdLevelSrc src, uint32_t l,
+                                                               const unsigned long long* __restrict__ C, uint64_t n,
+                                                               uint64_t w_begin, uint64_t w_end,
+                                                               uint32_t* __restrict__ out,
+                                                               const int32_t* __restrict__ flag) {
+  __shared__ uint32_t sbuf[DD_THREADS * DD_WPT];  // the run walk's words (dynamic index) before the vector stores
   if (flag && *flag) return;
   const uint64_t w0 = w_begin + ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * DD_WPT;
   if (w0 >= w_end) return;
@@ -590,6 +599,9 @@ __global__ void k_dd_merge_level(DdOffsets sg, DdLevelSrc src, uint32_t l, const
   const uint64_t qend = min(32 * w1, n);
   const uint32_t sh = sg.L - l;  // node v of level l spans leaves [v << sh, (v + 1) << sh)
   const uint64_t nodes = 1ull << l;
+  uint32_t v8[DD_WPT];  // the thread's words (zero past n)
+#pragma unroll
+  for (uint32_t i = 0; i < DD_WPT; ++i) v8[i] = 0;
   uint64_t q = 32 * w0;
   if (q < qend) {
     uint64_t v = 0, sp = 0, rem = 0;  // current run: segment h, source positions [sp, sp + rem)
@@ -615,10 +627,8 @@ __global__ void k_dd_merge_level(DdOffsets sg, DdLevelSrc src, uint32_t l, const
       }
     };
     enter(0);
-    if (rem >= qend - q) {
-      // one run covers the thread's whole range (long runs: shallow levels, few
-      // segments): a funnel-shifted copy with all source loads issued first
-      const uint32_t len = (uint32_t)(qend - q), nw = (len + 31) / 32;
+    if (rem >= qend - q) {  // one run: a funnel-shifted copy
+      const uint32_t len = (uint32_t)(qend - q);
       const uint32_t* sbits = src.bits[h];
       const uint64_t sw = (sp - src.base[h]) >> 5;
       const uint32_t o = (uint32_t)(sp & 31);
@@ -628,52 +638,61 @@ __global__ void k_dd_merge_level(DdOffsets sg, DdLevelSrc src, uint32_t l, const
       for (uint32_t i = 0; i <= DD_WPT; ++i) x[i] = i <= last ? sbits[sw + i] : 0u;
 #pragma unroll
       for (uint32_t i = 0; i < DD_WPT; ++i) {
-        if (i < nw) {
-          uint32_t v = __funnelshift_r(x[i], x[i + 1], o);
-          if (32 * (i + 1) > len) v &= (1u << (len - 32 * i)) - 1u;
-          out[(q >> 5) + i - w_begin] = v;
+        const uint32_t y = __funnelshift_r(x[i], x[i + 1], o);
+        v8[i] = 32 * (i + 1) <= len ? y : (32 * i < len ? y & ((1u << (len - 32 * i)) - 1u) : 0u);
+      }
+    } else {  // the run walk, words into this thread's shared slot
+      uint32_t* mine = sbuf + threadIdx.x * DD_WPT;
+#pragma unroll
+      for (uint32_t i = 0; i < DD_WPT; ++i) mine[i] = 0;
+      uint32_t acc = 0;
+      for (;;) {
+        const uint32_t d = (uint32_t)(q & 31);
+        const uint32_t len = (uint32_t)min(min(rem, qend - q), (uint64_t)(32 - d));
+        const uint32_t* s = src.bits[h];
+        const uint64_t sw = (sp - src.base[h]) >> 5;
+        const uint32_t o = (uint32_t)(sp & 31);
+        const uint32_t lo_w = s[sw];
+        const uint32_t hi_w = (o + len > 32) ? s[sw + 1] : 0u;
+        uint32_t x = __funnelshift_r(lo_w, hi_w, o);
+        if (len < 32) x &= (1u << len) - 1u;
+        acc |= x << d;
+        q += len;
+        sp += len;
+        rem -= len;
+        if ((q & 31) == 0) {
+          mine[(q >> 5) - 1 - w0] = acc;
+          acc = 0;
         }
-      }
-      q = qend;
-    } else {
-    uint32_t acc = 0;
-    for (;;) {
-      const uint32_t d = (uint32_t)(q & 31);
-      const uint32_t len = (uint32_t)min(min(rem, qend - q), (uint64_t)(32 - d));
-      const uint32_t* s = src.bits[h];
-      const uint64_t sw = (sp - src.base[h]) >> 5;
-      const uint32_t o = (uint32_t)(sp & 31);
-      const uint32_t lo_w = s[sw];
-      const uint32_t hi_w = (o + len > 32) ? s[sw + 1] : 0u;
-      uint32_t x = __funnelshift_r(lo_w, hi_w, o);
-      if (len < 32) x &= (1u << len) - 1u;
-      acc |= x << d;
-      q += len;
-      sp += len;
-      rem -= len;
-      if ((q & 31) == 0) {
-        out[(q >> 5) - 1 - w_begin] = acc;
-        acc = 0;
-      }
-      if (q >= qend) break;
-      if (rem == 0) {  // next non-empty run: later segment of v, else a later node
-        uint32_t g = h + 1;
-        for (; g < sg.k; ++g) {
-          const uint64_t a = sg.C[g][v << sh], sz = sg.C[g][(v + 1) << sh] - a;
-          if (sz) {
-            h = g;
-            sp = a;
-            rem = sz;
-            break;
+        if (q >= qend) break;
+        if (rem == 0) {  // next non-empty run: later segment of v, else a later node
+          uint32_t g = h + 1;
+          for (; g < sg.k; ++g) {
+            const uint64_t a = sg.C[g][v << sh], sz = sg.C[g][(v + 1) << sh] - a;
+            if (sz) {
+              h = g;
+              sp = a;
+              rem = sz;
+              break;
+            }
           }
+          if (g == sg.k) enter(v + 1);
         }
-        if (g == sg.k) enter(v + 1);
       }
-    }
-    if (q & 31) out[(q >> 5) - w_begin] = acc;  // q == n: the last, partial word
+      if (q & 31) mine[(q >> 5) - w0] = acc;  // q == n: the last, partial word
+#pragma unroll
+      for (uint32_t i = 0; i < DD_WPT; ++i) v8[i] = mine[i];
     }
   }
-  for (uint64_t w = max(w0, (n + 31) >> 5); w < w1; ++w) out[w - w_begin] = 0;  // padding past n
+  uint32_t* dst = out + (w0 - w_begin);
+  if (w1 - w0 == DD_WPT && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+    reinterpret_cast<uint4*>(dst)[0] = make_uint4(v8[0], v8[1], v8[2], v8[3]);
+    reinterpret_cast<uint4*>(dst)[1] = make_uint4(v8[4], v8[5], v8[6], v8[7]);
+  } else {
+#pragma unroll
+    for (uint32_t i = 0; i < DD_WPT; ++i)
+      if (w0 + i < w1) dst[i] = v8[i];
+  }
 }
 
 // C = sum over the segments' node offsets
