@@ -2,7 +2,11 @@
 set -u
 mkdir -p gpurun_out
 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build.log 2>&1
-WT_QUAD=2 WT_DEBUG_SYNC=1 timeout 300 python tools/quad_check.py > gpurun_out/quad_check.log 2>&1; echo "rc=$?" >> gpurun_out/quad_check.log
-for c in 3 4 5; do
-  WT_QUAD=2 timeout 300 python bench.py --config $c --no-cpu-baseline --no-extra --no-graph --e2e-steps 1 --out gpurun_out/qw_cfg$c.json > gpurun_out/qw_cfg$c.log 2>&1
+for r in 1 2; do
+for v in lut1 main lut2 lut8; do
+  if [ $v = main ]; then L=""; else L=tools/libwt_$v.so; fi
+  echo "== $v" >> gpurun_out/ab_lut.log
+  WT_LIB=$L timeout 300 python tools/ab_cfg.py 2 50 >> gpurun_out/ab_lut.log 2>&1
 done
+done
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "l2 or config_parity and 2 or edge_sizes" > gpurun_out/pytest_p2.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_p2.log
