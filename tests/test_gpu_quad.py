@@ -119,3 +119,20 @@ def test_quad_full_size_cfg3(wt, quad_on):
     for l, (ob, osb, _) in oracle_levels_parallel(S, sigma, tree.levels):
         assert np.array_equal(B[l], ob), f"level {l} bitmap"
         assert np.array_equal(SB[l], osb), f"level {l} superblocks"
+
+
+def test_quad_inside_segmented_build(wt, quad_on):
+    # a segmented build (n > seg_max, here lowered) runs the direct sequence --
+    # with its quads -- on every segment, then merges
+    old = os.environ.get("WT_SEG_MAX")
+    os.environ["WT_SEG_MAX"] = str(4 * 4096)
+    try:
+        for sigma, n, kind in [(256, 100_003, "zipf"), (1 << 16, 70_001, "uniform")]:
+            S = wt_inputs.random_case(n, n, sigma, kind)
+            plan = check(wt, S, sigma, f"segmented sigma={sigma} n={n}")
+            assert "dd_merge" in plan and "quad" in plan
+    finally:
+        if old is None:
+            del os.environ["WT_SEG_MAX"]
+        else:
+            os.environ["WT_SEG_MAX"] = old

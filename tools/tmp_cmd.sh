@@ -2,11 +2,7 @@
 set -u
 mkdir -p gpurun_out
 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build.log 2>&1
-for r in 1 2; do
-for v in lut1 main lut2 lut8; do
-  if [ $v = main ]; then L=""; else L=tools/libwt_$v.so; fi
-  echo "== $v" >> gpurun_out/ab_lut.log
-  WT_LIB=$L timeout 300 python tools/ab_cfg.py 2 50 >> gpurun_out/ab_lut.log 2>&1
-done
-done
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "l2 or config_parity and 2 or edge_sizes" > gpurun_out/pytest_p2.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_p2.log
+CMD="python bench.py --config 5 --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-extra --no-graph"
+# level 20 of the 5th build (22 level launches per build: skip 4 builds + 20)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_level' -s 108 -c 1 -o gpurun_out/lvl5 $CMD > gpurun_out/ncu_lvl5.log 2>&1
+echo rc=$? >> gpurun_out/ncu_lvl5.log
