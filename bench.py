@@ -59,7 +59,7 @@ def parse(argv=None):
     return ap.parse_args(argv)
 
 
-def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
+def algorithmic_bytes(kind: str, n: int, w: int, L: int, c_in_final: bool = True) -> int:
     """Bytes the levelwise method itself must move per launch (DESIGN.md §6 table)."""
     nsb = (n + 511) // 512 + 1
     bitmap = 4 * 16 * ((n + 511) // 512)
@@ -80,8 +80,10 @@ def algorithmic_bytes(kind: str, n: int, w: int, L: int) -> int:
         tables = sum(4 * (2 << l) + 8 * (1 << l) for l in range(max(L - 1, 0)))
         zero = sum(16 * (1 << l) for l in range(max(L - 1, 0))) + (bitmap if L >= 2 else 0)
         return 8 * tiles + (tables + zero) // levels
-    if kind == "final_scan":  # last-level superblocks from its bitmap, C from the leaf counts
-        return bitmap + 8 * nsb + 4 * (1 << L) + 8 * ((1 << L) + 1)
+    if kind == "final_scan":  # last-level superblocks from its bitmap (and C from the leaf counts)
+        return bitmap + 8 * nsb + ((4 * (1 << L) + 8 * ((1 << L) + 1)) if c_in_final else 0)
+    if kind == "leaf_offsets":  # C from the level-(L-2) node table and B_{L-1}'s ranks at the node starts
+        return 8 * ((1 << L) + 1) + 8 * (1 << max(L - 2, 0))
     return 0
 
 
@@ -301,7 +303,7 @@ def kernel_table(res, n, w, L, peak):
         kinds.setdefault(kd, []).append(t)
     out = {}
     for kd, ts in kinds.items():
-        ab = algorithmic_bytes(kd, n, w, L)
+        ab = algorithmic_bytes(kd, n, w, L, c_in_final="leaf_offsets" not in plan)
         fr = [ab / (t * 1e-3) / 1e9 / peak for t in ts if t > 0]
         e = {"launches_per_step": len(ts), "ms_per_step": sum(ts), "share": sum(ts) / ms,
              "per_launch_ms": {"min": min(ts), "mean": sum(ts) / len(ts), "max": max(ts)},

@@ -345,6 +345,30 @@ cudaError_t pair2_setup(int* blocks_per_sm) {
   *blocks_per_sm = bps[dev];
   return err[dev];
 }
+// The fused final pair of deeper trees (k_pairn, wt_pairn.cuh); WT_NO_PAIRN=1
+// (read per call) uses the general fused pair k_level<T, 2> instead (A/B, tests).
+bool pairn_enabled() {
+  const char* v = std::getenv("WT_NO_PAIRN");
+  return !(v && *v && *v != '0');
+}
+template <typename T>
+cudaError_t pairn_setup(int* blocks_per_sm) {
+  static int bps[MAX_DEVICES] = {};
+  static cudaError_t err[MAX_DEVICES] = {};
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  if (bps[dev] == 0) {
+    int b = 0;
+    cudaError_t e = cudaFuncSetAttribute(wt::k_pairn<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)wt::pn_smem_bytes());
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, wt::k_pairn<T>, 32 * wt::PN_WARPS, wt::pn_smem_bytes());
+    err[dev] = e;
+    bps[dev] = b < 1 ? 1 : b;
+  }
+  *blocks_per_sm = bps[dev];
+  return err[dev];
+}
 template <typename T>
 cudaError_t quad_setup(int* blocks_per_sm) {
   static int bps[MAX_DEVICES] = {};
@@ -551,6 +575,8 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   const uint32_t grid_pair = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)bps_pair * (uint64_t)num_sms());
   // two levels of 1-byte symbols: the specialised pass (wt_pair2.cuh) replaces the fused pair
   const bool pair2 = (L == 2 && !matrix && sizeof(T) == 1 && n >= 128 && pair2_enabled());
+  // any other tree: the general fused final pair without symbol moves (wt_pairn.cuh)
+  const bool pairn = (!pair2 && !matrix && n * sizeof(T) >= 128 && pairn_enabled());
   auto level = [&](uint32_t l, int mode) -> wt_status {
     note(mode == 0 ? K_LAST : mode == 2 ? K_PAIR : K_LEVEL);
     if (dry) return WT_OK;
@@ -572,6 +598,23 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       return WT_OK;
     }
     const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
+    if (mode == 2 && pairn) {
+      int bps = 1;
+      if ((e = pairn_setup<T>(&bps)) != cudaSuccess) return fail_cuda(e, "k_pairn setup");
+      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      const uint32_t grid = (uint32_t)std::min<uint64_t>((c.ntiles + wt::PN_WARPS - 1) / wt::PN_WARPS,
+                                                         (uint64_t)bps * num_sms());
+      CUtensorMap tmap;
+      if (!rows128_tensor_map(&tmap, in, n * sizeof(T), 16)) return fail(WT_ERR_CUDA, "cuTensorMapEncodeTiled");
+      e = launch_pdl(wt::k_pairn<T>, grid, (uint32_t)(32 * wt::PN_WARPS), wt::pn_smem_bytes(), stream, in,
+                     (uint32_t)n, (uint32_t)c.ntiles, (const uint32_t*)pre, (const uint2*)(tab + ((1ull << l) - 1)),
+                     out->bitmaps + (uint64_t)l * c.words, (uint32_t)c.words,
+                     reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb, (uint32_t)c.nsb,
+                     out->bitmaps + (uint64_t)(L - 1) * c.words, (const int32_t*)flag, tmap);
+      if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_pairn");
+      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      return WT_OK;
+    }
     T* o = mode == 0 ? nullptr : mode == 2 ? reinterpret_cast<T*>(out->bitmaps + (uint64_t)(L - 1) * c.words)
                                            : buf[l & 1];
     const int red = pair_red_override();
@@ -712,18 +755,19 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       if ((st = prep(K_FINAL, wt::OpBitsPopZ{lastbits, sbl, c.nsb - 1, mzeros + (L - 1), n}, c.nsb - 1, wt::OpNone{},
                      0, nozero, "k_prep(final)")) != WT_OK)
         return st;
-    } else if (pair2) {
-      // B_1's superblocks, then C from them (k_pair2 counts no leaves)
+    } else if (pair2 || pairn) {
+      // B_{L-1}'s superblocks, then C from them (k_pair2 / k_pairn count no leaves)
       if ((st = prep(K_FINAL, wt::OpBitsPop{lastbits, sbl, c.nsb - 1}, c.nsb - 1, wt::OpNone{}, 0, nozero,
                      "k_prep(final)")) != WT_OK)
         return st;
       note(K_P2C);
       if (!dry) {
         if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-        e = launch_pdl(wt::k_pair2_offsets, 1u, 32u, (size_t)0, stream, (const uint32_t*)lastbits,
-                       (const unsigned long long*)sbl, c.nsb, (const unsigned long long*)ones0, n, C,
-                       (const int32_t*)flag);
-        if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_pair2_offsets");
+        const uint64_t nq = 1ull << (L - 1);
+        const uint32_t g = (uint32_t)std::min<uint64_t>((nq + 255) / 256, 8ull * num_sms());
+        e = launch_pdl(wt::k_leaf_offsets, g, 256u, (size_t)0, stream, (const uint2*)(tab + ((1ull << (L - 2)) - 1)),
+                       L, (const uint32_t*)lastbits, (const unsigned long long*)sbl, n, C, (const int32_t*)flag);
+        if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_leaf_offsets");
         if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
       }
     } else if ((st = prep(K_FINAL, wt::OpBitsPop{lastbits, sbl, c.nsb - 1}, c.nsb - 1,

@@ -15,6 +15,7 @@
 #include "wt_device.cuh"
 #include "wt_prologue.cuh"
 #include "wt_pair2.cuh"
+#include "wt_pairn.cuh"
 #include "wt_quad.cuh"
 
 namespace wt {
@@ -366,6 +367,39 @@ __device__ __forceinline__ uint64_t rank1(const uint32_t* __restrict__ B,
   for (uint32_t w = 0; w < wi; ++w) r += (uint32_t)__popc(blk[w]);
   if (bi) r += (uint32_t)__popc(blk[wi] & ((1u << bi) - 1u));
   return r;
+}
+
+// Node offsets C (the output, line 7's exclusive prefix of the leaf counts,
+// P:541-543) of a tree whose last pass was the fused pair (k_pairn, k_pair2),
+// which counts no leaves.  Level-(L-1) node q = leaf pair (2q, 2q+1) spans
+// [s_q, s_{q+1}); its start from the level-(L-2) node table {ob, Zn} of its
+// parent v = q >> 1 (the zeros of level L-2 before v's end, Zn[v], plus the
+// ones before v, ob[v], for the right child; Zn[v-1] + ob[v] for the left);
+// leaf 2q+1's size is the ones of B_{L-1} inside node q (Prop. 1: bit 0).  So
+//   C[2q] = s_q,   C[2q+1] = s_{q+1} - (rank1(s_{q+1}) - rank1(s_q)),   C[2^L] = n.
+// One thread per level-(L-1) node; B_{L-1}'s superblocks must be final.
+__device__ __forceinline__ uint64_t leaf_node_start(const uint2* __restrict__ tab, uint64_t q, uint64_t nq,
+                                                    uint64_t n) {
+  if (q >= nq) return n;
+  const uint64_t v = q >> 1;
+  const uint2 t = tab[v];
+  if (q & 1) return (uint64_t)t.y + t.x;
+  return (v ? (uint64_t)tab[v - 1].y : 0ull) + t.x;
+}
+__global__ void k_leaf_offsets(const uint2* __restrict__ tab, uint32_t L, const uint32_t* __restrict__ B,
+                               const unsigned long long* __restrict__ SB, uint64_t n,
+                               unsigned long long* __restrict__ C, const int32_t* __restrict__ flag) {
+  pdl_wait();
+  if (*flag) return;
+  const uint64_t nq = 1ull << (L - 1);
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s0 = leaf_node_start(tab, q, nq, n), s1 = leaf_node_start(tab, q + 1, nq, n);
+    const uint64_t ones = rank1(B, SB, s1) - rank1(B, SB, s0);
+    C[2 * q] = s0;
+    C[2 * q + 1] = s1 - ones;
+    if (q + 1 == nq) C[2 * nq] = n;
+  }
+  pdl_trigger();
 }
 
 // out[k] = ones of level lv[k] before position pos[k] (pos <= n): bit-level

@@ -207,28 +207,4 @@ __global__ void __launch_bounds__(32 * P2_WARPS, 6)
   pdl_trigger();
 }
 
-// Node offsets of the two-level tree: C = [0, H0, H0+H1, H0+H1+H2, n] with
-// H0 + H1 = Z (level 0's zeros), H1 = ones of B_1 before Z (its zeros' run),
-// H3 = ones of B_1 from Z on.  Reads SB_1 (the final scan wrote it) and at
-// most 16 words of B_1.  One thread.
-__global__ void k_pair2_offsets(const uint32_t* __restrict__ B1, const unsigned long long* __restrict__ SB1,
-                                uint64_t nsb, const unsigned long long* __restrict__ ones0, uint64_t n,
-                                unsigned long long* __restrict__ C, const int32_t* __restrict__ flag) {
-  pdl_wait();
-  if (threadIdx.x != 0 || blockIdx.x != 0 || *flag) return;
-  const uint64_t Z = n - *ones0;
-  uint64_t r = SB1[Z >> 9];  // ones of B_1 before Z
-  const uint32_t* blk = B1 + 16 * (Z >> 9);
-  const uint32_t wi = (uint32_t)(Z >> 5) & 15u, bi = (uint32_t)Z & 31u;
-  for (uint32_t k = 0; k < wi; ++k) r += (uint32_t)__popc(blk[k]);
-  if (bi) r += (uint32_t)__popc(blk[wi] & ((1u << bi) - 1u));
-  const uint64_t H1 = r, H0 = Z - H1, H3 = SB1[nsb - 1] - H1;
-  C[0] = 0;
-  C[1] = H0;
-  C[2] = Z;
-  C[3] = n - H3;
-  C[4] = n;
-  pdl_trigger();
-}
-
 }  // namespace wt

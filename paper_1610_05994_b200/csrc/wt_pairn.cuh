@@ -1,0 +1,256 @@
+// wt_pairn.cuh -- the fused final pair of any tree with L >= 2: pass L-2 over
+// T_{L-2} writes B_{L-2}, SB_{L-2} and B_{L-1} (a5 with k = 2 at the bottom
+// of the tree; Alg. 1 lines 8-13 for levels L-2 and L-1).
+//
+// T_{L-2} is S stably sorted by the top L-2 bits (Prop. 1), so a
+// position j of node v (v = s >> 2) with level-(L-2) bit b1 = bit 1 of s goes
+// to T_{L-1} position
+//   b1 = 0: j - r(j) + ob[v]        b1 = 1: r(j) + Zn[v]
+// (r(j) = level-(L-2) ones before j; {ob, Zn} = the node table the prep built,
+// the closed form of Alg. 1's C[node]++ cursors), and B_{L-1} at that position
+// is bit 0 of s.  No symbol moves: a lane's run of symbols inside one node
+// sends its zeros' bit-0 string (in order) to one destination and its ones'
+// bit-0 string to another, both contiguous.
+//
+// This is k_pair2's execution (wt_pair2.cuh) made general: per warp a ring of
+// 2 KiB TMA tensor copies of T_{L-2} (rows of 128 bytes, 128-byte swizzle; the
+// level pass's tile, so its tile prefixes pre[t] apply), each lane 64 bytes =
+// E symbols, compacted 4 at a time by the 256-entry table (bit 0 / bit 1 of
+// 4 symbols -> their level-(L-2) bits, the zeros' and ones' bit-0 strings and
+// the strings' position multipliers).  Node changes inside a lane's symbols
+// split its two strings into per-node substrings (the strings are in position
+// order, so node g's part is the bits between the zeros / ones before g's
+// first symbol and after its last).  Every substring is stored with its
+// interior words plain and its first / last word OR-ed into the zero-filled
+// B_{L-1} (the paper's atomic boundary words).  No leaves are
+// counted: C comes from B_{L-1}'s superblocks afterwards (k_leaf_offsets).
+#pragma once
+#include <cuda.h>
+
+#include "wt_device.cuh"
+#include "wt_pair2.cuh"
+#include "wt_ptx.cuh"
+
+namespace wt {
+
+template <typename T>
+struct PnCfg {
+  static constexpr int W = (int)sizeof(T);
+  static constexpr int E = 64 / W;          // symbols per lane
+  static constexpr int TILE = 32 * E;       // symbols per tile (= LvTile<T>::TILE, 2 KiB)
+  static constexpr int G = E / 4;           // groups of 4 symbols per lane
+  static constexpr int NH = E > 32 ? 2 : 1;  // 32-symbol halves per lane
+  static constexpr int GH = G / NH;         // groups per half
+};
+constexpr int PN_WARPS = 4;  // independent warps per CTA (they share the table)
+constexpr int PN_NB = 3;     // per-warp ring of input tiles
+
+struct PnSmem {
+  alignas(1024) uint4 ring[PN_WARPS][PN_NB][2048 / 16];  // 16 rows of 128 bytes per tile, 128-byte swizzle
+  uint2 lut[256];
+  alignas(8) unsigned long long bar[PN_WARPS][PN_NB];
+};
+constexpr size_t pn_smem_bytes() { return sizeof(PnSmem) + 1024; }
+
+// the (bit 0, bit 1) pairs of symbols 4g .. 4g+3 of a lane (w: its 16 words)
+// as the table index (bit 2j = bit 0 of symbol j, bit 2j+1 = its bit 1)
+template <typename T>
+__device__ __forceinline__ uint32_t pn_index(const uint32_t (&w)[16], int g) {
+  if constexpr (sizeof(T) == 1) {
+    // byte j's two bits to 24 + 2j (masked to 2 bits: no carries into the top byte)
+    return ((w[g] & 0x03030303u) * 0x01041040u) >> 24;
+  } else if constexpr (sizeof(T) == 2) {
+    const uint32_t x = (w[2 * g] & 0x00030003u) | ((w[2 * g + 1] & 0x00030003u) << 4);
+    return (x | (x >> 14)) & 0xffu;
+  } else {
+    return (w[4 * g] & 3u) | ((w[4 * g + 1] & 3u) << 2) | ((w[4 * g + 2] & 3u) << 4) | ((w[4 * g + 3] & 3u) << 6);
+  }
+}
+
+// symbol j of a lane (j may be a run-time value: the word is selected from
+// the registers, so the lane's words stay out of local memory)
+template <typename T>
+__device__ __forceinline__ uint32_t pn_sym(const uint32_t (&w)[16], uint32_t j) {
+  constexpr uint32_t SPW = 4 / sizeof(T);
+  const uint32_t k = j / SPW;
+  uint32_t x = w[0];
+#pragma unroll
+  for (uint32_t i = 1; i < 16; ++i) x = (k == i) ? w[i] : x;
+  if constexpr (sizeof(T) == 1) return (x >> (8 * (j & 3))) & 0xffu;
+  else if constexpr (sizeof(T) == 2) return (x >> (16 * (j & 1))) & 0xffffu;
+  else return x;
+}
+// symbol j of a lane, j a compile-time index
+template <typename T, int J>
+__device__ __forceinline__ uint32_t pn_sym_c(const uint32_t (&w)[16]) {
+  if constexpr (sizeof(T) == 1) return (w[J >> 2] >> (8 * (J & 3))) & 0xffu;
+  else if constexpr (sizeof(T) == 2) return (w[J >> 1] >> (16 * (J & 1))) & 0xffffu;
+  else return w[J];
+}
+// bit j of the lane: symbol j's node differs from symbol j-1's (j >= 1)
+template <typename T, int J = 1>
+__device__ __forceinline__ uint64_t pn_heads(const uint32_t (&w)[16], uint32_t prev) {
+  constexpr int E = 64 / (int)sizeof(T);
+  if constexpr (J >= E) {
+    return 0ull;
+  } else {
+    const uint32_t nd = pn_sym_c<T, J>(w) >> 2;
+    return ((uint64_t)(nd != prev) << J) | pn_heads<T, J + 1>(w, nd);
+  }
+}
+
+// bits [a, a + k) of a 64-bit string as two words (k <= 64)
+__device__ __forceinline__ void pn_sub(uint64_t s, uint32_t a, uint32_t k, uint32_t (&v)[2]) {
+  const uint64_t x = (a >= 64 ? 0ull : (s >> a)) & (k >= 64 ? ~0ull : ((1ull << k) - 1ull));
+  v[0] = (uint32_t)x;
+  v[1] = (uint32_t)(x >> 32);
+}
+
+// B_{L-2} (bits), its superblocks and B_{L-1} (must be zero on entry) from
+// T_{L-2} (n symbols, n < 2^32), the level-(L-2) tile prefixes pre[t] and node
+// table tab[v] = {ob[v], Zn[v]}.
+template <typename T>
+__global__ void __launch_bounds__(32 * PN_WARPS, 6)
+    k_pairn(const T* __restrict__ in, uint32_t n, uint32_t ntiles, const uint32_t* __restrict__ pre,
+            const uint2* __restrict__ tab, uint32_t* __restrict__ bits, uint32_t words,
+            unsigned long long* __restrict__ sb, uint32_t nsb, uint32_t* __restrict__ B1,
+            const int32_t* __restrict__ flag, const __grid_constant__ CUtensorMap tmap) {
+  using C = PnCfg<T>;
+  constexpr int E = C::E, TILE = C::TILE, NH = C::NH, GH = C::GH;
+  extern __shared__ unsigned char pn_raw[];
+  PnSmem& sm = *reinterpret_cast<PnSmem*>((reinterpret_cast<uintptr_t>(pn_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t i = threadIdx.x; i < 256; i += 32 * PN_WARPS) sm.lut[i] = p2_lut_entry(i);
+  if (lane == 0) {
+    for (int b = 0; b < PN_NB; ++b) mbar_init(&sm.bar[wid][b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t gw = blockIdx.x * PN_WARPS + wid, nw = gridDim.x * PN_WARPS;
+  const uint64_t nbytes = (uint64_t)n * sizeof(T);
+  const uint64_t full_bytes = nbytes & ~127ull;  // the tensor map's whole rows
+  auto issue = [&](uint32_t it) {
+    const uint32_t tile = gw + it * nw;
+    if (tile >= ntiles) return;
+    const int b = (int)(it % PN_NB);
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&sm.bar[wid][b], 2048);  // (rows past the tensor's end are zero-filled)
+    p2_tma(sm.ring[wid][b], &tmap, (int32_t)(tile * 16u), &sm.bar[wid][b]);
+  };
+  pdl_wait();  // T_{L-2}, the tile prefixes, the node table, the zero-filled B_{L-1}
+  if (*flag) return;
+  if (lane == 0)
+    for (uint32_t b = 0; b < PN_NB; ++b) issue(b);
+  const uint32_t row = lane >> 1, swz = row & 7u;
+  const uint64_t padded = ((uint64_t)n + 511) & ~511ull;
+  const unsigned char* inb = reinterpret_cast<const unsigned char*>(in);
+  for (uint32_t it = 0;; ++it) {
+    const uint32_t tile = gw + it * nw;
+    if (tile >= ntiles) break;
+    const int b = (int)(it % PN_NB);
+    const uint32_t T0 = tile * (uint32_t)TILE;
+    const uint64_t p0 = (uint64_t)T0 + (uint32_t)E * lane;  // the lane's first position
+    const uint32_t P = __ldg(&pre[tile]);
+    mbar_wait(&sm.bar[wid][b], (it / PN_NB) & 1u);
+    unsigned char* const buf = reinterpret_cast<unsigned char*>(sm.ring[wid][b]);
+    const uint64_t B0 = (uint64_t)T0 * sizeof(T);
+    if (B0 + 2048 > full_bytes && full_bytes < nbytes) {  // the partial last row: into its swizzled place
+      for (uint64_t g = full_bytes + lane; g < nbytes; g += 32) {
+        const uint32_t off = (uint32_t)(g - B0), r = off >> 7, c = (off >> 4) & 7u;
+        buf[r * 128 + ((c ^ (r & 7u)) << 4) + (off & 15u)] = inb[g];
+      }
+      __syncwarp();
+    }
+    uint32_t w[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t c = 4 * (lane & 1u) + (uint32_t)k;
+      const uint4 q = *reinterpret_cast<const uint4*>(buf + row * 128 + ((c ^ swz) << 4));
+      w[4 * k] = q.x, w[4 * k + 1] = q.y, w[4 * k + 2] = q.z, w[4 * k + 3] = q.w;
+    }
+    __syncwarp();  // every lane has read the slot: refill it
+    if (lane == 0) issue(it + PN_NB);
+    const uint32_t nvalid = p0 >= n ? 0u : (uint32_t)min((uint64_t)E, n - p0);
+
+    // level-(L-2) bits m (position order) and the zeros' / ones' bit-0 strings
+    uint32_t m[NH];
+    uint64_t zc = 0, oc = 0;
+    uint32_t nz = 0, no = 0;  // string lengths
+    if (nvalid == (uint32_t)E) {
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        uint32_t mm = 0, Zs = 0, Os = 0, pz = 1, po = 1;
+#pragma unroll
+        for (int g = 0; g < GH; ++g) {
+          const uint2 e = sm.lut[pn_index<T>(w, h * GH + g)];
+          mm |= ((e.x >> 16) & 15u) << (4 * g);
+          Zs += (e.x & 15u) * pz;
+          Os += ((e.x >> 8) & 15u) * po;
+          pz *= e.y & 0xffu;
+          po *= e.y >> 8;
+        }
+        m[h] = mm;
+        const uint32_t o = (uint32_t)__popc(mm), z = (uint32_t)(4 * GH) - o;
+        zc |= (uint64_t)Zs << nz;
+        oc |= (uint64_t)Os << no;
+        nz += z;
+        no += o;
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < NH; ++h) m[h] = 0;
+      for (uint32_t j = 0; j < nvalid; ++j) {
+        const uint32_t s = pn_sym<T>(w, j);
+        const uint32_t b1 = (s >> 1) & 1u, b0 = s & 1u;
+        if (NH == 1 || j < 32) m[0] |= b1 << (j & 31);
+        else m[NH - 1] |= b1 << (j & 31);
+        if (b1) oc |= (uint64_t)b0 << no++;
+        else zc |= (uint64_t)b0 << nz++;
+      }
+    }
+    // bitmap words of level L-2 (the last tile's padding words: zero)
+    if constexpr (E == 64) {
+      if (p0 < padded) *reinterpret_cast<uint2*>(bits + p0 / 32) = make_uint2(m[0], m[NH - 1]);
+    } else if constexpr (E == 32) {
+      if (p0 < padded) bits[p0 / 32] = m[0];
+    } else {  // E == 16: two lanes per word
+      const uint32_t wv = m[0] | (__shfl_down_sync(FULL, m[0], 1) << 16);
+      if ((lane & 1) == 0 && p0 < padded) bits[p0 / 32] = wv;
+    }
+    const uint32_t ones = (uint32_t)__popc(m[0]) + (NH == 2 ? (uint32_t)__popc(m[NH - 1]) : 0u);
+    const uint32_t inc = warp_incl_scan_u32(ones);
+    const uint32_t R = inc - ones;  // level-(L-2) ones before the lane, inside the tile
+    if ((p0 & 511u) == 0 && p0 < n) sb[p0 / 512] = P + R;
+    if (tile + 1 == ntiles && lane == 31) sb[nsb - 1] = P + inc;
+    if (nvalid == 0) continue;
+
+    // the lane's runs of one node each: [a, e) with node v
+    uint32_t v = pn_sym_c<T, 0>(w) >> 2;
+    const uint32_t vlast = (nvalid == (uint32_t)E ? pn_sym_c<T, E - 1>(w) : pn_sym<T>(w, nvalid - 1)) >> 2;
+    uint64_t heads = 0;  // bit j: symbol j starts a new node (j >= 1)
+    if (v != vlast) heads = pn_heads<T>(w, v) & (nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull));
+    const uint64_t m64 = (uint64_t)m[0] | (NH == 2 ? ((uint64_t)m[NH - 1] << 32) : 0ull);
+    uint32_t a = 0, oa = 0;  // run start, level-(L-2) ones before it in the lane
+    for (;;) {
+      const uint32_t e = heads ? (uint32_t)(__ffsll((long long)heads) - 1) : nvalid;
+      const uint64_t em = e >= 64 ? ~0ull : ((1ull << e) - 1ull);
+      const uint32_t oe = (uint32_t)__popcll(m64 & em);
+      const uint2 tv = __ldg(&tab[v]);
+      uint32_t sz[2], so[2];
+      pn_sub(zc, a - oa, (e - a) - (oe - oa), sz);
+      pn_sub(oc, oa, oe - oa, so);
+      // zeros before position p0 + a: (p0 + a) - (P + R + oa), + ob[v]; ones: P + R + oa + Zn[v]
+      // (mod 2^32: every position is < n < 2^32)
+      p2_put(B1, (uint64_t)((uint32_t)p0 + a - P - R - oa + tv.x), sz, (e - a) - (oe - oa));
+      p2_put(B1, (uint64_t)(uint32_t)(P + R + oa + tv.y), so, oe - oa);
+      if (e >= nvalid) break;
+      a = e;
+      oa = oe;
+      v = pn_sym<T>(w, e) >> 2;
+      heads &= heads - 1;
+    }
+  }
+  pdl_trigger();
+}
+
+}  // namespace wt

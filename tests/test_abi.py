@@ -93,7 +93,8 @@ def test_launch_plan(wt):
     # pass; pass L-2 is fused with level L-1 (writes B_{L-1}), then the last
     # level's superblocks (from its bitmap) and C in one launch
     lv = ["prep", "level"]
-    pair = ["prep", "pair", "final_scan"]
+    # (the fused final pair counts no leaves: C from B_{L-1}'s ranks at the node starts)
+    pair = ["prep", "pair", "final_scan", "leaf_offsets"]
     # interior fused groups (a5, k = 2) at l = 0, 2, .. <= 6 while l + 2 <= L - 2:
     # tile prefixes + zeroing, the quad pass, the superblocks of its level l+1
     # (opt-in, WT_QUAD=1: slower than the level passes on B200)
@@ -108,9 +109,21 @@ def test_launch_plan(wt):
         assert wt.launch_plan(1 << 20, 8, 1) == ["prologue"] + lv + pair   # L = 3: no quad
     finally:
         del os.environ["WT_QUAD"]
-    # two levels of 1-byte symbols: the specialised pair pass, C from B_1's superblocks
-    assert wt.launch_plan(1 << 20, 4, 1) == ["prologue"] + pair + ["pair2_offsets"]
+    # two levels of 1-byte symbols: the specialised pair pass (k_pair2)
+    assert wt.launch_plan(1 << 20, 4, 1) == ["prologue"] + pair
     assert wt.launch_plan(1 << 20, 4, 2) == ["prologue"] + pair
+    # fewer than 128 bytes of symbols (no TMA tensor rows) or WT_NO_PAIRN=1: the
+    # general fused pair, which counts the leaves (C from the final scan)
+    gpair = ["prep", "pair", "final_scan"]
+    assert wt.launch_plan(127, 256, 1) == ["prologue"] + lv * 6 + gpair
+    assert wt.launch_plan(31, 1 << 20, 4) == ["prologue"] + lv * 18 + gpair
+    os.environ["WT_NO_PAIRN"] = "1"
+    try:
+        assert wt.launch_plan(1 << 20, 256, 1) == ["prologue"] + lv * 6 + gpair
+        assert wt.launch_plan(1 << 20, 4, 1) == ["prologue"] + pair      # (k_pair2 is separate)
+        assert wt.launch_plan(1 << 20, 4, 2) == ["prologue"] + gpair
+    finally:
+        del os.environ["WT_NO_PAIRN"]
     assert wt.launch_plan(1 << 20, 8, 1) == ["prologue"] + lv + pair
     assert wt.launch_plan(100, 2, 1) == ["prologue", "prep", "last_level"]
     assert wt.launch_plan(100, 1, 1) == ["prologue", "scan"]

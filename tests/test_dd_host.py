@@ -66,6 +66,6 @@ def test_segmented_sizes_and_plan(wt):
     assert s.levels == 2 and s.words_per_level == 16 * ((n + 511) // 512)
     assert s.workspace_bytes > 2 * n // 8   # three segment trees of two levels
     plan = wt.launch_plan(n, 4, 1)
-    seg = ["prologue", "prep", "pair", "final_scan", "pair2_offsets"]
+    seg = ["prologue", "prep", "pair", "final_scan", "leaf_offsets"]
     assert plan == (seg + ["flags"]) * 3 + ["dd_offsets"] + ["dd_merge", "dd_superblocks"] * 2
     assert wt.launch_plan(1 << 20, 4, 1) == seg

@@ -496,9 +496,54 @@ def test_l2_edges(wt, width):
 
 @pytest.fixture
 def no_pair2():
+    # (and no k_pairn, which would otherwise take over the two-level trees)
     os.environ["WT_NO_PAIR2"] = "1"
+    os.environ["WT_NO_PAIRN"] = "1"
     yield
     del os.environ["WT_NO_PAIR2"]
+    del os.environ["WT_NO_PAIRN"]
+
+
+@pytest.fixture
+def no_pairn():
+    os.environ["WT_NO_PAIRN"] = "1"
+    yield
+    del os.environ["WT_NO_PAIRN"]
+
+
+@pytest.mark.parametrize("width", [1, 2, 4])
+def test_general_fused_pair(wt, no_pairn, width):
+    # WT_NO_PAIRN=1: the final pair through the general k_level<T, 2> (it counts
+    # the leaves itself; C from the final scan)
+    sigma = {1: 256, 2: 1 << 16, 4: 1 << 20}[width]
+    dtype = {1: np.uint8, 2: np.uint16, 4: np.uint32}[width]
+    assert "leaf_offsets" not in wt.launch_plan(100_000, sigma, width)
+    for k, kind in enumerate(["uniform", "zipf", "runs"]):
+        S = wt_inputs.random_case(700 + k, 100_000 + 37 * k, sigma, kind, dtype=dtype)
+        check_case(wt, S, sigma, f"general pair w={width} {kind}")
+
+
+@pytest.mark.parametrize("width", [1, 2, 4])
+def test_pairn_node_changes(wt, width):
+    # k_pairn: a lane's symbols span many level-(L-2) nodes (sorted / uniform
+    # over a large alphabet: a new node at almost every symbol), one node
+    # (constant), node runs crossing lanes and tiles, every tail geometry
+    # around the 128-byte tensor rows, the 2 KiB tile and the 64-byte lane
+    dtype = {1: np.uint8, 2: np.uint16, 4: np.uint32}[width]
+    t = TILE[width]
+    rows = 128 // width
+    cases = []
+    for sigma in ({1: (5, 8, 256), 2: (8, 300, 1 << 16), 4: (8, 1 << 12, 1 << 24)}[width]):
+        for kind in ("uniform", "sorted", "runs", "constant", "zipf"):
+            cases.append((sigma, kind, 3 * t + 77))
+    for n in (rows, rows + 1, 2 * rows - 1, t - 1, t + rows, 5 * t + 64 // width - 1, 5 * t + 64 // width + 1):
+        cases.append(({1: 256, 2: 1 << 16, 4: 1 << 24}[width], "uniform", n))
+        cases.append((8, "sorted", n))
+    for i, (sigma, kind, n) in enumerate(cases):
+        S = wt_inputs.random_case(900 + i, n, sigma, kind, dtype=dtype)
+        if n * width >= 128 and sigma > 4:
+            assert "leaf_offsets" in wt.launch_plan(n, sigma, width)
+        check_case(wt, S, sigma, f"pairn w={width} sigma={sigma} {kind} n={n}")
 
 
 @pytest.mark.parametrize("sigma,n", [(4, 300_001), (3, 100_000), (4, 2048 * 7 + 5)])

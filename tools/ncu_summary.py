@@ -18,9 +18,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def kind_of(name: str) -> str:
-    if "k_pair2_offsets" in name:
-        return "pair2_offsets"
-    if "k_pair2" in name:
+    if "k_leaf_offsets" in name:
+        return "leaf_offsets"
+    if "k_pair2" in name or "k_pairn" in name:
         return "pair"
     if "k_prep" in name:
         return "final_scan" if ("OpBitsPop" in name or "OpBlockPop" in name) else "prep"
@@ -116,7 +116,7 @@ def main():
         if lvl:
             traffic = {}
             for r in lvl:
-                kd = ("pair" if (", 2>" in r["kernel"] or "k_pair2" in r["kernel"]) else
+                kd = ("pair" if (", 2>" in r["kernel"] or "k_pair2" in r["kernel"] or "k_pairn" in r["kernel"]) else
                       "level" if ", 1>" in r["kernel"] else "last_level")
                 traffic.setdefault(kd, r["dram_read"] + r["dram_write"])
             traffic["_source"] = f"profiles/{tag}/ncu_summary_cfg{cfg}.txt"
