@@ -386,6 +386,19 @@ __device__ __forceinline__ uint64_t leaf_node_start(const uint2* __restrict__ ta
   if (q & 1) return (uint64_t)t.y + t.x;
   return (v ? (uint64_t)tab[v - 1].y : 0ull) + t.x;
 }
+// ones of one level in [s0, s1): short ranges (the deep trees' small nodes)
+// by popcounts of their words, long ones as a rank difference
+__device__ __forceinline__ uint64_t ones_between(const uint32_t* __restrict__ B,
+                                                 const unsigned long long* __restrict__ SB, uint64_t s0, uint64_t s1) {
+  if (s1 <= s0) return 0;
+  if (s1 - s0 > 512) return rank1(B, SB, s1) - rank1(B, SB, s0);
+  const uint64_t w0 = s0 >> 5, w1 = (s1 - 1) >> 5;  // words holding the first and the last bit
+  const uint32_t head = 0xffffffffu << (s0 & 31), tail = 0xffffffffu >> (31 - ((s1 - 1) & 31));
+  if (w0 == w1) return (uint32_t)__popc(B[w0] & head & tail);
+  uint64_t c = (uint32_t)__popc(B[w0] & head) + (uint32_t)__popc(B[w1] & tail);
+  for (uint64_t w = w0 + 1; w < w1; ++w) c += (uint32_t)__popc(B[w]);
+  return c;
+}
 __global__ void k_leaf_offsets(const uint2* __restrict__ tab, uint32_t L, const uint32_t* __restrict__ B,
                                const unsigned long long* __restrict__ SB, uint64_t n,
                                unsigned long long* __restrict__ C, const int32_t* __restrict__ flag) {
@@ -394,9 +407,8 @@ __global__ void k_leaf_offsets(const uint2* __restrict__ tab, uint32_t L, const 
   const uint64_t nq = 1ull << (L - 1);
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t s0 = leaf_node_start(tab, q, nq, n), s1 = leaf_node_start(tab, q + 1, nq, n);
-    const uint64_t ones = rank1(B, SB, s1) - rank1(B, SB, s0);
     C[2 * q] = s0;
-    C[2 * q + 1] = s1 - ones;
+    C[2 * q + 1] = s1 - ones_between(B, SB, s0, s1);
     if (q + 1 == nq) C[2 * nq] = n;
   }
   pdl_trigger();

@@ -99,6 +99,18 @@ __device__ __forceinline__ uint64_t pn_heads(const uint32_t (&w)[16], uint32_t p
   }
 }
 
+// nb <= 32 bits of v at global bit position pos of `bits`: a word wholly
+// inside [pos, pos + nb) stored, a partial one OR-ed
+__device__ __forceinline__ void pn_put32(uint32_t* bits, uint64_t pos, uint32_t v, uint32_t nb) {
+  if (nb == 0) return;
+  const uint64_t j = pos >> 5;
+  const uint32_t off = (uint32_t)(pos & 31u), end = off + nb;
+  const uint32_t w0 = v << off;
+  if (off == 0 && end == 32) bits[j] = w0;
+  else atomicOr(&bits[j], w0);
+  if (end > 32) atomicOr(&bits[j + 1], v >> (32 - off));  // (off > 0 here; end < 64)
+}
+
 // bits [a, a + k) of a 64-bit string as two words (k <= 64)
 __device__ __forceinline__ void pn_sub(uint64_t s, uint32_t a, uint32_t k, uint32_t (&v)[2]) {
   const uint64_t x = (a >= 64 ? 0ull : (s >> a)) & (k >= 64 ? ~0ull : ((1ull << k) - 1ull));
@@ -236,13 +248,21 @@ __global__ void __launch_bounds__(32 * PN_WARPS, 6)
       const uint64_t em = e >= 64 ? ~0ull : ((1ull << e) - 1ull);
       const uint32_t oe = (uint32_t)__popcll(m64 & em);
       const uint2 tv = __ldg(&tab[v]);
-      uint32_t sz[2], so[2];
-      pn_sub(zc, a - oa, (e - a) - (oe - oa), sz);
-      pn_sub(oc, oa, oe - oa, so);
       // zeros before position p0 + a: (p0 + a) - (P + R + oa), + ob[v]; ones: P + R + oa + Zn[v]
       // (mod 2^32: every position is < n < 2^32)
-      p2_put(B1, (uint64_t)((uint32_t)p0 + a - P - R - oa + tv.x), sz, (e - a) - (oe - oa));
-      p2_put(B1, (uint64_t)(uint32_t)(P + R + oa + tv.y), so, oe - oa);
+      const uint64_t dz = (uint32_t)p0 + a - P - R - oa + tv.x, d1 = (uint32_t)(P + R + oa + tv.y);
+      const uint32_t kz = (e - a) - (oe - oa), ko = oe - oa;
+      if constexpr (E == 64) {
+        uint32_t sz[2], so[2];
+        pn_sub(zc, a - oa, kz, sz);
+        pn_sub(oc, oa, ko, so);
+        p2_put(B1, dz, sz, kz);
+        p2_put(B1, d1, so, ko);
+      } else {  // strings of <= 32 bits
+        const uint32_t za = a - oa;
+        pn_put32(B1, dz, (za >= 32 ? 0u : (uint32_t)zc >> za) & lowmask(kz), kz);
+        pn_put32(B1, d1, (oa >= 32 ? 0u : (uint32_t)oc >> oa) & lowmask(ko), ko);
+      }
       if (e >= nvalid) break;
       a = e;
       oa = oe;
