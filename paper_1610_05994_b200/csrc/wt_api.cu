@@ -584,10 +584,11 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       int bps = 1;
       if ((e = pair2_setup(&bps)) != cudaSuccess) return fail_cuda(e, "k_pair2 setup");
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      const uint32_t grid = (uint32_t)std::min<uint64_t>((c.ntiles + wt::P2_WARPS - 1) / wt::P2_WARPS,
+      const uint64_t nwt = (n + wt::P2_WT - 1) / wt::P2_WT;  // warp tiles
+      const uint32_t grid = (uint32_t)std::min<uint64_t>((nwt + wt::P2_WARPS - 1) / wt::P2_WARPS,
                                                          (uint64_t)bps * num_sms());
       CUtensorMap tmap;
-      if (!rows128_tensor_map(&tmap, seq, n, wt::P2_TILE / 128)) return fail(WT_ERR_CUDA, "cuTensorMapEncodeTiled");
+      if (!rows128_tensor_map(&tmap, seq, n, wt::P2_WT / 128)) return fail(WT_ERR_CUDA, "cuTensorMapEncodeTiled");
       e = launch_pdl(wt::k_pair2, grid, (uint32_t)(32 * wt::P2_WARPS), wt::p2_smem_bytes(), stream,
                      reinterpret_cast<const uint8_t*>(seq), n, (uint32_t)c.ntiles, (const uint32_t*)pre,
                      (const unsigned long long*)ones0, out->bitmaps,

@@ -105,11 +105,30 @@ __device__ __forceinline__ void p2_put(uint32_t* bits, uint64_t pos, const uint3
   }
 }
 
+// nb <= 128 bits of v (v[0] low) at global bit position pos of `bits`: the
+// words wholly inside [pos, pos + nb) stored, the partial first / last OR-ed
+__device__ __forceinline__ void p2_put4(uint32_t* bits, uint64_t pos, const uint32_t (&v)[4], uint32_t nb) {
+  const uint64_t j = pos >> 5;
+  const uint32_t off = (uint32_t)(pos & 31u), end = off + nb;  // bit range [off, end) of words j ..
+#pragma unroll
+  for (uint32_t k = 0; k < 5; ++k) {
+    if (32 * k >= end) break;
+    const uint32_t lo = k ? v[k - 1] : 0u, hi = k < 4 ? v[k] : 0u;
+    const uint32_t wk = __funnelshift_lc(lo, hi, off);
+    if ((k > 0 || off == 0) && 32 * k + 32 <= end) bits[j + k] = wk;
+    else atomicOr(&bits[j + k], wk);
+  }
+}
+
 constexpr int P2_WARPS = 4;   // independent warps per CTA (they share the table)
-constexpr int P2_NB = 3;      // per-warp ring of input tiles
+#ifndef WT_P2_NB
+#define WT_P2_NB 2
+#endif
+constexpr int P2_NB = WT_P2_NB;  // per-warp ring of input tiles
+constexpr int P2_WT = 4096;      // bytes (symbols) per warp tile: one 128-byte row per lane, two level tiles
 
 struct P2Smem {
-  alignas(1024) uint4 ring[P2_WARPS][P2_NB][P2_TILE / 16];  // 16 rows of 128 bytes per tile, 128-byte swizzle
+  alignas(1024) uint4 ring[P2_WARPS][P2_NB][P2_WT / 16];  // 32 rows of 128 bytes per tile, 128-byte swizzle
   uint2 lut[256];
   alignas(8) unsigned long long bar[P2_WARPS][P2_NB];
 };
@@ -125,10 +144,13 @@ __device__ __forceinline__ void p2_tma(void* dst, const void* tmap, int32_t row,
 
 // B_0, SB_0 and B_1 (which must be zero on entry) of a two-level tree of n
 // 1-byte symbols.  P2_WARPS independent warps per CTA (no block barrier after
-// the table is built); tiles round-robin over all warps.  Each warp streams
-// its tiles through a ring of P2_NB buffers filled by TMA tensor copies (S as
-// rows of 128 bytes, 128-byte swizzle: lane l owns half of row l/2 and reads
-// its four 16-byte chunks from distinct banks).
+// the table is built); warp tiles of 4096 symbols (two level tiles, whose
+// prefixes pre[t] the scan produced) round-robin over all warps.  Each warp
+// streams its tiles through a ring of P2_NB buffers filled by TMA tensor
+// copies (S as rows of 128 bytes, 128-byte swizzle): lane l owns row l, 128
+// consecutive symbols, and reads its eight 16-byte chunks in an order in which
+// the lanes of a load hit distinct banks.  The lane's two strings (<= 128 bits
+// each) are stored with their inner words plain, the first / last OR-ed.
 __global__ void __launch_bounds__(32 * P2_WARPS, 6)
     k_pair2(const uint8_t* __restrict__ S, uint64_t n, uint32_t ntiles, const uint32_t* __restrict__ pre,
             const unsigned long long* __restrict__ ones0, uint32_t* __restrict__ B0,
@@ -144,65 +166,90 @@ __global__ void __launch_bounds__(32 * P2_WARPS, 6)
   }
   __syncthreads();
   const uint32_t gw = blockIdx.x * P2_WARPS + wid, nw = gridDim.x * P2_WARPS;  // this warp, all warps
+  const uint32_t nwt = (uint32_t)((n + P2_WT - 1) / P2_WT);                   // warp tiles
   const uint64_t full_bytes = n & ~127ull;  // the tensor map's whole rows
   auto issue = [&](uint32_t it) {           // lane 0: the warp's it-th tile into ring slot it % P2_NB
     const uint32_t tile = gw + it * nw;
-    if (tile >= ntiles) return;
+    if (tile >= nwt) return;
     const int b = (int)(it % P2_NB);
     fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&sm.bar[wid][b], P2_TILE);  // (rows past the tensor's end are zero-filled)
-    p2_tma(sm.ring[wid][b], &tmap, (int32_t)(tile * (P2_TILE / 128)), &sm.bar[wid][b]);
+    mbar_arrive_expect_tx(&sm.bar[wid][b], P2_WT);  // (rows past the tensor's end are zero-filled)
+    p2_tma(sm.ring[wid][b], &tmap, (int32_t)(tile * (P2_WT / 128)), &sm.bar[wid][b]);
   };
   pdl_wait();  // the tile prefixes, ones0, the zero-filled B_1 (and no range error)
   if (*flag) return;
   if (lane == 0)
     for (uint32_t b = 0; b < P2_NB; ++b) issue(b);
   const uint64_t Z = n - *ones0;  // the zeros of level 0: B_1's ones' run starts here
-  const uint32_t row = lane >> 1, swz = row & 7u;
+  const uint32_t swz = lane & 7u;
   for (uint32_t it = 0;; ++it) {
     const uint32_t tile = gw + it * nw;
-    if (tile >= ntiles) break;
+    if (tile >= nwt) break;
     const int b = (int)(it % P2_NB);
-    const uint64_t T0 = (uint64_t)tile * P2_TILE;
-    const uint64_t p0 = T0 + 64ull * lane;
-    const uint32_t P = __ldg(&pre[tile]);  // level-0 ones before the tile (issued before the wait)
+    const uint64_t T0 = (uint64_t)tile * P2_WT;
+    const uint64_t p0 = T0 + 128ull * lane;
+    const uint32_t pt = 2 * tile + (lane >> 4);                // the lane's level tile
+    const uint32_t P = pt < ntiles ? __ldg(&pre[pt]) : 0u;     // level-0 ones before it
     mbar_wait(&sm.bar[wid][b], (it / P2_NB) & 1u);
     unsigned char* const buf = reinterpret_cast<unsigned char*>(sm.ring[wid][b]);
-    if (T0 + P2_TILE > full_bytes && full_bytes < n) {  // the partial last row: into its swizzled place
+    if (T0 + P2_WT > full_bytes && full_bytes < n) {  // the partial last row: into its swizzled place
       for (uint64_t g = full_bytes + lane; g < n; g += 32) {
         const uint32_t off = (uint32_t)(g - T0), r = off >> 7, c = (off >> 4) & 7u;
         buf[r * 128 + ((c ^ (r & 7u)) << 4) + (off & 15u)] = S[g];
       }
       __syncwarp();
     }
-    uint32_t w[16];
+    const uint32_t nvalid = p0 >= n ? 0u : (uint32_t)min((uint64_t)128, n - p0);
+    uint32_t m[4];
+    uint64_t zc[2], oc[2];
+    uint32_t nzh[2], noh[2];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t c = 4 * (lane & 1u) + (uint32_t)k;
-      const uint4 q = *reinterpret_cast<const uint4*>(buf + row * 128 + ((c ^ swz) << 4));
-      w[4 * k] = q.x, w[4 * k + 1] = q.y, w[4 * k + 2] = q.z, w[4 * k + 3] = q.w;
+    for (int h = 0; h < 2; ++h) {  // the lane's two 64-symbol halves
+      uint32_t w[16];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t c = 4 * (uint32_t)h + (uint32_t)k;
+        const uint4 q = *reinterpret_cast<const uint4*>(buf + lane * 128 + ((c ^ swz) << 4));
+        w[4 * k] = q.x, w[4 * k + 1] = q.y, w[4 * k + 2] = q.z, w[4 * k + 3] = q.w;
+      }
+      const uint32_t hv = nvalid > 64u * h ? min(nvalid - 64u * h, 64u) : 0u;
+      uint32_t Zs[2], Os[2];
+      p2_quarter(w, min(hv, 32u), sm.lut, m[2 * h], Zs[0], Os[0]);
+      p2_quarter(w + 8, hv > 32 ? hv - 32 : 0u, sm.lut, m[2 * h + 1], Zs[1], Os[1]);
+      const uint32_t o0 = (uint32_t)__popc(m[2 * h]);
+      const uint32_t z0 = min(hv, 32u) - o0;
+      noh[h] = o0 + (uint32_t)__popc(m[2 * h + 1]);
+      nzh[h] = hv - noh[h];
+      zc[h] = (uint64_t)Zs[0] | ((uint64_t)Zs[1] << z0);
+      oc[h] = (uint64_t)Os[0] | ((uint64_t)Os[1] << o0);
     }
     __syncwarp();  // every lane has read the slot: refill it
     if (lane == 0) issue(it + P2_NB);
-    const uint32_t nvalid = p0 >= n ? 0u : (uint32_t)min((uint64_t)64, n - p0);
-    uint32_t m[2], Zs[2], Os[2];
-    p2_quarter(w, min(nvalid, 32u), sm.lut, m[0], Zs[0], Os[0]);
-    p2_quarter(w + 8, nvalid > 32 ? nvalid - 32 : 0u, sm.lut, m[1], Zs[1], Os[1]);
     // level-0 words (the last tile's padding words: zero)
-    if (p0 < ((n + 511) & ~511ull)) *reinterpret_cast<uint2*>(B0 + p0 / 32) = make_uint2(m[0], m[1]);
-    const uint32_t o0 = (uint32_t)__popc(m[0]), o1 = (uint32_t)__popc(m[1]);
-    const uint32_t no = o0 + o1;
+    if (p0 < ((n + 511) & ~511ull)) *reinterpret_cast<uint4*>(B0 + p0 / 32) = make_uint4(m[0], m[1], m[2], m[3]);
+    const uint32_t no = noh[0] + noh[1];
     const uint32_t inc = warp_incl_scan_u32(no);
-    const uint32_t R = inc - no;  // level-0 ones before the lane, inside the tile
-    if ((lane & 7u) == 0 && p0 < n) SB0[p0 / 512] = P + R;
-    if (tile + 1 == ntiles && lane == 31) SB0[nsb - 1] = P + inc;
-    // the lane's two 64-bit strings: quarter 1's bits after quarter 0's
-    const uint32_t z0 = min(nvalid, 32u) - o0, nzl = nvalid - no;
-    const uint64_t zc = (uint64_t)Zs[0] | ((uint64_t)Zs[1] << z0), oc = (uint64_t)Os[0] | ((uint64_t)Os[1] << o0);
-    const uint32_t Zv[2] = {(uint32_t)zc, (uint32_t)(zc >> 32)};
-    const uint32_t Ov[2] = {(uint32_t)oc, (uint32_t)(oc >> 32)};
-    p2_put(B1, T0 - P + (64ull * lane - R), Zv, nzl);   // zeros before the lane: positions - ones
-    p2_put(B1, Z + P + R, Ov, no);
+    const uint32_t h15 = __shfl_sync(FULL, inc, 15);
+    const uint32_t hb = (lane >> 4) ? h15 : 0u;  // (lanes 16..31: the second level tile)
+    const uint32_t R = inc - no - hb;  // level-0 ones before the lane, inside its level tile
+    const uint32_t P0 = __shfl_sync(FULL, P, 0);
+    if ((lane & 3u) == 0 && p0 < n) SB0[p0 / 512] = P + R;
+    if (tile + 1 == nwt && lane == 31) SB0[nsb - 1] = P0 + inc;
+    // the lane's two strings of <= 128 bits: half 1's bits after half 0's
+    uint32_t Zv[4], Ov[4];
+    {
+      const uint64_t lo = zc[0] | (nzh[0] >= 64 ? 0ull : (zc[1] << nzh[0]));
+      const uint64_t hi = nzh[0] == 0 ? 0ull : (nzh[0] >= 64 ? zc[1] : (zc[1] >> (64 - nzh[0])));
+      Zv[0] = (uint32_t)lo, Zv[1] = (uint32_t)(lo >> 32), Zv[2] = (uint32_t)hi, Zv[3] = (uint32_t)(hi >> 32);
+    }
+    {
+      const uint64_t lo = oc[0] | (noh[0] >= 64 ? 0ull : (oc[1] << noh[0]));
+      const uint64_t hi = noh[0] == 0 ? 0ull : (noh[0] >= 64 ? oc[1] : (oc[1] >> (64 - noh[0])));
+      Ov[0] = (uint32_t)lo, Ov[1] = (uint32_t)(lo >> 32), Ov[2] = (uint32_t)hi, Ov[3] = (uint32_t)(hi >> 32);
+    }
+    const uint32_t nzl = nvalid - no;
+    if (nzl) p2_put4(B1, p0 - P - R, Zv, nzl);   // zeros before the lane: positions - ones
+    if (no) p2_put4(B1, Z + P + R, Ov, no);
   }
   pdl_trigger();
 }

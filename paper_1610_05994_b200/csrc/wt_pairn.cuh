@@ -63,7 +63,12 @@ __device__ __forceinline__ uint32_t pn_index(const uint32_t (&w)[16], int g) {
     const uint32_t x = (w[2 * g] & 0x00030003u) | ((w[2 * g + 1] & 0x00030003u) << 4);
     return (x | (x >> 14)) & 0xffu;
   } else {
-    return (w[4 * g] & 3u) | ((w[4 * g + 1] & 3u) << 2) | ((w[4 * g + 2] & 3u) << 4) | ((w[4 * g + 3] & 3u) << 6);
+    // the four low bytes into one word (three byte permutes), then as for bytes
+    uint32_t a, b, x;
+    asm("prmt.b32 %0, %1, %2, 0x0040;" : "=r"(a) : "r"(w[4 * g]), "r"(w[4 * g + 1]));      // [w0.b0, w1.b0, ..]
+    asm("prmt.b32 %0, %1, %2, 0x0040;" : "=r"(b) : "r"(w[4 * g + 2]), "r"(w[4 * g + 3]));  // [w2.b0, w3.b0, ..]
+    asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(x) : "r"(a), "r"(b));                       // [w0, w1, w2, w3].b0
+    return ((x & 0x03030303u) * 0x01041040u) >> 24;
   }
 }
 
@@ -180,8 +185,7 @@ __global__ void __launch_bounds__(32 * PN_WARPS, 6)
       const uint4 q = *reinterpret_cast<const uint4*>(buf + row * 128 + ((c ^ swz) << 4));
       w[4 * k] = q.x, w[4 * k + 1] = q.y, w[4 * k + 2] = q.z, w[4 * k + 3] = q.w;
     }
-    __syncwarp();  // every lane has read the slot: refill it
-    if (lane == 0) issue(it + PN_NB);
+
     const uint32_t nvalid = p0 >= n ? 0u : (uint32_t)min((uint64_t)E, n - p0);
 
     // level-(L-2) bits m (position order) and the zeros' / ones' bit-0 strings
@@ -234,41 +238,47 @@ __global__ void __launch_bounds__(32 * PN_WARPS, 6)
     const uint32_t R = inc - ones;  // level-(L-2) ones before the lane, inside the tile
     if ((p0 & 511u) == 0 && p0 < n) sb[p0 / 512] = P + R;
     if (tile + 1 == ntiles && lane == 31) sb[nsb - 1] = P + inc;
-    if (nvalid == 0) continue;
-
     // the lane's runs of one node each: [a, e) with node v
     uint32_t v = pn_sym_c<T, 0>(w) >> 2;
-    const uint32_t vlast = (nvalid == (uint32_t)E ? pn_sym_c<T, E - 1>(w) : pn_sym<T>(w, nvalid - 1)) >> 2;
-    uint64_t heads = 0;  // bit j: symbol j starts a new node (j >= 1)
-    if (v != vlast) heads = pn_heads<T>(w, v) & (nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull));
-    const uint64_t m64 = (uint64_t)m[0] | (NH == 2 ? ((uint64_t)m[NH - 1] << 32) : 0ull);
-    uint32_t a = 0, oa = 0;  // run start, level-(L-2) ones before it in the lane
-    for (;;) {
-      const uint32_t e = heads ? (uint32_t)(__ffsll((long long)heads) - 1) : nvalid;
-      const uint64_t em = e >= 64 ? ~0ull : ((1ull << e) - 1ull);
-      const uint32_t oe = (uint32_t)__popcll(m64 & em);
-      const uint2 tv = __ldg(&tab[v]);
-      // zeros before position p0 + a: (p0 + a) - (P + R + oa), + ob[v]; ones: P + R + oa + Zn[v]
-      // (mod 2^32: every position is < n < 2^32)
-      const uint64_t dz = (uint32_t)p0 + a - P - R - oa + tv.x, d1 = (uint32_t)(P + R + oa + tv.y);
-      const uint32_t kz = (e - a) - (oe - oa), ko = oe - oa;
-      if constexpr (E == 64) {
-        uint32_t sz[2], so[2];
-        pn_sub(zc, a - oa, kz, sz);
-        pn_sub(oc, oa, ko, so);
-        p2_put(B1, dz, sz, kz);
-        p2_put(B1, d1, so, ko);
-      } else {  // strings of <= 32 bits
-        const uint32_t za = a - oa;
-        pn_put32(B1, dz, (za >= 32 ? 0u : (uint32_t)zc >> za) & lowmask(kz), kz);
-        pn_put32(B1, d1, (oa >= 32 ? 0u : (uint32_t)oc >> oa) & lowmask(ko), ko);
+    const uint32_t vlast =
+        (nvalid == (uint32_t)E ? pn_sym_c<T, E - 1>(w) : pn_sym<T>(w, nvalid ? nvalid - 1 : 0u)) >> 2;
+    if (nvalid) {
+      uint64_t heads = 0;  // bit j: symbol j starts a new node (j >= 1)
+      if (v != vlast) heads = pn_heads<T>(w, v) & (nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull));
+      const uint64_t m64 = (uint64_t)m[0] | (NH == 2 ? ((uint64_t)m[NH - 1] << 32) : 0ull);
+      uint32_t a = 0, oa = 0;  // run start, level-(L-2) ones before it in the lane
+      for (;;) {
+        const uint32_t e = heads ? (uint32_t)(__ffsll((long long)heads) - 1) : nvalid;
+        const uint64_t em = e >= 64 ? ~0ull : ((1ull << e) - 1ull);
+        const uint32_t oe = (uint32_t)__popcll(m64 & em);
+        const uint2 tv = __ldg(&tab[v]);
+        // zeros before position p0 + a: (p0 + a) - (P + R + oa), + ob[v]; ones: P + R + oa + Zn[v]
+        // (mod 2^32: every position is < n < 2^32)
+        const uint64_t dz = (uint32_t)p0 + a - P - R - oa + tv.x, d1 = (uint32_t)(P + R + oa + tv.y);
+        const uint32_t kz = (e - a) - (oe - oa), ko = oe - oa;
+        if constexpr (E == 64) {
+          uint32_t sz[2], so[2];
+          pn_sub(zc, a - oa, kz, sz);
+          pn_sub(oc, oa, ko, so);
+          p2_put(B1, dz, sz, kz);
+          p2_put(B1, d1, so, ko);
+        } else {  // strings of <= 32 bits
+          const uint32_t za = a - oa;
+          pn_put32(B1, dz, (za >= 32 ? 0u : (uint32_t)zc >> za) & lowmask(kz), kz);
+          pn_put32(B1, d1, (oa >= 32 ? 0u : (uint32_t)oc >> oa) & lowmask(ko), ko);
+        }
+        if (e >= nvalid) break;
+        a = e;
+        oa = oe;
+        {  // node of symbol e: its bytes in the (swizzled) ring slot, still unreleased
+          const uint32_t off = (uint32_t)(E * lane + e) * (uint32_t)sizeof(T), r = off >> 7, c = (off >> 4) & 7u;
+          v = (uint32_t)*reinterpret_cast<const T*>(buf + r * 128 + ((c ^ (r & 7u)) << 4) + (off & 15u)) >> 2;
+        }
+        heads &= heads - 1;
       }
-      if (e >= nvalid) break;
-      a = e;
-      oa = oe;
-      v = pn_sym<T>(w, e) >> 2;
-      heads &= heads - 1;
     }
+    __syncwarp();  // every lane is done with the slot: refill it
+    if (lane == 0) issue(it + PN_NB);
   }
   pdl_trigger();
 }
