@@ -603,10 +603,12 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       int bps = 1;
       if ((e = pairn_setup<T>(&bps)) != cudaSuccess) return fail_cuda(e, "k_pairn setup");
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      const uint32_t grid = (uint32_t)std::min<uint64_t>((c.ntiles + wt::PN_WARPS - 1) / wt::PN_WARPS,
+      const uint64_t nwt = (n + wt::PnCfg<T>::WT - 1) / wt::PnCfg<T>::WT;  // warp tiles
+      const uint32_t grid = (uint32_t)std::min<uint64_t>((nwt + wt::PN_WARPS - 1) / wt::PN_WARPS,
                                                          (uint64_t)bps * num_sms());
       CUtensorMap tmap;
-      if (!rows128_tensor_map(&tmap, in, n * sizeof(T), 16)) return fail(WT_ERR_CUDA, "cuTensorMapEncodeTiled");
+      if (!rows128_tensor_map(&tmap, in, n * sizeof(T), wt::PN_WT / 128))
+        return fail(WT_ERR_CUDA, "cuTensorMapEncodeTiled");
       e = launch_pdl(wt::k_pairn<T>, grid, (uint32_t)(32 * wt::PN_WARPS), wt::pn_smem_bytes(), stream, in,
                      (uint32_t)n, (uint32_t)c.ntiles, (const uint32_t*)pre, (const uint2*)(tab + ((1ull << l) - 1)),
                      out->bitmaps + (uint64_t)l * c.words, (uint32_t)c.words,

@@ -36,17 +36,20 @@ namespace wt {
 template <typename T>
 struct PnCfg {
   static constexpr int W = (int)sizeof(T);
-  static constexpr int E = 64 / W;          // symbols per lane
-  static constexpr int TILE = 32 * E;       // symbols per tile (= LvTile<T>::TILE, 2 KiB)
-  static constexpr int G = E / 4;           // groups of 4 symbols per lane
-  static constexpr int NH = E > 32 ? 2 : 1;  // 32-symbol halves per lane
-  static constexpr int GH = G / NH;         // groups per half
+  static constexpr int EH = 64 / W;         // symbols per half lane (64 bytes)
+  static constexpr int E = 2 * EH;          // symbols per lane: one 128-byte row
+  static constexpr int LT = 16 * E;         // symbols per level tile (= LvTile<T>::TILE, 2 KiB): 16 lanes
+  static constexpr int WT = 32 * E;         // symbols per warp tile (4 KiB): two level tiles
+  static constexpr int G = EH / 4;          // groups of 4 symbols per half
+  static constexpr int NH = EH > 32 ? 2 : 1;  // 32-symbol words of a half's bits
+  static constexpr int GH = G / NH;         // groups per word
 };
 constexpr int PN_WARPS = 4;  // independent warps per CTA (they share the table)
-constexpr int PN_NB = 3;     // per-warp ring of input tiles
+constexpr int PN_NB = 2;     // per-warp ring of input tiles
+constexpr int PN_WT = 4096;  // bytes per warp tile
 
 struct PnSmem {
-  alignas(1024) uint4 ring[PN_WARPS][PN_NB][2048 / 16];  // 16 rows of 128 bytes per tile, 128-byte swizzle
+  alignas(1024) uint4 ring[PN_WARPS][PN_NB][PN_WT / 16];  // 32 rows of 128 bytes per tile, 128-byte swizzle
   uint2 lut[256];
   alignas(8) unsigned long long bar[PN_WARPS][PN_NB];
 };
@@ -93,14 +96,13 @@ __device__ __forceinline__ uint32_t pn_sym_c(const uint32_t (&w)[16]) {
   else return w[J];
 }
 // bit j of the lane: symbol j's node differs from symbol j-1's (j >= 1)
-template <typename T, int J = 1>
+template <typename T, int J, int E>
 __device__ __forceinline__ uint64_t pn_heads(const uint32_t (&w)[16], uint32_t prev) {
-  constexpr int E = 64 / (int)sizeof(T);
   if constexpr (J >= E) {
     return 0ull;
   } else {
     const uint32_t nd = pn_sym_c<T, J>(w) >> 2;
-    return ((uint64_t)(nd != prev) << J) | pn_heads<T, J + 1>(w, nd);
+    return ((uint64_t)(nd != prev) << J) | pn_heads<T, J + 1, E>(w, nd);
   }
 }
 
@@ -123,9 +125,76 @@ __device__ __forceinline__ void pn_sub(uint64_t s, uint32_t a, uint32_t k, uint3
   v[1] = (uint32_t)(x >> 32);
 }
 
+// one half lane (64 bytes, EH symbols, `nv` of them real): level-(L-2) bits m
+// (position order), the zeros' / ones' bit-0 strings and their lengths
+template <typename T>
+__device__ __forceinline__ void pn_half(const uint32_t (&w)[16], uint32_t nv, const uint2* lut,
+                                        uint32_t (&m)[PnCfg<T>::NH], uint64_t& zc, uint64_t& oc, uint32_t& nz,
+                                        uint32_t& no) {
+  using C = PnCfg<T>;
+  constexpr int EH = C::EH, NH = C::NH, GH = C::GH;
+  zc = oc = 0;
+  nz = no = 0;
+  if (nv == (uint32_t)EH) {
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      uint32_t mm = 0, Zs = 0, Os = 0, pz = 1, po = 1;
+#pragma unroll
+      for (int g = 0; g < GH; ++g) {
+        const uint2 e = lut[pn_index<T>(w, h * GH + g)];
+        mm |= ((e.x >> 16) & 15u) << (4 * g);
+        Zs += (e.x & 15u) * pz;
+        Os += ((e.x >> 8) & 15u) * po;
+        pz *= e.y & 0xffu;
+        po *= e.y >> 8;
+      }
+      m[h] = mm;
+      const uint32_t o = (uint32_t)__popc(mm), z = (uint32_t)(4 * GH) - o;
+      zc |= (uint64_t)Zs << nz;
+      oc |= (uint64_t)Os << no;
+      nz += z;
+      no += o;
+    }
+  } else {
+#pragma unroll
+    for (int h = 0; h < NH; ++h) m[h] = 0;
+    for (uint32_t j = 0; j < nv; ++j) {
+      const uint32_t s = pn_sym<T>(w, j);
+      const uint32_t b1 = (s >> 1) & 1u, b0 = s & 1u;
+      if (NH == 1 || j < 32) m[0] |= b1 << (j & 31);
+      else m[NH - 1] |= b1 << (j & 31);
+      if (b1) oc |= (uint64_t)b0 << no++;
+      else zc |= (uint64_t)b0 << nz++;
+    }
+  }
+}
+
+// nb bits (<= 2 EH <= 128) of the concatenation of two strings a (na bits) and
+// b at global bit position pos
+template <int EH>
+__device__ __forceinline__ void pn_put_cat(uint32_t* bits, uint64_t pos, uint64_t a, uint32_t na, uint64_t b,
+                                           uint32_t nb) {
+  if (na + nb == 0) return;
+  if constexpr (EH == 64) {  // 128-bit strings
+    const uint64_t lo = a | (na >= 64 ? 0ull : (b << na));
+    const uint64_t hi = na == 0 ? 0ull : (na >= 64 ? b : (b >> (64 - na)));
+    const uint32_t v[4] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32)};
+    p2_put4(bits, pos, v, na + nb);
+  } else if constexpr (EH == 32) {  // 64-bit strings
+    const uint64_t x = a | (b << na);
+    const uint32_t v[2] = {(uint32_t)x, (uint32_t)(x >> 32)};
+    p2_put(bits, pos, v, na + nb);
+  } else {  // 32-bit strings
+    pn_put32(bits, pos, (uint32_t)a | ((uint32_t)b << na), na + nb);
+  }
+}
+
 // B_{L-2} (bits), its superblocks and B_{L-1} (must be zero on entry) from
 // T_{L-2} (n symbols, n < 2^32), the level-(L-2) tile prefixes pre[t] and node
-// table tab[v] = {ob[v], Zn[v]}.
+// table tab[v] = {ob[v], Zn[v]}.  Warp tiles of 4 KiB (two level tiles); lane
+// l owns row l (128 bytes), processed as two 64-byte halves.  A lane inside
+// one node stores its two strings whole; a lane that spans nodes splits each
+// half's strings at the node changes.
 template <typename T>
 __global__ void __launch_bounds__(32 * PN_WARPS, 6)
     k_pairn(const T* __restrict__ in, uint32_t n, uint32_t ntiles, const uint32_t* __restrict__ pre,
@@ -133,7 +202,7 @@ __global__ void __launch_bounds__(32 * PN_WARPS, 6)
             unsigned long long* __restrict__ sb, uint32_t nsb, uint32_t* __restrict__ B1,
             const int32_t* __restrict__ flag, const __grid_constant__ CUtensorMap tmap) {
   using C = PnCfg<T>;
-  constexpr int E = C::E, TILE = C::TILE, NH = C::NH, GH = C::GH;
+  constexpr int E = C::E, EH = C::EH, WT = C::WT, NH = C::NH;
   extern __shared__ unsigned char pn_raw[];
   PnSmem& sm = *reinterpret_cast<PnSmem*>((reinterpret_cast<uintptr_t>(pn_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -144,137 +213,123 @@ __global__ void __launch_bounds__(32 * PN_WARPS, 6)
   }
   __syncthreads();
   const uint32_t gw = blockIdx.x * PN_WARPS + wid, nw = gridDim.x * PN_WARPS;
+  const uint32_t nwt = (uint32_t)(((uint64_t)n + WT - 1) / WT);  // warp tiles
   const uint64_t nbytes = (uint64_t)n * sizeof(T);
   const uint64_t full_bytes = nbytes & ~127ull;  // the tensor map's whole rows
   auto issue = [&](uint32_t it) {
     const uint32_t tile = gw + it * nw;
-    if (tile >= ntiles) return;
+    if (tile >= nwt) return;
     const int b = (int)(it % PN_NB);
     fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&sm.bar[wid][b], 2048);  // (rows past the tensor's end are zero-filled)
-    p2_tma(sm.ring[wid][b], &tmap, (int32_t)(tile * 16u), &sm.bar[wid][b]);
+    mbar_arrive_expect_tx(&sm.bar[wid][b], PN_WT);  // (rows past the tensor's end are zero-filled)
+    p2_tma(sm.ring[wid][b], &tmap, (int32_t)(tile * (PN_WT / 128)), &sm.bar[wid][b]);
   };
   pdl_wait();  // T_{L-2}, the tile prefixes, the node table, the zero-filled B_{L-1}
   if (*flag) return;
   if (lane == 0)
     for (uint32_t b = 0; b < PN_NB; ++b) issue(b);
-  const uint32_t row = lane >> 1, swz = row & 7u;
+  const uint32_t swz = lane & 7u;
   const uint64_t padded = ((uint64_t)n + 511) & ~511ull;
   const unsigned char* inb = reinterpret_cast<const unsigned char*>(in);
   for (uint32_t it = 0;; ++it) {
     const uint32_t tile = gw + it * nw;
-    if (tile >= ntiles) break;
+    if (tile >= nwt) break;
     const int b = (int)(it % PN_NB);
-    const uint32_t T0 = tile * (uint32_t)TILE;
-    const uint64_t p0 = (uint64_t)T0 + (uint32_t)E * lane;  // the lane's first position
-    const uint32_t P = __ldg(&pre[tile]);
+    const uint64_t T0 = (uint64_t)tile * WT;
+    const uint64_t p0 = T0 + (uint32_t)E * lane;  // the lane's first position
+    const uint32_t lt = 2 * tile + (lane >> 4);  // its level tile
+    const uint32_t P = lt < ntiles ? __ldg(&pre[lt]) : 0u;
     mbar_wait(&sm.bar[wid][b], (it / PN_NB) & 1u);
     unsigned char* const buf = reinterpret_cast<unsigned char*>(sm.ring[wid][b]);
-    const uint64_t B0 = (uint64_t)T0 * sizeof(T);
-    if (B0 + 2048 > full_bytes && full_bytes < nbytes) {  // the partial last row: into its swizzled place
+    const uint64_t B0 = T0 * sizeof(T);
+    if (B0 + PN_WT > full_bytes && full_bytes < nbytes) {  // the partial last row: into its swizzled place
       for (uint64_t g = full_bytes + lane; g < nbytes; g += 32) {
         const uint32_t off = (uint32_t)(g - B0), r = off >> 7, c = (off >> 4) & 7u;
         buf[r * 128 + ((c ^ (r & 7u)) << 4) + (off & 15u)] = inb[g];
       }
       __syncwarp();
     }
-    uint32_t w[16];
+    const uint32_t nvalid = p0 >= n ? 0u : (uint32_t)min((uint64_t)E, n - p0);
+    const uint32_t nv0 = min(nvalid, (uint32_t)EH), nv1 = nvalid - nv0;
+    uint32_t w0[16], w1[16];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t c = 4 * (lane & 1u) + (uint32_t)k;
-      const uint4 q = *reinterpret_cast<const uint4*>(buf + row * 128 + ((c ^ swz) << 4));
-      w[4 * k] = q.x, w[4 * k + 1] = q.y, w[4 * k + 2] = q.z, w[4 * k + 3] = q.w;
+      const uint4 q0 = *reinterpret_cast<const uint4*>(buf + lane * 128 + (((uint32_t)k ^ swz) << 4));
+      const uint4 q1 = *reinterpret_cast<const uint4*>(buf + lane * 128 + (((uint32_t)(k + 4) ^ swz) << 4));
+      w0[4 * k] = q0.x, w0[4 * k + 1] = q0.y, w0[4 * k + 2] = q0.z, w0[4 * k + 3] = q0.w;
+      w1[4 * k] = q1.x, w1[4 * k + 1] = q1.y, w1[4 * k + 2] = q1.z, w1[4 * k + 3] = q1.w;
     }
-
-    const uint32_t nvalid = p0 >= n ? 0u : (uint32_t)min((uint64_t)E, n - p0);
-
-    // level-(L-2) bits m (position order) and the zeros' / ones' bit-0 strings
-    uint32_t m[NH];
-    uint64_t zc = 0, oc = 0;
-    uint32_t nz = 0, no = 0;  // string lengths
-    if (nvalid == (uint32_t)E) {
-#pragma unroll
-      for (int h = 0; h < NH; ++h) {
-        uint32_t mm = 0, Zs = 0, Os = 0, pz = 1, po = 1;
-#pragma unroll
-        for (int g = 0; g < GH; ++g) {
-          const uint2 e = sm.lut[pn_index<T>(w, h * GH + g)];
-          mm |= ((e.x >> 16) & 15u) << (4 * g);
-          Zs += (e.x & 15u) * pz;
-          Os += ((e.x >> 8) & 15u) * po;
-          pz *= e.y & 0xffu;
-          po *= e.y >> 8;
-        }
-        m[h] = mm;
-        const uint32_t o = (uint32_t)__popc(mm), z = (uint32_t)(4 * GH) - o;
-        zc |= (uint64_t)Zs << nz;
-        oc |= (uint64_t)Os << no;
-        nz += z;
-        no += o;
-      }
-    } else {
-#pragma unroll
-      for (int h = 0; h < NH; ++h) m[h] = 0;
-      for (uint32_t j = 0; j < nvalid; ++j) {
-        const uint32_t s = pn_sym<T>(w, j);
-        const uint32_t b1 = (s >> 1) & 1u, b0 = s & 1u;
-        if (NH == 1 || j < 32) m[0] |= b1 << (j & 31);
-        else m[NH - 1] |= b1 << (j & 31);
-        if (b1) oc |= (uint64_t)b0 << no++;
-        else zc |= (uint64_t)b0 << nz++;
-      }
-    }
+    uint32_t m0[NH], m1[NH];
+    uint64_t zc0, oc0, zc1, oc1;
+    uint32_t nz0, no0, nz1, no1;
+    pn_half<T>(w0, nv0, sm.lut, m0, zc0, oc0, nz0, no0);
+    pn_half<T>(w1, nv1, sm.lut, m1, zc1, oc1, nz1, no1);
     // bitmap words of level L-2 (the last tile's padding words: zero)
-    if constexpr (E == 64) {
-      if (p0 < padded) *reinterpret_cast<uint2*>(bits + p0 / 32) = make_uint2(m[0], m[NH - 1]);
-    } else if constexpr (E == 32) {
-      if (p0 < padded) bits[p0 / 32] = m[0];
-    } else {  // E == 16: two lanes per word
-      const uint32_t wv = m[0] | (__shfl_down_sync(FULL, m[0], 1) << 16);
-      if ((lane & 1) == 0 && p0 < padded) bits[p0 / 32] = wv;
+    if (p0 < padded) {
+      if constexpr (EH == 64) *reinterpret_cast<uint4*>(bits + p0 / 32) = make_uint4(m0[0], m0[1], m1[0], m1[1]);
+      else if constexpr (EH == 32) *reinterpret_cast<uint2*>(bits + p0 / 32) = make_uint2(m0[0], m1[0]);
+      else bits[p0 / 32] = m0[0] | (m1[0] << 16);
     }
-    const uint32_t ones = (uint32_t)__popc(m[0]) + (NH == 2 ? (uint32_t)__popc(m[NH - 1]) : 0u);
+    const uint32_t ones = no0 + no1;
     const uint32_t inc = warp_incl_scan_u32(ones);
-    const uint32_t R = inc - ones;  // level-(L-2) ones before the lane, inside the tile
+    const uint32_t h15 = __shfl_sync(FULL, inc, 15);
+    const uint32_t R = inc - ones - ((lane >> 4) ? h15 : 0u);  // ones before the lane, inside its level tile
+    const uint32_t P0 = __shfl_sync(FULL, P, 0);
     if ((p0 & 511u) == 0 && p0 < n) sb[p0 / 512] = P + R;
-    if (tile + 1 == ntiles && lane == 31) sb[nsb - 1] = P + inc;
-    // the lane's runs of one node each: [a, e) with node v
-    uint32_t v = pn_sym_c<T, 0>(w) >> 2;
-    const uint32_t vlast =
-        (nvalid == (uint32_t)E ? pn_sym_c<T, E - 1>(w) : pn_sym<T>(w, nvalid ? nvalid - 1 : 0u)) >> 2;
+    if (tile + 1 == nwt && lane == 31) sb[nsb - 1] = P0 + inc;
     if (nvalid) {
-      uint64_t heads = 0;  // bit j: symbol j starts a new node (j >= 1)
-      if (v != vlast) heads = pn_heads<T>(w, v) & (nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull));
-      const uint64_t m64 = (uint64_t)m[0] | (NH == 2 ? ((uint64_t)m[NH - 1] << 32) : 0ull);
-      uint32_t a = 0, oa = 0;  // run start, level-(L-2) ones before it in the lane
-      for (;;) {
-        const uint32_t e = heads ? (uint32_t)(__ffsll((long long)heads) - 1) : nvalid;
-        const uint64_t em = e >= 64 ? ~0ull : ((1ull << e) - 1ull);
-        const uint32_t oe = (uint32_t)__popcll(m64 & em);
+      const uint32_t v = pn_sym_c<T, 0>(w0) >> 2;
+      const uint32_t vlast =
+          (nv1 == (uint32_t)EH ? pn_sym_c<T, EH - 1>(w1) : nv1 ? pn_sym<T>(w1, nv1 - 1) : pn_sym<T>(w0, nv0 - 1)) >> 2;
+      const uint32_t pr = (uint32_t)p0 - P - R;  // zeros before the lane (mod 2^32: positions < n < 2^32)
+      if (v == vlast) {  // the lane inside one node: both strings whole
         const uint2 tv = __ldg(&tab[v]);
-        // zeros before position p0 + a: (p0 + a) - (P + R + oa), + ob[v]; ones: P + R + oa + Zn[v]
-        // (mod 2^32: every position is < n < 2^32)
-        const uint64_t dz = (uint32_t)p0 + a - P - R - oa + tv.x, d1 = (uint32_t)(P + R + oa + tv.y);
-        const uint32_t kz = (e - a) - (oe - oa), ko = oe - oa;
-        if constexpr (E == 64) {
-          uint32_t sz[2], so[2];
-          pn_sub(zc, a - oa, kz, sz);
-          pn_sub(oc, oa, ko, so);
-          p2_put(B1, dz, sz, kz);
-          p2_put(B1, d1, so, ko);
-        } else {  // strings of <= 32 bits
-          const uint32_t za = a - oa;
-          pn_put32(B1, dz, (za >= 32 ? 0u : (uint32_t)zc >> za) & lowmask(kz), kz);
-          pn_put32(B1, d1, (oa >= 32 ? 0u : (uint32_t)oc >> oa) & lowmask(ko), ko);
+        pn_put_cat<EH>(B1, (uint64_t)(uint32_t)(pr + tv.x), zc0, nz0, zc1, nz1);
+        pn_put_cat<EH>(B1, (uint64_t)(uint32_t)(P + R + tv.y), oc0, no0, oc1, no1);
+      } else {
+        // each half: its runs of one node [a, e) with node vv
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t nvh = h ? nv1 : nv0;
+          if (nvh == 0) continue;
+          const uint32_t(&w)[16] = h ? w1 : w0;
+          const uint32_t(&m)[NH] = h ? m1 : m0;
+          const uint64_t zc = h ? zc1 : zc0, oc = h ? oc1 : oc0;
+          const uint32_t ph = (uint32_t)p0 + (h ? (uint32_t)EH : 0u);  // the half's first position
+          const uint32_t Rh = P + R + (h ? no0 : 0u);                  // level-(L-2) ones before it
+          uint32_t vv = pn_sym_c<T, 0>(w) >> 2;
+          uint64_t heads = pn_heads<T, 1, EH>(w, vv) & (nvh >= 64 ? ~0ull : ((1ull << nvh) - 1ull));
+          const uint64_t m64 = (uint64_t)m[0] | (NH == 2 ? ((uint64_t)m[NH - 1] << 32) : 0ull);
+          uint32_t a = 0, oa = 0;  // run start, ones before it in the half
+          for (;;) {
+            const uint32_t e = heads ? (uint32_t)(__ffsll((long long)heads) - 1) : nvh;
+            const uint64_t em = e >= 64 ? ~0ull : ((1ull << e) - 1ull);
+            const uint32_t oe = (uint32_t)__popcll(m64 & em);
+            const uint2 tv = __ldg(&tab[vv]);
+            const uint64_t dz = (uint32_t)(ph + a - Rh - oa + tv.x), d1 = (uint32_t)(Rh + oa + tv.y);
+            const uint32_t kz = (e - a) - (oe - oa), ko = oe - oa;
+            if constexpr (EH == 64) {
+              uint32_t sz[2], so[2];
+              pn_sub(zc, a - oa, kz, sz);
+              pn_sub(oc, oa, ko, so);
+              p2_put(B1, dz, sz, kz);
+              p2_put(B1, d1, so, ko);
+            } else {  // strings of <= 32 bits
+              const uint32_t za = a - oa;
+              pn_put32(B1, dz, (za >= 32 ? 0u : (uint32_t)zc >> za) & lowmask(kz), kz);
+              pn_put32(B1, d1, (oa >= 32 ? 0u : (uint32_t)oc >> oa) & lowmask(ko), ko);
+            }
+            if (e >= nvh) break;
+            a = e;
+            oa = oe;
+            {  // node of symbol e of the half: its bytes in the (swizzled) ring slot
+              const uint32_t off = (uint32_t)(E * lane + (h ? EH : 0) + e) * (uint32_t)sizeof(T);
+              const uint32_t r = off >> 7, c = (off >> 4) & 7u;
+              vv = (uint32_t)*reinterpret_cast<const T*>(buf + r * 128 + ((c ^ (r & 7u)) << 4) + (off & 15u)) >> 2;
+            }
+            heads &= heads - 1;
+          }
         }
-        if (e >= nvalid) break;
-        a = e;
-        oa = oe;
-        {  // node of symbol e: its bytes in the (swizzled) ring slot, still unreleased
-          const uint32_t off = (uint32_t)(E * lane + e) * (uint32_t)sizeof(T), r = off >> 7, c = (off >> 4) & 7u;
-          v = (uint32_t)*reinterpret_cast<const T*>(buf + r * 128 + ((c ^ (r & 7u)) << 4) + (off & 15u)) >> 2;
-        }
-        heads &= heads - 1;
       }
     }
     __syncwarp();  // every lane is done with the slot: refill it

@@ -536,7 +536,8 @@ def test_pairn_node_changes(wt, width):
     for sigma in ({1: (5, 8, 256), 2: (8, 300, 1 << 16), 4: (8, 1 << 12, 1 << 24)}[width]):
         for kind in ("uniform", "sorted", "runs", "constant", "zipf"):
             cases.append((sigma, kind, 3 * t + 77))
-    for n in (rows, rows + 1, 2 * rows - 1, t - 1, t + rows, 5 * t + 64 // width - 1, 5 * t + 64 // width + 1):
+    for n in (rows, rows + 1, 2 * rows - 1, t - 1, t + rows, 2 * t - 1, 2 * t + 1, 3 * t + 128 // width + 3,
+              5 * t + 64 // width - 1, 5 * t + 64 // width + 1):
         cases.append(({1: 256, 2: 1 << 16, 4: 1 << 24}[width], "uniform", n))
         cases.append((8, "sorted", n))
     for i, (sigma, kind, n) in enumerate(cases):
