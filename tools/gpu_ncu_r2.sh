@@ -3,7 +3,7 @@
 # roofline kernel(s), summarised ON THE BOX (tools/ncu_summary.py) into gpurun_out/profiles_out/
 # (the .ncu-rep files of the multi-kernel captures are too large to bring back).
 set -u
-TAG=${TAG:-r02_v3}
+TAG=${TAG:-r02_v5}
 mkdir -p gpurun_out/profiles_out
 cap() {  # cfg kregex skip count keep_rep
   local CFG=$1 K=$2 SKIP=$3 COUNT=$4 KEEP=$5
@@ -18,7 +18,7 @@ cap() {  # cfg kregex skip count keep_rep
   [ "$KEEP" = 1 ] || rm -f gpurun_out/prof_cfg$CFG.ncu-rep
 }
 cap 2 'k_pair2$' 3 1 1
-cap 3 'k_level' 21 7 0
-cap 4 'k_level' 45 15 0
-cap 5 'k_level' 69 23 0
+cap 3 'k_level|k_pairn' 21 7 0
+cap 4 'k_level|k_pairn' 45 15 0
+cap 5 'k_level|k_pairn' 69 23 0
 du -sh gpurun_out

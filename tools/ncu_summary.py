@@ -112,7 +112,7 @@ def main():
         lines.append(f"ncu --set full capture (level pass), cfg{cfg}:")
         for r in fc:
             lines.append("  " + json.dumps(r))
-        lvl = [r for r in fc if "k_level" in r["kernel"] or "k_pair2" in r["kernel"]]
+        lvl = [r for r in fc if "k_level" in r["kernel"] or "k_pair2" in r["kernel"] or "k_pairn" in r["kernel"]]
         if lvl:
             traffic = {}
             for r in lvl:
