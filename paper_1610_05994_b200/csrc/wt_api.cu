@@ -730,7 +730,9 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     // pre_l (scan of agg_l), the node tables of level l (from the level-(l+1)
     // node sizes counted by pass l-1, or from ones0 for l = 0), and zero the
     // node-count buffer pass l fills (and B_{L-1}, OR-ed by the fused pass)
-    wt::ZeroFill z{dry ? nullptr : reinterpret_cast<uint4*>(cnt[l & 1]), matrix ? 1ull : 1ull << l,
+    // (k_pairn counts no leaves: no count buffer to zero before it)
+    wt::ZeroFill z{dry ? nullptr : reinterpret_cast<uint4*>(cnt[l & 1]),
+                   (pair && pairn) ? 0ull : matrix ? 1ull : 1ull << l,
                    pair && !dry ? reinterpret_cast<uint4*>(lastbits) : nullptr, pair ? c.words / 4 : 0};
     if (matrix) {  // the level's one-node table from the scan of its per-tile ones
       wt::OpMatrixTab tb{agg + (uint64_t)l * c.ntiles, tab + l, mzeros + l, n, c.ntiles};
@@ -766,8 +768,8 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       note(K_P2C);
       if (!dry) {
         if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-        const uint64_t nq = 1ull << (L - 1);
-        const uint32_t g = (uint32_t)std::min<uint64_t>((nq + 255) / 256, 8ull * num_sms());
+        const uint64_t nv = 1ull << (L - 2);  // one thread per level-(L-2) node
+        const uint32_t g = (uint32_t)std::min<uint64_t>((nv + 255) / 256, 8ull * num_sms());
         e = launch_pdl(wt::k_leaf_offsets, g, 256u, (size_t)0, stream, (const uint2*)(tab + ((1ull << (L - 2)) - 1)),
                        L, (const uint32_t*)lastbits, (const unsigned long long*)sbl, n, C, (const int32_t*)flag);
         if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_leaf_offsets");

@@ -377,15 +377,8 @@ __device__ __forceinline__ uint64_t rank1(const uint32_t* __restrict__ B,
 // ones before v, ob[v], for the right child; Zn[v-1] + ob[v] for the left);
 // leaf 2q+1's size is the ones of B_{L-1} inside node q (Prop. 1: bit 0).  So
 //   C[2q] = s_q,   C[2q+1] = s_{q+1} - (rank1(s_{q+1}) - rank1(s_q)),   C[2^L] = n.
-// One thread per level-(L-1) node; B_{L-1}'s superblocks must be final.
-__device__ __forceinline__ uint64_t leaf_node_start(const uint2* __restrict__ tab, uint64_t q, uint64_t nq,
-                                                    uint64_t n) {
-  if (q >= nq) return n;
-  const uint64_t v = q >> 1;
-  const uint2 t = tab[v];
-  if (q & 1) return (uint64_t)t.y + t.x;
-  return (v ? (uint64_t)tab[v - 1].y : 0ull) + t.x;
-}
+// B_{L-1}'s superblocks must be final.
+
 // ones of one level in [s0, s1): short ranges (the deep trees' small nodes)
 // by popcounts of their words, long ones as a rank difference
 __device__ __forceinline__ uint64_t ones_between(const uint32_t* __restrict__ B,
@@ -399,17 +392,30 @@ __device__ __forceinline__ uint64_t ones_between(const uint32_t* __restrict__ B,
   for (uint64_t w = w0 + 1; w < w1; ++w) c += (uint32_t)__popc(B[w]);
   return c;
 }
+
+// One thread per level-(L-2) node v: its two children q = 2v, 2v+1 (starts
+// s_{2v} = Zn[v-1] + ob[v], s_{2v+1} = Zn[v] + ob[v], s_{2v+2} = Zn[v] + ob[v+1]),
+// C[4v .. 4v+3] as two 16-byte stores when C is 16-byte aligned.
 __global__ void k_leaf_offsets(const uint2* __restrict__ tab, uint32_t L, const uint32_t* __restrict__ B,
                                const unsigned long long* __restrict__ SB, uint64_t n,
                                unsigned long long* __restrict__ C, const int32_t* __restrict__ flag) {
   pdl_wait();
   if (*flag) return;
-  const uint64_t nq = 1ull << (L - 1);
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t s0 = leaf_node_start(tab, q, nq, n), s1 = leaf_node_start(tab, q + 1, nq, n);
-    C[2 * q] = s0;
-    C[2 * q + 1] = s1 - ones_between(B, SB, s0, s1);
-    if (q + 1 == nq) C[2 * nq] = n;
+  const uint64_t nv = 1ull << (L - 2);
+  const bool al16 = (reinterpret_cast<uintptr_t>(C) & 15u) == 0;
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 t = tab[v];
+    const uint64_t s0 = (v ? (uint64_t)tab[v - 1].y : 0ull) + t.x;
+    const uint64_t s1 = (uint64_t)t.y + t.x;
+    const uint64_t s2 = v + 1 < nv ? (uint64_t)t.y + tab[v + 1].x : n;
+    const uint64_t c1 = s1 - ones_between(B, SB, s0, s1), c3 = s2 - ones_between(B, SB, s1, s2);
+    if (al16) {
+      reinterpret_cast<ulonglong2*>(C)[2 * v] = make_ulonglong2(s0, c1);
+      reinterpret_cast<ulonglong2*>(C)[2 * v + 1] = make_ulonglong2(s1, c3);
+    } else {
+      C[4 * v] = s0, C[4 * v + 1] = c1, C[4 * v + 2] = s1, C[4 * v + 3] = c3;
+    }
+    if (v + 1 == nv) C[4 * nv] = n;
   }
   pdl_trigger();
 }

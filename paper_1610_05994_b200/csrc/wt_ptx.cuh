@@ -97,12 +97,27 @@ __device__ __forceinline__ uint32_t swar_bits(const uint32_t (&xa)[XN], uint32_t
     // (x & msk) * (2^(30-sh) + 2^(15-sh)), then a multiply-high to 2k.
     static_assert(NW <= 16, "u16: at most 16 words per 32-bit mask");
     const uint32_t msk = 0x00010001u << sh;
-    const uint32_t magic = (1u << (30 - sh)) | (1u << (15 - sh));
+    if (NW % 2 == 0 && sh <= 13) {
+      // two words per multiply: t = (x_k & msk) + 4 (x_{k+1} & msk) holds the
+      // 4 symbols' bits at sh, sh+16, sh+2, sh+18; t * (2^(28-sh) + 2^(13-sh))
+      // puts them at 28..31 in symbol order (the other products land at 13, 15
+      // or past bit 31: no carries); a multiply-high moves the nibble to 4k.
+      const uint32_t magic = (1u << (28 - sh)) | (1u << (13 - sh));
 #pragma unroll
-    for (int k = 0; k < NW; ++k) {
-      const uint32_t p = (xw[k] & msk) * magic;
-      const uint32_t v = (k == 15) ? p : __umulhi(p, 1u << (2 + 2 * k));
-      m |= v & (3u << (2 * k));
+      for (int k = 0; k < NW / 2; ++k) {
+        const uint32_t t = (xw[2 * k] & msk) + (xw[2 * k + 1] & msk) * 4u;
+        const uint32_t p = t * magic;
+        const uint32_t v = (k == 7) ? p : __umulhi(p, 1u << (4 + 4 * k));
+        m |= v & (0xfu << (4 * k));
+      }
+    } else {
+      const uint32_t magic = (1u << (30 - sh)) | (1u << (15 - sh));
+#pragma unroll
+      for (int k = 0; k < NW; ++k) {
+        const uint32_t p = (xw[k] & msk) * magic;
+        const uint32_t v = (k == 15) ? p : __umulhi(p, 1u << (2 + 2 * k));
+        m |= v & (3u << (2 * k));
+      }
     }
   } else {
 #pragma unroll
