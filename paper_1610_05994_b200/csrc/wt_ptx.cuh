@@ -85,12 +85,30 @@ __device__ __forceinline__ uint32_t swar_bits(const uint32_t (&xa)[XN], uint32_t
     // a multiply-high moves the nibble to 4k.  2 ALU + 2 FMA-pipe ops per word.
     static_assert(NW <= 8, "u8: at most 8 words per 32-bit mask");
     const uint32_t msk = 0x01010101u << sh;
-    const uint32_t magic = 0x00204081u << (7 - sh);
+    if constexpr (NW % 2 == 0) {
+      // two words per multiply: t holds word k's four bits and word k+1's four
+      // bits 4 apart (at s + 8j and s + 4 + 8j, s = sh for sh <= 3, else sh - 4),
+      // t * (0x00204081 << (3 - s)) puts them at 24..31 in symbol order (the
+      // other products are single bits at distinct positions below 24 or past
+      // bit 31: no carries); a multiply-high moves the byte to 8k.
+      const bool lo = sh <= 3;
+      const uint32_t magic = 0x00204081u << (lo ? 3 - sh : 7 - sh);
 #pragma unroll
-    for (int k = 0; k < NW; ++k) {
-      const uint32_t p = (xw[k] & msk) * magic;
-      const uint32_t v = (k == 7) ? p : __umulhi(p, 1u << (4 + 4 * k));
-      m |= v & (0xfu << (4 * k));
+      for (int k = 0; k < NW / 2; ++k) {
+        const uint32_t a = xw[2 * k] & msk, b = xw[2 * k + 1] & msk;
+        const uint32_t t = lo ? a + b * 16u : (a >> 4) + b;
+        const uint32_t p = t * magic;
+        const uint32_t v = (k == 3) ? p : __umulhi(p, 1u << (8 + 8 * k));
+        m |= v & (0xffu << (8 * k));
+      }
+    } else {
+      const uint32_t magic = 0x00204081u << (7 - sh);
+#pragma unroll
+      for (int k = 0; k < NW; ++k) {
+        const uint32_t p = (xw[k] & msk) * magic;
+        const uint32_t v = (k == 7) ? p : __umulhi(p, 1u << (4 + 4 * k));
+        m |= v & (0xfu << (4 * k));
+      }
     }
   } else if constexpr (sizeof(T) == 2) {
     // bits sh and 16+sh of the word -> bits 30, 31 by one multiply
