@@ -82,6 +82,11 @@ def algorithmic_bytes(kind: str, n: int, w: int, L: int, c_in_final: bool = True
         return 8 * tiles + (tables + zero) // levels
     if kind == "final_scan":  # last-level superblocks from its bitmap (and C from the leaf counts)
         return bitmap + 8 * nsb + ((4 * (1 << L) + 8 * ((1 << L) + 1)) if c_in_final else 0)
+    if kind == "class_count":  # (opt-in triple) read T_{L-3}, per-tile class counts (agg01, agg11)
+        tile = {1: 2048, 2: 1024, 4: 512}[w]
+        return n * w + 8 * ((n + tile - 1) // tile)
+    if kind == "triple":       # (opt-in) read T_{L-3}, three bitmaps, superblocks of level L-3
+        return n * w + 3 * bitmap + 8 * nsb
     if kind == "leaf_offsets":  # C from the level-(L-2) node table and B_{L-1}'s ranks at the node starts
         return 8 * ((1 << L) + 1) + 8 * (1 << max(L - 2, 0))
     return 0

@@ -341,7 +341,10 @@ wt_status wt_rank1(const wt_tree_t* tree, uint64_t n, uint64_t sigma, const uint
  * 11 per-level preparation (the level's tile-prefix scan, its node-table scan
  * and the zeroing of the node counts the pass fills -- and of B_{L-1} before
  * pass 8), 12 final scans (superblocks of level L-1 straight from its bitmap,
- * node_offsets).
+ * and node_offsets from the leaf counts when kind 8 is the general pass),
+ * 17 node_offsets from B_{L-1}'s ranks at the level-(L-1) node starts (after
+ * the no-move fused pair, which counts no leaves: the default for L >= 2),
+ * 18 interior fused pair of levels (opt-in).
  * A segmented build (n > seg_max) lists each segment's launches followed by
  * 16 (its range flag OR-ed into the build's), then 13 the merged node
  * offsets and, per level, 14 the level merge and 15 its superblock scan

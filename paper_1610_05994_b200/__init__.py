@@ -32,7 +32,8 @@ _lib = ctypes.CDLL(LIB_PATH)
 WT_OK, WT_ERR_ARG, WT_ERR_SYMBOL_RANGE, WT_ERR_INDEX, WT_ERR_CUDA, WT_ERR_WORKSPACE = range(6)
 KIND_NAMES = {1: "prologue", 2: "scan", 3: "tables", 4: "level", 5: "last_level", 6: "tile_scan", 7: "memset",
               8: "pair", 9: "sb_scan", 10: "block_pop", 11: "prep", 12: "final_scan", 13: "dd_offsets",
-              14: "dd_merge", 15: "dd_superblocks", 16: "flags", 17: "leaf_offsets", 18: "quad"}
+              14: "dd_merge", 15: "dd_superblocks", 16: "flags", 17: "leaf_offsets", 18: "quad",
+              21: "class_count", 22: "triple"}
 
 
 class WtSizes(ctypes.Structure):

@@ -109,6 +109,7 @@ struct Carve {
   // a5 interior fused groups (k_quad): per-tile class counts (zeroed with the
   // control block), their prefixes, the level-2 node sizes for the first quad
   size_t off_agg01 = 0, off_agg11 = 0, off_hist4 = 0, off_pre01 = 0, off_pre11 = 0;
+  size_t off_tr = 0;  // k_triple: agg01, agg11, pre01, pre11 (ntiles each), cls, tab3 (2^(L-3) each)
   // host-API extras (after total)
   size_t off_seq = 0, off_bits = 0, off_sb = 0, off_c = 0, host_total = 0;
   // segmented build (n > seg_max(): S is cut into k segments, each built with
@@ -250,6 +251,12 @@ Carve carve_direct(uint64_t n, uint64_t sigma, uint32_t width) {
   if (qrows) o += align_up(c.ntiles * sizeof(uint32_t));
   c.off_tab = o;
   o += align_up(c.tab_entries * sizeof(uint2));
+  // k_triple (the fused final three levels): per-tile class counts and their
+  // prefixes, per level-(L-3) node the class sizes and the classes before it
+  if (c.L >= 3) {
+    c.off_tr = o;
+    o += 4 * align_up(c.ntiles * sizeof(uint32_t)) + 2 * align_up((1ull << (c.L - 3)) * sizeof(uint2));
+  }
   c.off_cnt = o;
   o += 2 * align_up(c.cnt_entries * sizeof(uint32_t));
   const size_t seq_bytes = align_up(n * width);
@@ -351,6 +358,31 @@ bool pairn_enabled() {
   const char* v = std::getenv("WT_NO_PAIRN");
   return !(v && *v && *v != '0');
 }
+// The fused final three levels (k_triple, wt_triple.cuh): opt-in, WT_TRIPLE=1
+// (read per call).  Measured on B200 slower than the level pass + k_pairn it
+// replaces.
+bool triple_enabled() {
+  const char* w = std::getenv("WT_TRIPLE");
+  return w && *w && *w != '0';
+}
+template <typename T>
+cudaError_t triple_setup(int* blocks_per_sm) {
+  static int bps[MAX_DEVICES] = {};
+  static cudaError_t err[MAX_DEVICES] = {};
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  if (bps[dev] == 0) {
+    int b = 0;
+    cudaError_t e = cudaFuncSetAttribute(wt::k_triple<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)wt::tr_smem_bytes());
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, wt::k_triple<T>, 32 * wt::PN_WARPS, wt::tr_smem_bytes());
+    err[dev] = e;
+    bps[dev] = b < 1 ? 1 : b;
+  }
+  *blocks_per_sm = bps[dev];
+  return err[dev];
+}
 template <typename T>
 cudaError_t pairn_setup(int* blocks_per_sm) {
   static int bps[MAX_DEVICES] = {};
@@ -435,7 +467,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), uint32_t grid, uint32_t block, si
 enum Kind : uint32_t {
   K_PRO = 1, K_SCAN = 2, K_TABLES = 3, K_LEVEL = 4, K_LAST = 5, K_TSCAN = 6, K_MEMSET = 7, K_PAIR = 8, K_SBSCAN = 9,
   K_PREP = 11, K_FINAL = 12, K_DD_OFFSETS = 13, K_DD_MERGE = 14, K_DD_SB = 15, K_FLAGS = 16, K_P2C = 17,
-  K_QUAD = 18
+  K_QUAD = 18, K_CLS3 = 21, K_TRIPLE = 22
 };
 
 // The launch sequence, shared by wt_build_async and wt_launch_plan.
@@ -577,6 +609,7 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   const bool pair2 = (L == 2 && !matrix && sizeof(T) == 1 && n >= 128 && pair2_enabled());
   // any other tree: the general fused final pair without symbol moves (wt_pairn.cuh)
   const bool pairn = (!pair2 && !matrix && n * sizeof(T) >= 128 && pairn_enabled());
+  const bool triple = (!matrix && L >= 3 && n * sizeof(T) >= 128 && 2 * nquad <= L - 3 && triple_enabled());
   auto level = [&](uint32_t l, int mode) -> wt_status {
     note(mode == 0 ? K_LAST : mode == 2 ? K_PAIR : K_LEVEL);
     if (dry) return WT_OK;
@@ -725,7 +758,8 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
                    c.nsb - 1, "k_scan(quad sb)")) != WT_OK)
       return st;
   }
-  for (uint32_t l = 2 * nquad; l < Lrun; ++l) {
+  const uint32_t lstop = triple ? std::min<uint32_t>(Lrun, L - 3) : Lrun;
+  for (uint32_t l = 2 * nquad; l < lstop; ++l) {
     const bool pair = (l + 2 == L);
     // pre_l (scan of agg_l), the node tables of level l (from the level-(l+1)
     // node sizes counted by pass l-1, or from ones0 for l = 0), and zero the
@@ -749,7 +783,86 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     }
     if ((st = level(l, pair ? 2 : 1)) != WT_OK) return st;
   }
-  if (Lrun == L - 1) {
+  if (triple && Lrun == L - 1) {
+    // the fused final three levels: the level-(L-3) prep (tile prefixes, node
+    // table; zero the class sizes and B_{L-2}), the class counts, their
+    // prefixes and node table (zero B_{L-1}), the pass, the superblocks of
+    // B_{L-2} and B_{L-1}, C
+    const uint32_t l = L - 3;
+    const uint64_t nt = c.ntiles, nv3 = 1ull << l;
+    char* tr = ws + c.off_tr;
+    uint32_t* tagg01 = reinterpret_cast<uint32_t*>(tr);
+    uint32_t* tagg11 = reinterpret_cast<uint32_t*>(tr + align_up(nt * 4));
+    uint32_t* tpre01 = reinterpret_cast<uint32_t*>(tr + 2 * align_up(nt * 4));
+    uint32_t* tpre11 = reinterpret_cast<uint32_t*>(tr + 3 * align_up(nt * 4));
+    uint2* cls = reinterpret_cast<uint2*>(tr + 4 * align_up(nt * 4));
+    uint2* tab3 = reinterpret_cast<uint2*>(tr + 4 * align_up(nt * 4) + align_up(nv3 * sizeof(uint2)));
+    uint32_t* B2 = dry ? nullptr : out->bitmaps + (uint64_t)(L - 2) * c.words;
+    uint32_t* B1 = lastbits;
+    const uint2* tabl = tab + ((1ull << l) - 1);
+    {
+      wt::ZeroFill z{dry ? nullptr : reinterpret_cast<uint4*>(cls), (nv3 * sizeof(uint2) + 15) / 16,
+                     dry ? nullptr : reinterpret_cast<uint4*>(B2), c.words / 4};
+      wt::OpLevelTab tb = (l == 0) ? wt::OpLevelTab{nullptr, tab, n, ones0}
+                                   : wt::OpLevelTab{dry ? nullptr : cnt[(l - 1) & 1], tab + ((1ull << l) - 1), n,
+                                                    nullptr};
+      if ((st = prep(K_PREP, wt::OpTilePrefix{agg + (uint64_t)l * c.ntiles, pre}, c.ntiles, tb, 1ull << l, z,
+                     "k_prep")) != WT_OK)
+        return st;
+    }
+    const T* in = (l == 0) ? seq : buf[(l - 1) & 1];
+    note(K_CLS3);
+    if (!dry) {
+      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((nt + 7) / 8, 8ull * num_sms()));
+      e = launch_pdl(wt::k_cls3<T>, g, 256u, (size_t)0, stream, in, (uint32_t)n, (uint32_t)nt, tagg01, tagg11, cls,
+                     (const int32_t*)flag);
+      if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_cls3");
+      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    }
+    {
+      wt::ZeroFill z{dry ? nullptr : reinterpret_cast<uint4*>(B1), c.words / 4, nullptr, 0};
+      if ((st = prep(K_PREP, wt::OpTilePrefix2{tagg01, tagg11, tpre01, tpre11}, nt, wt::OpNodeCls{cls, tab3}, nv3, z,
+                     "k_prep(classes)")) != WT_OK)
+        return st;
+    }
+    note(K_TRIPLE);
+    if (!dry) {
+      int bps = 1;
+      if ((e = triple_setup<T>(&bps)) != cudaSuccess) return fail_cuda(e, "k_triple setup");
+      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      const uint64_t nwt = (n + wt::TrCfg<T>::WT - 1) / wt::TrCfg<T>::WT;
+      const uint32_t grid = (uint32_t)std::min<uint64_t>((nwt + wt::PN_WARPS - 1) / wt::PN_WARPS,
+                                                         (uint64_t)bps * num_sms());
+      CUtensorMap tmap;
+      if (!rows128_tensor_map(&tmap, in, n * sizeof(T), wt::PN_WT / 128))
+        return fail(WT_ERR_CUDA, "cuTensorMapEncodeTiled");
+      e = launch_pdl(wt::k_triple<T>, grid, (uint32_t)(32 * wt::PN_WARPS), wt::tr_smem_bytes(), stream, in,
+                     (uint32_t)n, (uint32_t)nt, (const uint32_t*)pre, (const uint32_t*)tpre01,
+                     (const uint32_t*)tpre11, tabl, (uint32_t)nv3, (const uint2*)tab3, (const uint2*)cls,
+                     out->bitmaps + (uint64_t)l * c.words,
+                     reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb, (uint32_t)c.nsb,
+                     B2, B1, (const int32_t*)flag, tmap);
+      if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_triple");
+      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    }
+    unsigned long long* const sb2 =
+        dry ? nullptr : reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)(L - 2) * c.nsb;
+    unsigned long long* const sb1 =
+        dry ? nullptr : reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)(L - 1) * c.nsb;
+    if ((st = prep(K_FINAL, wt::OpBitsPop{B2, sb2, c.nsb - 1}, c.nsb - 1, wt::OpBitsPop{B1, sb1, c.nsb - 1},
+                   c.nsb - 1, nozero, "k_prep(final)")) != WT_OK)
+      return st;
+    note(K_P2C);
+    if (!dry) {
+      if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
+      const uint32_t g = (uint32_t)std::min<uint64_t>((nv3 + 255) / 256, 8ull * num_sms());
+      e = launch_pdl(wt::k_leaf3, g, 256u, (size_t)0, stream, tabl, (const uint2*)tab3, (const uint2*)cls, L,
+                     (const uint32_t*)B1, (const unsigned long long*)sb1, n, C, (const int32_t*)flag);
+      if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_leaf3");
+      if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
+    }
+  } else if (Lrun == L - 1) {
     // superblocks of level L-1 from the bitmap the fused pass wrote, and C
     // (exclusive scan of the leaf counts pass L-2 made)
     // superblocks of level L-1: one scan launch that reads B_{L-1} itself

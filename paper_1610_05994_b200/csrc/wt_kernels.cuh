@@ -16,6 +16,7 @@
 #include "wt_prologue.cuh"
 #include "wt_pair2.cuh"
 #include "wt_pairn.cuh"
+#include "wt_triple.cuh"
 #include "wt_quad.cuh"
 
 namespace wt {
@@ -299,6 +300,21 @@ struct OpTilePrefix2 {
   }
 };
 
+// k_triple's node table: per level-(L-3) node the class-01 and class-11
+// symbols before it (exclusive scan of the packed class sizes cls[v] = {01,
+// 11}; each prefix < 2^32, no carry between the halves).
+struct OpNodeCls {
+  const uint2* cls;
+  uint2* tab3;
+  __device__ uint64_t load(uint64_t v) const {
+    const uint2 c = cls[v];
+    return c.x | ((uint64_t)c.y << 32);
+  }
+  __device__ void store(uint64_t v, uint64_t excl, uint64_t) const {
+    tab3[v] = make_uint2((uint32_t)excl, (uint32_t)(excl >> 32));
+  }
+};
+
 // Node tables of level l from the sizes of the level-(l+1) nodes
 // (cnt[u], u < 2^(l+1); counted by pass l-1, or by the prologue for l = 0:
 // cnt1 = ones0, cnt0 = n - ones0).  For level-l node v:
@@ -416,6 +432,31 @@ __global__ void k_leaf_offsets(const uint2* __restrict__ tab, uint32_t L, const 
       C[4 * v] = s0, C[4 * v + 1] = c1, C[4 * v + 2] = s1, C[4 * v + 3] = c3;
     }
     if (v + 1 == nv) C[4 * nv] = n;
+  }
+  pdl_trigger();
+}
+
+// Node offsets C after k_triple (which counts no leaves): per level-(L-3) node
+// v its level-(L-1) nodes q = 4v + c start at N(4v) = s_v, N(4v+1) = s_v +
+// size00, N(4v+2) = s_v + zeros_v, N(4v+3) = N(4v+2) + size10, N(4v+4) = the
+// next node's start; C[2q] = N(q), C[2q+1] = N(q+1) - (ones of B_{L-1} in
+// [N(q), N(q+1))).  B_{L-1}'s superblocks must be final.  One thread per v.
+__global__ void k_leaf3(const uint2* __restrict__ tab, const uint2* __restrict__ tab3, const uint2* __restrict__ cls,
+                        uint32_t L, const uint32_t* __restrict__ B, const unsigned long long* __restrict__ SB,
+                        uint64_t n, unsigned long long* __restrict__ C, const int32_t* __restrict__ flag) {
+  pdl_wait();
+  if (*flag) return;
+  const uint32_t nv = 1u << (L - 3);
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
+    const TrNode d = tr_node(tab, tab3, cls, (uint32_t)v, nv, (uint32_t)n);
+    const uint64_t sv = (uint64_t)d.zb + d.ob, zv = (uint64_t)d.Zn - d.zb, ov = (uint64_t)d.ob1 - d.ob;
+    const uint64_t N[5] = {sv, sv + zv - d.s01, sv + zv, sv + zv + ov - d.s11, sv + zv + ov};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      C[8 * v + 2 * c] = N[c];
+      C[8 * v + 2 * c + 1] = N[c + 1] - ones_between(B, SB, N[c], N[c + 1]);
+    }
+    if (v + 1 == nv) C[8ull * nv] = n;
   }
   pdl_trigger();
 }

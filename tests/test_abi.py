@@ -99,6 +99,19 @@ def test_launch_plan(wt):
     # tile prefixes + zeroing, the quad pass, the superblocks of its level l+1
     # (opt-in, WT_QUAD=1: slower than the level passes on B200)
     assert wt.launch_plan(1 << 20, 256, 1) == ["prologue"] + lv * 6 + pair
+    assert wt.launch_plan(1 << 20, 8, 1) == ["prologue"] + lv + pair
+    # the fused final three levels (opt-in, WT_TRIPLE=1: slower than a level pass
+    # + the pair on B200): the level's prep, the class counts,
+    # their prep, the pass, the superblocks of its two OR-ed levels, C
+    trip = ["prep", "class_count", "prep", "triple", "final_scan", "leaf_offsets"]
+    os.environ["WT_TRIPLE"] = "1"
+    try:
+        assert wt.launch_plan(1 << 20, 256, 1) == ["prologue"] + lv * 5 + trip
+        assert wt.launch_plan(1 << 20, 8, 1) == ["prologue"] + trip
+        assert wt.launch_plan(1 << 20, 1 << 16, 2) == ["prologue"] + lv * 13 + trip
+        assert wt.launch_plan(1 << 20, 4, 1) == ["prologue"] + pair   # (L = 2)
+    finally:
+        del os.environ["WT_TRIPLE"]
     quad = ["prep", "quad", "sb_scan"]
     os.environ["WT_QUAD"] = "1"
     try:
@@ -107,6 +120,10 @@ def test_launch_plan(wt):
         assert wt.launch_plan(1 << 20, 32, 1) == ["prologue"] + quad + lv + pair
         assert wt.launch_plan(1 << 20, 16, 4) == ["prologue"] + quad + pair
         assert wt.launch_plan(1 << 20, 8, 1) == ["prologue"] + lv + pair   # L = 3: no quad
+        os.environ["WT_TRIPLE"] = "1"
+        assert wt.launch_plan(1 << 20, 32, 1) == ["prologue"] + quad + trip   # (T_2 from the quad)
+        assert wt.launch_plan(1 << 20, 16, 4) == ["prologue"] + quad + pair   # (the quad reaches T_2 > T_{L-3})
+        del os.environ["WT_TRIPLE"]
     finally:
         del os.environ["WT_QUAD"]
     # two levels of 1-byte symbols: the specialised pair pass (k_pair2)

@@ -511,6 +511,50 @@ def no_pairn():
     del os.environ["WT_NO_PAIRN"]
 
 
+@pytest.fixture
+def triple_forced():
+    os.environ["WT_TRIPLE"] = "1"
+    yield
+    del os.environ["WT_TRIPLE"]
+
+
+
+
+@pytest.mark.parametrize("width", [1, 2, 4])
+def test_triple(wt, triple_forced, width):
+    # k_triple (the fused final three levels) on every tree with L >= 3 (forced,
+    # whatever the node sizes): lanes inside one node, lanes spanning many nodes
+    # (uniform over a large alphabet, sorted runs), constant and Zipf inputs,
+    # tails around the 128-byte rows, the lane, the 2 KiB level tile and the
+    # 4 KiB warp tile, L = 3 (the pass reads S)
+    dtype = {1: np.uint8, 2: np.uint16, 4: np.uint32}[width]
+    t = TILE[width]
+    cases = []
+    for sigma in {1: (5, 8, 27, 256), 2: (8, 300, 1 << 16), 4: (8, 1 << 12, 1 << 24)}[width]:
+        for kind in ("uniform", "sorted", "runs", "constant", "zipf"):
+            cases.append((sigma, kind, 3 * t + 77))
+    for n in (128 // width, 128 // width + 1, t - 1, t + 5, 2 * t - 1, 2 * t + 1, 3 * t + 128 // width + 3,
+              5 * t + 64 // width - 1, 9 * t):
+        cases.append(({1: 256, 2: 1 << 16, 4: 1 << 24}[width], "uniform", n))
+        cases.append((16, "sorted", n))
+        cases.append((8, "zipf", n))
+    for i, (sigma, kind, n) in enumerate(cases):
+        S = wt_inputs.random_case(1100 + i, n, sigma, kind, dtype=dtype)
+        if n * width >= 128 and sigma > 4:
+            assert "triple" in wt.launch_plan(n, sigma, width)
+        check_case(wt, S, sigma, f"triple w={width} sigma={sigma} {kind} n={n}")
+
+
+def test_triple_random(wt, triple_forced):
+    # forced k_triple over the small random suite's alphabets and shapes
+    for sigma in (5, 8, 16, 27, 230, 256, 1000, 1 << 12, 1 << 16, 70000, 1 << 24):
+        rng = np.random.default_rng(sigma + 5)
+        for k, kind in enumerate(["uniform", "zipf", "runs", "sorted", "reverse", "constant"]):
+            n = int(rng.integers(1, 70000))
+            S = wt_inputs.random_case(300 * sigma + k, n, sigma, kind)
+            check_case(wt, S, sigma, f"triple sigma={sigma} n={n} kind={kind}")
+
+
 @pytest.mark.parametrize("width", [1, 2, 4])
 def test_general_fused_pair(wt, no_pairn, width):
     # WT_NO_PAIRN=1: the final pair through the general k_level<T, 2> (it counts

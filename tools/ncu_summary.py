@@ -20,6 +20,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def kind_of(name: str) -> str:
     if "k_leaf_offsets" in name:
         return "leaf_offsets"
+    if "k_triple" in name:
+        return "triple"
+    if "k_cls3" in name:
+        return "class_count"
     if "k_pair2" in name or "k_pairn" in name:
         return "pair"
     if "k_prep" in name:
