@@ -7,10 +7,16 @@
 //                     ahead by the level passes ("progressive counting").
 //   a2 k_prep         per level: decoupled-look-back scans (this file) of the
 //                     per-tile ones (tile prefixes) and of the node sizes (node
-//                     tables); the final one writes C (line 7, P:541-543,
-//                     exclusive) and the last level's superblocks.
-//   a3/a5 k_level     (wt_level.cuh) the per-level stable segmented bit-partition
-//                     of T_l; the pass of level L-2 is fused with level L-1.
+//                     tables); the final one writes the last level's
+//                     superblocks (and C, line 7, exclusive, after
+//                     the general fused pair).
+//   a3 k_level        (wt_level.cuh) the per-level stable segmented bit-partition
+//                     of T_l, levels 0 .. L-3.
+//   a5 k_pairn        (wt_pairn.cuh) pass L-2 fused with level L-1, no symbol
+//                     moves; k_pair2 (wt_pair2.cuh) for two-level byte trees;
+//                     k_leaf_offsets (this file) then C from B_{L-1}'s ranks.
+//                     Opt-in: k_quad (interior pairs of levels), k_triple (the
+//                     final three levels, wt_triple.cuh).
 #pragma once
 #include "wt_device.cuh"
 #include "wt_prologue.cuh"
