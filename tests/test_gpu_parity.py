@@ -363,6 +363,26 @@ def test_config_parity(wt, cfg):
     device_access_all(tree, S)
 
 
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_config_parity_opt_in_bottom_groups(wt, cfg):
+    # the opt-in fused final three levels (WT_TRIPLE=1) at full size: every
+    # level word for word against the direct build (itself checked against the
+    # oracle above), and C
+    S, sigma = wt_inputs.generate(cfg)
+    d = to_dev(S)
+    ref = wt.build(d, sigma)
+    os.environ["WT_TRIPLE"] = "1"
+    try:
+        assert "triple" in wt.launch_plan(S.size, sigma, S.dtype.itemsize)
+        tr = wt.build(d, sigma)
+    finally:
+        del os.environ["WT_TRIPLE"]
+    torch.cuda.synchronize()
+    assert torch.equal(tr.bitmaps, ref.bitmaps)
+    assert torch.equal(tr.superblocks, ref.superblocks)
+    assert torch.equal(tr.node_offsets, ref.node_offsets)
+
+
 # ------------------------------------------------------------ wavelet matrix (NEXT-4)
 
 
