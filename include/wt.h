@@ -114,12 +114,15 @@ wt_status wt_sizes(uint64_t n, uint64_t sigma, uint32_t width, wt_sizes_t* out);
  * d_seq       n symbols, little-endian, `width` bytes each; 16-byte aligned
  *             (any torch/cudaMalloc allocation is).  Read only.
  * out         device pointers sized per wt_sizes (bitmaps, superblocks,
- *             node_offsets); fully overwritten.
+ *             node_offsets); fully overwritten.  bitmaps 16-byte aligned
+ *             (the pair passes store 16-byte words), superblocks and
+ *             node_offsets 8-byte aligned (any torch/cudaMalloc allocation is).
  * d_workspace >= wt_sizes().workspace_bytes of device memory, 256-byte aligned;
  *             contents on entry are irrelevant.
  * d_status    optional (may be NULL): receives WT_OK or WT_ERR_SYMBOL_RANGE
  *             (int32) when the stream reaches the end of the build.
- * Returns WT_ERR_ARG / WT_ERR_WORKSPACE on bad arguments (nothing enqueued),
+ * Returns WT_ERR_ARG / WT_ERR_WORKSPACE on bad arguments (nothing enqueued;
+ * WT_ERR_ARG also for a misaligned d_seq, d_workspace or output pointer),
  * WT_ERR_CUDA if a launch failed, else WT_OK.
  */
 wt_status wt_build_async(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t width,

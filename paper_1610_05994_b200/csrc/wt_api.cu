@@ -1062,6 +1062,9 @@ wt_status wt_build_async(const void* d_seq, uint64_t n, uint64_t sigma, uint32_t
     return fail(WT_ERR_ARG, "output pointers are NULL");
   if (n > 0 && !d_seq) return fail(WT_ERR_ARG, "d_seq is NULL");
   if (n > 0 && (reinterpret_cast<uintptr_t>(d_seq) & 15)) return fail(WT_ERR_ARG, "d_seq must be 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(out->bitmaps) & 15) || (reinterpret_cast<uintptr_t>(out->superblocks) & 7) ||
+      (reinterpret_cast<uintptr_t>(out->node_offsets) & 7))
+    return fail(WT_ERR_ARG, "bitmaps must be 16-byte aligned, superblocks and node_offsets 8-byte aligned");
   const Carve c = carve(n, sigma, width);
   if (!d_workspace || workspace_bytes < c.total) return fail(WT_ERR_WORKSPACE, "workspace too small");
   if (reinterpret_cast<uintptr_t>(d_workspace) & (ALIGN - 1))

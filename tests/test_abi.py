@@ -78,6 +78,10 @@ def test_build_validates_before_touching_the_device(wt):
     assert lib.wt_build_async(33, 10, 4, 1, ctypes.byref(tree), 256, 1 << 20, None, None) == wt.WT_ERR_ARG
     assert lib.wt_build_async(32, 10, 4, 1, ctypes.byref(tree), 257, 1 << 20, None, None) == wt.WT_ERR_ARG
     assert lib.wt_build_async(32, 10, 4, 3, ctypes.byref(tree), 256, 1 << 20, None, None) == wt.WT_ERR_ARG
+    # misaligned outputs (the pair passes store 16-byte bitmap words)
+    for bad in (wt.WtTree(20, 16, 16), wt.WtTree(16, 20, 16), wt.WtTree(16, 16, 12)):
+        assert lib.wt_build_async(32, 10, 4, 1, ctypes.byref(bad), 256, 1 << 20, None, None) == wt.WT_ERR_ARG
+        assert b"aligned" in lib.wt_last_error()
     assert lib.wt_access(None, 10, 4, None, 1, None, None, None) == wt.WT_ERR_ARG
     # the host-buffer build: NULL status word / host pointers, then the workspace size
     htree = wt.WtTree(16, 16, 16)
