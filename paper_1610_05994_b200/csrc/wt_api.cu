@@ -143,7 +143,7 @@ size_t tree_bytes(uint64_t n, uint32_t L) {
 }
 // superblock scans over nblocks blocks: look-back tiles
 uint64_t sb_scan_tiles(uint64_t nblocks) {
-  return std::max<uint64_t>(1, (nblocks + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+  return std::max<uint64_t>(1, (nblocks + wt::SCAN_TILE_MIN - 1) / wt::SCAN_TILE_MIN);
 }
 
 Carve carve_direct(uint64_t n, uint64_t sigma, uint32_t width);
@@ -212,11 +212,11 @@ Carve carve_direct(uint64_t n, uint64_t sigma, uint32_t width) {
   c.nsb = (n + 511) / 512 + 1;
   c.c_len = (1ull << c.L) + 1;
   c.ntiles = (n + level_tile(width) - 1) / level_tile(width);
-  const uint64_t scan_tiles = ((1ull << c.L) + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
+  const uint64_t scan_tiles = ((1ull << c.L) + wt::SCAN_TILE_MIN - 1) / wt::SCAN_TILE_MIN;
   c.tab_entries = c.L >= 2 ? (1ull << (c.L - 1)) - 1 : 0;
   c.cnt_entries = c.L >= 2 ? (1ull << c.L) : 0;
-  const uint64_t pre_tiles = (c.ntiles + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
-  const uint64_t sb_tiles = (c.nsb + wt::SCAN_TILE - 1) / wt::SCAN_TILE;  // last level's superblock scan
+  const uint64_t pre_tiles = (c.ntiles + wt::SCAN_TILE_MIN - 1) / wt::SCAN_TILE_MIN;
+  const uint64_t sb_tiles = (c.nsb + wt::SCAN_TILE_MIN - 1) / wt::SCAN_TILE_MIN;  // last level's superblock scan
   c.status_entries = std::max<uint64_t>(1, std::max(std::max(pre_tiles, scan_tiles), sb_tiles));
   size_t o = 0;
   c.off_flag = o;
@@ -532,7 +532,8 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   auto scan = [&](auto op, uint64_t cnt_, const char* what) -> wt_status {
     if (!dry) {
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      const uint32_t g = (uint32_t)((cnt_ + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+      constexpr uint64_t ST = wt::scan_tile_of<decltype(op)>();
+      const uint32_t g = (uint32_t)((cnt_ + ST - 1) / ST);
       wt::k_scan<decltype(op)><<<g, wt::SCAN_THREADS, 0, stream>>>(op, cnt_, status, counters + counter, epoch, flag);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, what);
       if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
@@ -564,7 +565,8 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     note(kind);
     if (!dry) {
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      const uint64_t ga = (na + wt::SCAN_TILE - 1) / wt::SCAN_TILE, gb = (nb + wt::SCAN_TILE - 1) / wt::SCAN_TILE;
+      constexpr uint64_t STA = wt::scan_tile_of<decltype(opA)>(), STB = wt::scan_tile_of<decltype(opB)>();
+      const uint64_t ga = (na + STA - 1) / STA, gb = (nb + STB - 1) / STB;
       const uint64_t zu = z.n0 + z.n1;
       const uint64_t gz = zu ? std::min<uint64_t>((zu + 4 * wt::SCAN_THREADS - 1) / (4 * wt::SCAN_THREADS),
                                                   4ull * num_sms())
@@ -931,7 +933,8 @@ cudaError_t launch_superblocks(const uint32_t* bits, uint64_t nblocks, uint64_t 
     wt::k_set_u64<<<1, 32, 0, s>>>(sb, base);
     return cudaGetLastError();
   }
-  const uint32_t tiles = (uint32_t)((nblocks + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+  constexpr uint64_t ST = wt::scan_tile_of<wt::OpBitsPop>();
+  const uint32_t tiles = (uint32_t)((nblocks + ST - 1) / ST);
   wt::k_scan<wt::OpBitsPop><<<tiles, wt::SCAN_THREADS, 0, s>>>(wt::OpBitsPop{bits, sb, nblocks, base}, nblocks, lb,
                                                                counter, epoch, noflag);
   return cudaGetLastError();
@@ -1265,7 +1268,8 @@ struct RemapCarve {
 RemapCarve remap_carve(uint64_t sigma) {
   RemapCarve r;
   r.words = (sigma + 31) / 32;
-  r.tiles = std::max<uint64_t>(1, (r.words + wt::SCAN_TILE - 1) / wt::SCAN_TILE);
+  constexpr uint64_t ST = wt::scan_tile_of<wt::OpPopPrefix>();
+  r.tiles = std::max<uint64_t>(1, (r.words + ST - 1) / ST);
   size_t o = 0;
   r.off_flag = o;
   o += ALIGN;

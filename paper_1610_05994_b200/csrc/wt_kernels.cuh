@@ -30,11 +30,16 @@ namespace wt {
 // ================================================================ a2 scans
 
 constexpr int SCAN_THREADS = 512;
-#ifndef WT_SCAN_ITEMS
-#define WT_SCAN_ITEMS 8
+// values per thread of a scan tile: 8 for the scans that read a bitmap's
+// 512-bit blocks themselves (their loads want bytes in flight), 4 for the
+// scans of per-tile / per-node values (latency-bound: more, smaller CTAs
+// start their look-back sooner; cfg5 build 11.95 -> 11.77 ms)
+constexpr int SCAN_ITEMS_BITS = 8;
+#ifndef WT_SCAN_ITEMS_V
+#define WT_SCAN_ITEMS_V 4
 #endif
-constexpr int SCAN_ITEMS = WT_SCAN_ITEMS;  // values per thread of a scan tile (experiment builds override)
-constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+constexpr int SCAN_ITEMS_VALS = WT_SCAN_ITEMS_V;
+constexpr int SCAN_TILE_MIN = SCAN_THREADS * (SCAN_ITEMS_VALS < SCAN_ITEMS_BITS ? SCAN_ITEMS_VALS : SCAN_ITEMS_BITS);
 
 // Scan ops whose values are the popcounts of consecutive 512-bit blocks of a
 // bitmap (`bits`): scan_tile loads the tile's blocks itself, coalesced.
@@ -47,8 +52,15 @@ struct ScanOfBits {
 // Op supplies load(i) and store(i, exclusive, value).  One CTA scans one tile
 // of SCAN_TILE values; tile ids come from an atomic ticket (forward progress).
 template <class Op>
+constexpr int scan_items_of() { return ScanOfBits<Op>::value ? SCAN_ITEMS_BITS : SCAN_ITEMS_VALS; }
+template <class Op>
+constexpr uint64_t scan_tile_of() { return (uint64_t)SCAN_THREADS * scan_items_of<Op>(); }
+
+template <class Op>
 __device__ __forceinline__ void scan_tile(const Op& op, uint64_t count, const LookbackState& status,
                                           uint32_t* tile_counter, uint32_t epoch) {
+  constexpr int SCAN_ITEMS = scan_items_of<Op>();
+  constexpr uint64_t SCAN_TILE = scan_tile_of<Op>();
   __shared__ uint64_t s_warp[SCAN_THREADS / 32];
   __shared__ uint64_t s_P;
   __shared__ uint32_t s_tile;
@@ -150,7 +162,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_prep(OpA a, uint64_t na, Lookb
                                                        ZeroFill z, const int32_t* __restrict__ flag) {
   pdl_wait();
   if (*flag) return;
-  const uint32_t ga = (uint32_t)((na + SCAN_TILE - 1) / SCAN_TILE), gb = (uint32_t)((nb + SCAN_TILE - 1) / SCAN_TILE);
+  const uint32_t ga = (uint32_t)((na + scan_tile_of<OpA>() - 1) / scan_tile_of<OpA>()),
+                 gb = (uint32_t)((nb + scan_tile_of<OpB>() - 1) / scan_tile_of<OpB>());
   if (blockIdx.x < ga) {
     scan_tile(a, na, sta, ca, ea);
   } else if (blockIdx.x < ga + gb) {
