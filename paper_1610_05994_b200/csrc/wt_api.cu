@@ -610,7 +610,7 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
   // two levels of 1-byte symbols: the specialised pass (wt_pair2.cuh) replaces the fused pair
   const bool pair2 = (L == 2 && !matrix && sizeof(T) == 1 && n >= 128 && pair2_enabled());
   // any other tree: the general fused final pair without symbol moves (wt_pairn.cuh)
-  const bool pairn = (!pair2 && !matrix && n * sizeof(T) >= 128 && pairn_enabled());
+  const bool pairn = (!pair2 && n * sizeof(T) >= 128 && pairn_enabled());
   const bool triple = (!matrix && L >= 3 && n * sizeof(T) >= 128 && 2 * nquad <= L - 3 && triple_enabled());
   auto level = [&](uint32_t l, int mode) -> wt_status {
     note(mode == 0 ? K_LAST : mode == 2 ? K_PAIR : K_LEVEL);
@@ -645,10 +645,12 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       if (!rows128_tensor_map(&tmap, in, n * sizeof(T), wt::PN_WT / 128))
         return fail(WT_ERR_CUDA, "cuTensorMapEncodeTiled");
       e = launch_pdl(wt::k_pairn<T>, grid, (uint32_t)(32 * wt::PN_WARPS), wt::pn_smem_bytes(), stream, in,
-                     (uint32_t)n, (uint32_t)c.ntiles, (const uint32_t*)pre, (const uint2*)(tab + ((1ull << l) - 1)),
-                     out->bitmaps + (uint64_t)l * c.words, (uint32_t)c.words,
+                     (uint32_t)n, (uint32_t)c.ntiles, (const uint32_t*)pre,
+                     (const uint2*)(matrix ? tab + l : tab + ((1ull << l) - 1)), out->bitmaps + (uint64_t)l * c.words,
+                     (uint32_t)c.words,
                      reinterpret_cast<unsigned long long*>(out->superblocks) + (uint64_t)l * c.nsb, (uint32_t)c.nsb,
-                     out->bitmaps + (uint64_t)(L - 1) * c.words, (const int32_t*)flag, tmap);
+                     out->bitmaps + (uint64_t)(L - 1) * c.words, matrix ? 0u : 0xffffffffu, (const int32_t*)flag,
+                     tmap);
       if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_pairn");
       if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
       return WT_OK;

@@ -199,8 +199,10 @@ template <typename T>
 __global__ void __launch_bounds__(32 * PN_WARPS, 6)
     k_pairn(const T* __restrict__ in, uint32_t n, uint32_t ntiles, const uint32_t* __restrict__ pre,
             const uint2* __restrict__ tab, uint32_t* __restrict__ bits, uint32_t words,
-            unsigned long long* __restrict__ sb, uint32_t nsb, uint32_t* __restrict__ B1,
+            unsigned long long* __restrict__ sb, uint32_t nsb, uint32_t* __restrict__ B1, uint32_t vmask,
             const int32_t* __restrict__ flag, const __grid_constant__ CUtensorMap tmap) {
+  // vmask: all ones for the tree (node v = s >> 2); 0 for the wavelet matrix,
+  // whose levels are one global node each (tab[0] = {0, Z_{L-2}})
   using C = PnCfg<T>;
   constexpr int E = C::E, EH = C::EH, WT = C::WT, NH = C::NH;
   extern __shared__ unsigned char pn_raw[];
@@ -278,9 +280,10 @@ __global__ void __launch_bounds__(32 * PN_WARPS, 6)
     if ((p0 & 511u) == 0 && p0 < n) sb[p0 / 512] = P + R;
     if (tile + 1 == nwt && lane == 31) sb[nsb - 1] = P0 + inc;
     if (nvalid) {
-      const uint32_t v = pn_sym_c<T, 0>(w0) >> 2;
+      const uint32_t v = (pn_sym_c<T, 0>(w0) >> 2) & vmask;
       const uint32_t vlast =
-          (nv1 == (uint32_t)EH ? pn_sym_c<T, EH - 1>(w1) : nv1 ? pn_sym<T>(w1, nv1 - 1) : pn_sym<T>(w0, nv0 - 1)) >> 2;
+          ((nv1 == (uint32_t)EH ? pn_sym_c<T, EH - 1>(w1) : nv1 ? pn_sym<T>(w1, nv1 - 1) : pn_sym<T>(w0, nv0 - 1)) >> 2) &
+          vmask;
       const uint32_t pr = (uint32_t)p0 - P - R;  // zeros before the lane (mod 2^32: positions < n < 2^32)
       if (v == vlast) {  // the lane inside one node: both strings whole
         const uint2 tv = __ldg(&tab[v]);
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(32 * PN_WARPS, 6)
           const uint64_t zc = h ? zc1 : zc0, oc = h ? oc1 : oc0;
           const uint32_t ph = (uint32_t)p0 + (h ? (uint32_t)EH : 0u);  // the half's first position
           const uint32_t Rh = P + R + (h ? no0 : 0u);                  // level-(L-2) ones before it
-          uint32_t vv = pn_sym_c<T, 0>(w) >> 2;
+          uint32_t vv = (pn_sym_c<T, 0>(w) >> 2) & vmask;
           uint64_t heads = pn_heads<T, 1, EH>(w, vv) & (nvh >= 64 ? ~0ull : ((1ull << nvh) - 1ull));
           const uint64_t m64 = (uint64_t)m[0] | (NH == 2 ? ((uint64_t)m[NH - 1] << 32) : 0ull);
           uint32_t a = 0, oa = 0;  // run start, ones before it in the half
@@ -325,7 +328,8 @@ __global__ void __launch_bounds__(32 * PN_WARPS, 6)
             {  // node of symbol e of the half: its bytes in the (swizzled) ring slot
               const uint32_t off = (uint32_t)(E * lane + (h ? EH : 0) + e) * (uint32_t)sizeof(T);
               const uint32_t r = off >> 7, c = (off >> 4) & 7u;
-              vv = (uint32_t)*reinterpret_cast<const T*>(buf + r * 128 + ((c ^ (r & 7u)) << 4) + (off & 15u)) >> 2;
+              vv = ((uint32_t)*reinterpret_cast<const T*>(buf + r * 128 + ((c ^ (r & 7u)) << 4) + (off & 15u)) >> 2) &
+                   vmask;
             }
             heads &= heads - 1;
           }
