@@ -386,6 +386,24 @@ def test_config_parity_opt_in_bottom_groups(wt, cfg):
 # ------------------------------------------------------------ wavelet matrix (NEXT-4)
 
 
+@pytest.mark.parametrize("width", [1, 2, 4])
+def test_matrix_general_pair(wt, width):
+    # WT_NO_PAIRN=1: the matrix's final pair through k_level<T, 2> (LV_MATRIX)
+    sigma = {1: 256, 2: 1 << 16, 4: 1 << 20}[width]
+    dtype = {1: np.uint8, 2: np.uint16, 4: np.uint32}[width]
+    os.environ["WT_NO_PAIRN"] = "1"
+    try:
+        for k, (kind, s) in enumerate([("uniform", sigma), ("zipf", sigma), ("runs", 4)]):
+            S = wt_inputs.random_case(1300 + k, 50_000 + 11 * k, s, kind, dtype=dtype)
+            mx = wt.build_matrix(to_dev(S), s)
+            om = oracle.build_matrix(S, s)
+            assert np.array_equal(mx.bitmaps.cpu().numpy().view(np.uint32), om.bitmaps), kind
+            assert np.array_equal(mx.superblocks.cpu().numpy().view(np.uint64), om.superblocks), kind
+            assert np.array_equal(mx.zeros.cpu().numpy().view(np.uint64), om.zeros), kind
+    finally:
+        del os.environ["WT_NO_PAIRN"]
+
+
 def test_degenerate_host_and_matrix_builds(wt):
     # n = 0 through the asynchronous host path; sigma = 1 (no levels) for the matrix
     # and the select index
