@@ -13,17 +13,20 @@
 // bit-0 string to another, both contiguous.
 //
 // This is k_pair2's execution (wt_pair2.cuh) made general: per warp a ring of
-// 2 KiB TMA tensor copies of T_{L-2} (rows of 128 bytes, 128-byte swizzle; the
-// level pass's tile, so its tile prefixes pre[t] apply), each lane 64 bytes =
-// E symbols, compacted 4 at a time by the 256-entry table (bit 0 / bit 1 of
-// 4 symbols -> their level-(L-2) bits, the zeros' and ones' bit-0 strings and
-// the strings' position multipliers).  Node changes inside a lane's symbols
-// split its two strings into per-node substrings (the strings are in position
-// order, so node g's part is the bits between the zeros / ones before g's
-// first symbol and after its last).  Every substring is stored with its
-// interior words plain and its first / last word OR-ed into the zero-filled
-// B_{L-1} (the paper's atomic boundary words).  No leaves are
-// counted: C comes from B_{L-1}'s superblocks afterwards (k_leaf_offsets).
+// two 4 KiB TMA tensor copies of T_{L-2} (rows of 128 bytes, 128-byte swizzle;
+// two of the level pass's tiles, so its tile prefixes pre[t] apply, one per
+// half warp); lane l owns row l (E symbols), compacted as two 64-byte halves,
+// 4 symbols at a time, by the 256-entry table (bit 0 / bit 1 of 4 symbols ->
+// their level-(L-2) bits, the zeros' and ones' bit-0 strings and the strings'
+// position multipliers).  A lane inside one node stores its two strings whole;
+// node changes inside a lane split each half's strings into per-node
+// substrings (the strings are in position order, so node g's part is the bits
+// between the zeros / ones before g's first symbol and after its last).  Every
+// string is stored with its interior words plain and its first / last word
+// OR-ed into the zero-filled B_{L-1} (the paper's atomic boundary words,
+// P:814-821).  No leaves are counted: C comes from B_{L-1}'s superblocks
+// afterwards (k_leaf_offsets).  The wavelet matrix (one global node per level)
+// runs the same kernel with the node index masked to 0.
 #pragma once
 #include <cuda.h>
 
