@@ -37,8 +37,9 @@ constexpr int P2_MINB = 32;    // warps (CTAs) per SM the register budget is siz
 // 256-entry table, index = the (bit 0, bit 1) pairs of 4 symbols (bit 2j =
 // bit 0 of symbol j, bit 2j+1 = its bit 1):
 //   .x = [3:0] bit 0 of the symbols with bit 1 = 0, in order (the zeros' string)
-//        [11:8] bit 0 of the symbols with bit 1 = 1 (the ones' string)
 //        [19:16] bit 1 of the four symbols (their level-0 bits)
+//        [31:28] bit 0 of the symbols with bit 1 = 1 (the ones' string: one
+//        shift extracts it)
 //   .y = [7:0] 2^(their zeros), [15:8] 2^(their ones): the strings' position multipliers
 __device__ __forceinline__ uint2 p2_lut_entry(uint32_t idx) {
   uint32_t zb = 0, nz = 0, ob = 0, no = 0, m1 = 0;
@@ -48,7 +49,7 @@ __device__ __forceinline__ uint2 p2_lut_entry(uint32_t idx) {
     if (b1) ob |= b0 << no++;
     else zb |= b0 << nz++;
   }
-  return make_uint2(zb | (ob << 8) | (m1 << 16), (1u << nz) | ((1u << no) << 8));
+  return make_uint2(zb | (m1 << 16) | (ob << 28), (1u << nz) | ((1u << no) << 8));
 }
 
 // 32 consecutive symbols (8 words), the first `valid` real: level-0 word m,
@@ -65,7 +66,7 @@ __device__ __forceinline__ void p2_quarter(const uint32_t* w, uint32_t valid, co
       const uint2 e = lut[(w[wi] * 0x01041040u) >> 24];
       m |= ((e.x >> 16) & 15u) << (4 * wi);
       Z += (e.x & 15u) * pz;
-      O += ((e.x >> 8) & 15u) * po;
+      O += (e.x >> 28) * po;
       pz *= e.y & 0xffu;
       po *= e.y >> 8;
     }

@@ -147,7 +147,7 @@ __device__ __forceinline__ void pn_half(const uint32_t (&w)[16], uint32_t nv, co
         const uint2 e = lut[pn_index<T>(w, h * GH + g)];
         mm |= ((e.x >> 16) & 15u) << (4 * g);
         Zs += (e.x & 15u) * pz;
-        Os += ((e.x >> 8) & 15u) * po;
+        Os += (e.x >> 28) * po;
         pz *= e.y & 0xffu;
         po *= e.y >> 8;
       }

@@ -91,8 +91,8 @@ __device__ __forceinline__ void tr_stage1(const uint32_t (&w)[16], int g0, uint3
       m |= ((a.x >> 16) & 15u) << (4 * g);
       Z1 += (a.x & 15u) * pz;
       Z0 += (b.x & 15u) * pz;
-      O1 += ((a.x >> 8) & 15u) * po;
-      O0 += ((b.x >> 8) & 15u) * po;
+      O1 += (a.x >> 28) * po;
+      O0 += (b.x >> 28) * po;
       pz *= a.y & 0xffu;
       po *= a.y >> 8;
     }
@@ -129,7 +129,7 @@ __device__ __forceinline__ void tr_stage2(uint32_t H, uint32_t Lo, uint32_t n, c
     if (4 * k >= (int)n) break;
     const uint2 e = lutc[(((H >> (4 * k)) & 15u) << 4) | ((Lo >> (4 * k)) & 15u)];
     c0 += (e.x & 15u) * p0;
-    c1 += ((e.x >> 8) & 15u) * p1;
+    c1 += (e.x >> 28) * p1;
     p0 *= e.y & 0xffu;
     p1 *= e.y >> 8;
   }
