@@ -105,12 +105,13 @@ wt_status wt_sizes(uint64_t n, uint64_t sigma, uint32_t width, wt_sizes_t* out);
 /*
  * wt_build_async: enqueue the whole construction on `stream`:
  *   a1 one pass over S (symbol-range check, level-0 tile ones), a3 one
- *   stable bit-partition pass per level l < L-1 (bitmap words, superblocks,
+ *   stable bit-partition pass per level l < L-2 (bitmap words, superblocks,
  *   T_{l+1}, and -- progressive counting -- the sizes of the level-(l+2)
  *   nodes), each preceded by a2 scans building that level's node tables;
- *   the last scatter pass counts the leaves, whose exclusive scan is
- *   node_offsets; a4 the last level (bitmap + superblocks).  No host
- *   synchronisation; CUDA-graph capturable.
+ *   a5 the pass of level L-2 fused with level L-1 (both bitmaps from T_{L-2}
+ *   with no symbol moved), then the last level's superblocks and
+ *   node_offsets from its ranks at the node starts; a4 the single level when
+ *   L = 1.  No host synchronisation; CUDA-graph capturable.
  * d_seq       n symbols, little-endian, `width` bytes each; 16-byte aligned
  *             (any torch/cudaMalloc allocation is).  Read only.
  * out         device pointers sized per wt_sizes (bitmaps, superblocks,
