@@ -133,7 +133,13 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
   const uint32_t nsh = (shf & LV_MATRIX) ? 31u : sh + 1;  // node id = symbol >> nsh
   const uint32_t i0 = lane * E;  // first tile position of this lane (phase A)
 
+#ifdef WT_LV_CHUNK
+  // contiguous chunks of tiles per warp
+  const uint32_t chunk = (ntiles + gridDim.x - 1) / gridDim.x;
+  auto tile_of = [&](uint32_t it) -> uint32_t { return it < chunk ? blockIdx.x * chunk + it : 0xffffffffu; };
+#else
   auto tile_of = [&](uint32_t it) -> uint32_t { return blockIdx.x + it * gridDim.x; };
+#endif
   auto issue = [&](uint32_t it) {  // lane 0: bulk-copy the warp's it-th tile into buf[it % NB]
     const uint32_t t = tile_of(it);
     if (t >= ntiles) return;
