@@ -14,7 +14,7 @@
 // run independently (no block barriers to wait on, only __syncwarp).  A warp
 // tile is 2 KiB of symbols (2048 / 1024 / 512 for 1 / 2 / 4-byte symbols, a
 // multiple of 512 positions: every bitmap word and superblock belongs to one
-// tile); tiles go round-robin over the warps.  Per warp a ring of 4 buffers:
+// tile); every warp takes a contiguous chunk of tiles.  Per warp a ring of 4 buffers:
 // tile `it` is TMA-bulk-loaded (cp.async.bulk + mbarrier) into buf[it % 4]
 // and its partitioned output is staged in buf[(it-1) % 4], the previous
 // tile's input buffer.
@@ -133,8 +133,11 @@ __global__ void __launch_bounds__(32, LvTile<T>::MINB)
   const uint32_t nsh = (shf & LV_MATRIX) ? 31u : sh + 1;  // node id = symbol >> nsh
   const uint32_t i0 = lane * E;  // first tile position of this lane (phase A)
 
-#ifdef WT_LV_CHUNK
-  // contiguous chunks of tiles per warp
+#ifndef WT_LV_ROUND_ROBIN
+  // every warp takes a contiguous chunk of tiles: its tiles mostly stay in one
+  // node, so the progressive counts (cc_flush) leave rarely and warps do not
+  // meet on the same counters (round-robin tiles put all warps in the same one
+  // or two nodes at once: cfg5 levels 7-9 0.51 / 0.49 / 0.45 -> 0.41 ms)
   const uint32_t chunk = (ntiles + gridDim.x - 1) / gridDim.x;
   auto tile_of = [&](uint32_t it) -> uint32_t { return it < chunk ? blockIdx.x * chunk + it : 0xffffffffu; };
 #else
