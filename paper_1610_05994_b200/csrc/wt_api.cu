@@ -534,7 +534,7 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
       constexpr uint64_t ST = wt::scan_tile_of<decltype(op)>();
       const uint32_t g = (uint32_t)((cnt_ + ST - 1) / ST);
-      wt::k_scan<decltype(op)><<<g, wt::SCAN_THREADS, 0, stream>>>(op, cnt_, status, counters + counter, epoch, flag);
+      wt::k_scan<decltype(op)><<<g, wt::scan_threads_of<decltype(op)>(), 0, stream>>>(op, cnt_, status, counters + counter, epoch, flag);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, what);
       if ((e = lk.post()) != cudaSuccess) return fail_cuda(e, "profile event record");
     }
@@ -565,13 +565,14 @@ wt_status enqueue(const T* seq, uint64_t n, uint64_t sigma, const wt_tree_t* out
     note(kind);
     if (!dry) {
       if ((e = lk.pre()) != cudaSuccess) return fail_cuda(e, "profile event record");
-      constexpr uint64_t STA = wt::scan_tile_of<decltype(opA)>(), STB = wt::scan_tile_of<decltype(opB)>();
+      constexpr int NT = wt::scan_threads_of<decltype(opA)>();  // (k_prep: CTAs of the first scan's size)
+      constexpr uint64_t STA = wt::scan_tile_of<decltype(opA), NT>(), STB = wt::scan_tile_of<decltype(opB), NT>();
       const uint64_t ga = (na + STA - 1) / STA, gb = (nb + STB - 1) / STB;
       const uint64_t zu = z.n0 + z.n1;
-      const uint64_t gz = zu ? std::min<uint64_t>((zu + 4 * wt::SCAN_THREADS - 1) / (4 * wt::SCAN_THREADS),
+      const uint64_t gz = zu ? std::min<uint64_t>((zu + 4 * NT - 1) / (4 * NT),
                                                   4ull * num_sms())
                              : (ga + gb ? 0 : 1);
-      e = launch_pdl(wt::k_prep<decltype(opA), decltype(opB)>, (uint32_t)(ga + gb + gz), wt::SCAN_THREADS, 0, stream,
+      e = launch_pdl(wt::k_prep<decltype(opA), decltype(opB)>, (uint32_t)(ga + gb + gz), (uint32_t)NT, 0, stream,
                      opA, na, status, counters + counter, epoch, opB, nb, status2, counters + counter + 1, epoch + 1, z,
                      (const int32_t*)flag);
       if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, what);
@@ -937,7 +938,7 @@ cudaError_t launch_superblocks(const uint32_t* bits, uint64_t nblocks, uint64_t 
   }
   constexpr uint64_t ST = wt::scan_tile_of<wt::OpBitsPop>();
   const uint32_t tiles = (uint32_t)((nblocks + ST - 1) / ST);
-  wt::k_scan<wt::OpBitsPop><<<tiles, wt::SCAN_THREADS, 0, s>>>(wt::OpBitsPop{bits, sb, nblocks, base}, nblocks, lb,
+  wt::k_scan<wt::OpBitsPop><<<tiles, wt::scan_threads_of<wt::OpBitsPop>(), 0, s>>>(wt::OpBitsPop{bits, sb, nblocks, base}, nblocks, lb,
                                                                counter, epoch, noflag);
   return cudaGetLastError();
 }
@@ -1325,7 +1326,7 @@ wt_status wt_remap_alphabet(const void* d_seq, uint64_t n, uint64_t sigma, uint3
   if (e != cudaSuccess) return fail_cuda(e, "k_remap_mark");
   const wt::LookbackState lb{reinterpret_cast<uint32_t*>(ws + r.off_status), reinterpret_cast<uint64_t*>(ws + r.off_value),
                              r.tiles};
-  wt::k_scan<wt::OpPopPrefix><<<(uint32_t)r.tiles, wt::SCAN_THREADS, 0, s>>>(
+  wt::k_scan<wt::OpPopPrefix><<<(uint32_t)r.tiles, wt::scan_threads_of<wt::OpPopPrefix>(), 0, s>>>(
       wt::OpPopPrefix{present, rank, r.words, total}, r.words, lb, reinterpret_cast<uint32_t*>(ws + r.off_counter), 1u,
       flag);
   if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "k_scan(remap)");

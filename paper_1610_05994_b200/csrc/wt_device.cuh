@@ -95,6 +95,61 @@ __device__ __forceinline__ uint64_t lookback(LookbackState lb, uint64_t tile, ui
   return exclusive;
 }
 
+// The same look-back by a whole CTA (blockDim.x = NT threads, all of them call
+// it): thread j looks at tile (tile - 1 - j), so one round trip covers NT
+// predecessors instead of 32 -- when the scan's CTAs start together (a grid of
+// one wave: the per-level preps) every aggregate is published at about the same
+// time and a 32-tile window walks tile / 32 dependent round trips back to the
+// first inclusive prefix.  `aggregate` is the tile's total (thread 0's copy is
+// used); s_sum / s_has: NT / 32 shared entries each.  Returns the exclusive
+// prefix to every thread; contains block barriers.
+template <int NT>
+__device__ __forceinline__ uint64_t block_lookback(LookbackState lb, uint64_t tile, uint64_t aggregate, uint32_t epoch,
+                                                   uint64_t* s_sum, uint32_t* s_has) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) lb_publish(lb, tile, tile ? ST_AGG : ST_PREFIX, epoch, aggregate);
+  uint64_t exclusive = 0;
+  int64_t base = (int64_t)tile - 1;
+  while (true) {  // (block-uniform trip count)
+    const int64_t idx = base - (int64_t)threadIdx.x;
+    uint32_t flag = ST_PREFIX;  // (before tile 0: an empty inclusive prefix)
+    uint64_t val = 0;
+    if (idx >= 0) {
+      while (true) {
+        const uint32_t w = ld_acquire_u32(&lb.status[idx]);
+        flag = ((w & 0xffu) == (epoch & 0xffu)) ? (w >> 30) : ST_INVALID;
+        if (flag != ST_INVALID) break;
+        __nanosleep(20);
+      }
+      val = ld_relaxed_u64(&lb.value[(flag == ST_PREFIX ? lb.tiles : 0) + idx]);
+    }
+    const uint32_t pm = __ballot_sync(FULL, flag == ST_PREFIX);
+    const uint32_t stop = pm ? (uint32_t)(__ffs(pm) - 1) : 31u;
+    uint64_t c = (lane <= stop) ? val : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if (lane == 0) {
+      s_sum[warp] = c;
+      s_has[warp] = pm ? 1u : 0u;
+    }
+    __syncthreads();
+    bool found = false;
+#pragma unroll 1
+    for (int w = 0; w < NT / 32; ++w) {
+      exclusive += s_sum[w];
+      if (s_has[w]) {
+        found = true;
+        break;
+      }
+    }
+    if (found) break;
+    base -= NT;
+    __syncthreads();  // (s_sum / s_has are rewritten)
+  }
+  if (threadIdx.x == 0 && tile) lb_publish(lb, tile, ST_PREFIX, epoch, exclusive + aggregate);
+  return exclusive;
+}
+
 // ------------------------------------------------------------- warp scans
 __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t x) {
   const uint32_t lane = threadIdx.x & 31;

@@ -29,17 +29,21 @@ namespace wt {
 
 // ================================================================ a2 scans
 
-constexpr int SCAN_THREADS = 512;
-// values per thread of a scan tile: 8 for the scans that read a bitmap's
-// 512-bit blocks themselves (their loads want bytes in flight), 4 for the
-// scans of per-tile / per-node values (latency-bound: more, smaller CTAs
-// start their look-back sooner; cfg5 build 11.95 -> 11.77 ms)
+// CTA sizes: 512 threads for the scans that read a bitmap's 512-bit blocks
+// themselves (SCAN_ITEMS_BITS = 8 blocks per thread: their loads want bytes in
+// flight), 1024 for the scans of per-tile / per-node values (4 per thread:
+// latency-bound -- fewer tiles shorten the look-back; 512 threads: cfg5 preps
+// 0.54 ms per build, 1024: 0.45).  A k_prep launch hosts two scans in CTAs of
+// one size, that of its first scan.
+constexpr int SCAN_THREADS_BITS = 512;
+constexpr int SCAN_THREADS_VALS = 1024;
 constexpr int SCAN_ITEMS_BITS = 8;
 #ifndef WT_SCAN_ITEMS_V
 #define WT_SCAN_ITEMS_V 4
 #endif
 constexpr int SCAN_ITEMS_VALS = WT_SCAN_ITEMS_V;
-constexpr int SCAN_TILE_MIN = SCAN_THREADS * (SCAN_ITEMS_VALS < SCAN_ITEMS_BITS ? SCAN_ITEMS_VALS : SCAN_ITEMS_BITS);
+// the smallest scan tile (sizes the look-back state: an upper bound on the tiles of any scan)
+constexpr int SCAN_TILE_MIN = SCAN_THREADS_BITS * (SCAN_ITEMS_VALS < SCAN_ITEMS_BITS ? SCAN_ITEMS_VALS : SCAN_ITEMS_BITS);
 
 // Scan ops whose values are the popcounts of consecutive 512-bit blocks of a
 // bitmap (`bits`): scan_tile loads the tile's blocks itself, coalesced.
@@ -49,19 +53,22 @@ struct ScanOfBits {
 };
 
 // Exclusive scan of uint64 values over [0, count) with a decoupled look-back.
-// Op supplies load(i) and store(i, exclusive, value).  One CTA scans one tile
-// of SCAN_TILE values; tile ids come from an atomic ticket (forward progress).
+// Op supplies load(i) and store(i, exclusive, value).  One CTA of NT threads
+// scans one tile of NT * items values; tile ids come from an atomic ticket
+// (forward progress).
 template <class Op>
 constexpr int scan_items_of() { return ScanOfBits<Op>::value ? SCAN_ITEMS_BITS : SCAN_ITEMS_VALS; }
 template <class Op>
-constexpr uint64_t scan_tile_of() { return (uint64_t)SCAN_THREADS * scan_items_of<Op>(); }
+constexpr int scan_threads_of() { return ScanOfBits<Op>::value ? SCAN_THREADS_BITS : SCAN_THREADS_VALS; }
+template <class Op, int NT = scan_threads_of<Op>()>
+constexpr uint64_t scan_tile_of() { return (uint64_t)NT * scan_items_of<Op>(); }
 
-template <class Op>
+template <class Op, int NT>
 __device__ __forceinline__ void scan_tile(const Op& op, uint64_t count, const LookbackState& status,
                                           uint32_t* tile_counter, uint32_t epoch) {
   constexpr int SCAN_ITEMS = scan_items_of<Op>();
-  constexpr uint64_t SCAN_TILE = scan_tile_of<Op>();
-  __shared__ uint64_t s_warp[SCAN_THREADS / 32];
+  constexpr uint64_t SCAN_TILE = scan_tile_of<Op, NT>();
+  __shared__ uint64_t s_warp[NT / 32];
   __shared__ uint64_t s_P;
   __shared__ uint32_t s_tile;
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
@@ -71,12 +78,12 @@ __device__ __forceinline__ void scan_tile(const Op& op, uint64_t count, const Lo
   uint64_t v[SCAN_ITEMS];
   uint64_t tsum = 0;
   if constexpr (ScanOfBits<Op>::value) {
-    // the tile's blocks as 16-byte chunks, chunk c read by thread c % SCAN_THREADS
+    // the tile's blocks as 16-byte chunks, chunk c read by thread c % NT
     // (a warp reads 512 consecutive bytes per load); 4 consecutive lanes
     // hold one block: two shuffles sum it, its first lane stores the count
     __shared__ __align__(16) uint32_t s_cnt[SCAN_TILE];
     static_assert(SCAN_ITEMS % 4 == 0, "16-byte item loads");
-    constexpr uint32_t CH = 4 * SCAN_TILE / SCAN_THREADS;  // chunks per thread
+    constexpr uint32_t CH = 4 * SCAN_TILE / NT;  // chunks per thread
     const uint4* src = reinterpret_cast<const uint4*>(op.bits) + 4 * tile * SCAN_TILE;
     const uint64_t t0 = tile * SCAN_TILE;  // (a surplus CTA's tile lies past count: no chunks)
     const uint64_t nch = t0 < count ? 4 * min((uint64_t)SCAN_TILE, count - t0) : 0;
@@ -85,7 +92,7 @@ __device__ __forceinline__ void scan_tile(const Op& op, uint64_t count, const Lo
       uint32_t c[8];
 #pragma unroll
       for (uint32_t k = 0; k < 8; ++k) {
-        const uint32_t ch = threadIdx.x + SCAN_THREADS * (j0 + k);
+        const uint32_t ch = threadIdx.x + NT * (j0 + k);
         const uint4 q = ch < nch ? ldg_nc_v4(src + ch) : make_uint4(0, 0, 0, 0);
         c[k] = (uint32_t)(__popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w));
       }
@@ -93,7 +100,7 @@ __device__ __forceinline__ void scan_tile(const Op& op, uint64_t count, const Lo
       for (uint32_t k = 0; k < 8; ++k) {
         c[k] += __shfl_xor_sync(FULL, c[k], 1);
         c[k] += __shfl_xor_sync(FULL, c[k], 2);
-        if ((threadIdx.x & 3) == 0) s_cnt[(threadIdx.x + SCAN_THREADS * (j0 + k)) >> 2] = c[k];
+        if ((threadIdx.x & 3) == 0) s_cnt[(threadIdx.x + NT * (j0 + k)) >> 2] = c[k];
       }
     }
     __syncthreads();
@@ -119,16 +126,33 @@ __device__ __forceinline__ void scan_tile(const Op& op, uint64_t count, const Lo
   const uint64_t incl = warp_incl_scan_u64(tsum);
   if (lane == 31) s_warp[warp] = incl;
   __syncthreads();
-  if (warp == 0) {
-    const uint64_t w = (lane < SCAN_THREADS / 32) ? s_warp[lane] : 0;
-    const uint64_t wi = warp_incl_scan_u64(w);
-    const uint64_t total = __shfl_sync(FULL, wi, 31);
-    if (lane < SCAN_THREADS / 32) s_warp[lane] = wi - w;
-    const uint64_t P = lookback(status, tile, total, epoch);
-    if (lane == 0) s_P = P;
+  uint64_t run;
+  if constexpr (ScanOfBits<Op>::value) {
+    // (the bitmap scans fill a wave of CTAs that still stream their blocks: a
+    // whole CTA polling its predecessors slowed cfg2's final scan 0.049 -> 0.052 ms)
+    if (warp == 0) {
+      const uint64_t w = (lane < NT / 32) ? s_warp[lane] : 0;
+      const uint64_t wi = warp_incl_scan_u64(w);
+      const uint64_t total = __shfl_sync(FULL, wi, 31);
+      if (lane < NT / 32) s_warp[lane] = wi - w;
+      const uint64_t P = lookback(status, tile, total, epoch);
+      if (lane == 0) s_P = P;
+    }
+    __syncthreads();
+    run = s_P + s_warp[warp] + incl - tsum;
+  } else {
+    // the look-back by the whole CTA: one round trip covers NT predecessors
+    __shared__ uint64_t s_sum[NT / 32];
+    __shared__ uint32_t s_has[NT / 32];
+    if (warp == 0) {
+      const uint64_t w = (lane < NT / 32) ? s_warp[lane] : 0;
+      const uint64_t wi = warp_incl_scan_u64(w);
+      if (lane < NT / 32) s_warp[lane] = wi - w;
+      if (lane == 31) s_P = wi;  // the tile's total
+    }
+    __syncthreads();
+    run = block_lookback<NT>(status, tile, s_P, epoch, s_sum, s_has) + s_warp[warp] + incl - tsum;
   }
-  __syncthreads();
-  uint64_t run = s_P + s_warp[warp] + incl - tsum;
 #pragma unroll
   for (int k = 0; k < SCAN_ITEMS; ++k) {
     if (base + k < count) op.store(base + k, run, v[k]);
@@ -137,11 +161,11 @@ __device__ __forceinline__ void scan_tile(const Op& op, uint64_t count, const Lo
 }
 
 template <class Op>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan(Op op, uint64_t count, LookbackState status,
-                                                       uint32_t* tile_counter, uint32_t epoch,
-                                                       const int32_t* __restrict__ flag) {
+__global__ void __launch_bounds__(scan_threads_of<Op>()) k_scan(Op op, uint64_t count, LookbackState status,
+                                                                uint32_t* tile_counter, uint32_t epoch,
+                                                                const int32_t* __restrict__ flag) {
   if (*flag) return;
-  scan_tile(op, count, status, tile_counter, epoch);
+  scan_tile<Op, scan_threads_of<Op>()>(op, count, status, tile_counter, epoch);
 }
 
 // Two independent scans (each with its own look-back state and ticket) and a
@@ -157,20 +181,21 @@ struct ZeroFill {
   uint64_t n1;
 };
 template <class OpA, class OpB>
-__global__ void __launch_bounds__(SCAN_THREADS) k_prep(OpA a, uint64_t na, LookbackState sta, uint32_t* ca, uint32_t ea,
-                                                       OpB b, uint64_t nb, LookbackState stb, uint32_t* cb, uint32_t eb,
-                                                       ZeroFill z, const int32_t* __restrict__ flag) {
+__global__ void __launch_bounds__(scan_threads_of<OpA>())
+    k_prep(OpA a, uint64_t na, LookbackState sta, uint32_t* ca, uint32_t ea, OpB b, uint64_t nb, LookbackState stb,
+           uint32_t* cb, uint32_t eb, ZeroFill z, const int32_t* __restrict__ flag) {
+  constexpr int NT = scan_threads_of<OpA>();  // (both scans in CTAs of the first one's size)
   pdl_wait();
   if (*flag) return;
-  const uint32_t ga = (uint32_t)((na + scan_tile_of<OpA>() - 1) / scan_tile_of<OpA>()),
-                 gb = (uint32_t)((nb + scan_tile_of<OpB>() - 1) / scan_tile_of<OpB>());
+  const uint32_t ga = (uint32_t)((na + scan_tile_of<OpA, NT>() - 1) / scan_tile_of<OpA, NT>()),
+                 gb = (uint32_t)((nb + scan_tile_of<OpB, NT>() - 1) / scan_tile_of<OpB, NT>());
   if (blockIdx.x < ga) {
-    scan_tile(a, na, sta, ca, ea);
+    scan_tile<OpA, NT>(a, na, sta, ca, ea);
   } else if (blockIdx.x < ga + gb) {
-    scan_tile(b, nb, stb, cb, eb);
+    scan_tile<OpB, NT>(b, nb, stb, cb, eb);
   } else {
-    const uint64_t nt = (uint64_t)(gridDim.x - ga - gb) * SCAN_THREADS;
-    const uint64_t t0 = (uint64_t)(blockIdx.x - ga - gb) * SCAN_THREADS + threadIdx.x;
+    const uint64_t nt = (uint64_t)(gridDim.x - ga - gb) * NT;
+    const uint64_t t0 = (uint64_t)(blockIdx.x - ga - gb) * NT + threadIdx.x;
     for (uint64_t i = t0; i < z.n0; i += nt) z.p0[i] = make_uint4(0, 0, 0, 0);
     for (uint64_t i = t0; i < z.n1; i += nt) z.p1[i] = make_uint4(0, 0, 0, 0);
   }
