@@ -169,8 +169,20 @@ __global__ void __launch_bounds__(32 * P2_WARPS, 6)
   const uint32_t gw = blockIdx.x * P2_WARPS + wid, nw = gridDim.x * P2_WARPS;  // this warp, all warps
   const uint32_t nwt = (uint32_t)((n + P2_WT - 1) / P2_WT);                   // warp tiles
   const uint64_t full_bytes = n & ~127ull;  // the tensor map's whole rows
+#ifndef WT_P2_ROUND_ROBIN
+  // a contiguous chunk of warp tiles per warp: its runs of B_1 are contiguous,
+  // so most boundary words are shared with the warp's own next tile instead of
+  // with another SM's at the same moment (pair 0.305 -> 0.298 ms on cfg2; a
+  // chunk per CTA with its warps round-robin inside it: 0.304; the general
+  // k_pairn measured slower with chunks and keeps round-robin tiles)
+  const uint32_t chunk = (nwt + nw - 1) / nw;
+#endif
   auto issue = [&](uint32_t it) {           // lane 0: the warp's it-th tile into ring slot it % P2_NB
+#ifndef WT_P2_ROUND_ROBIN
+    const uint32_t tile = it < chunk ? gw * chunk + it : 0xffffffffu;
+#else
     const uint32_t tile = gw + it * nw;
+#endif
     if (tile >= nwt) return;
     const int b = (int)(it % P2_NB);
     fence_proxy_async_smem();
@@ -184,7 +196,11 @@ __global__ void __launch_bounds__(32 * P2_WARPS, 6)
   const uint64_t Z = n - *ones0;  // the zeros of level 0: B_1's ones' run starts here
   const uint32_t swz = lane & 7u;
   for (uint32_t it = 0;; ++it) {
+#ifndef WT_P2_ROUND_ROBIN
+    const uint32_t tile = it < chunk ? gw * chunk + it : 0xffffffffu;
+#else
     const uint32_t tile = gw + it * nw;
+#endif
     if (tile >= nwt) break;
     const int b = (int)(it % P2_NB);
     const uint64_t T0 = (uint64_t)tile * P2_WT;
