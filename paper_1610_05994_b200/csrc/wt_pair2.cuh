@@ -158,7 +158,9 @@ __global__ void __launch_bounds__(32 * P2_WARPS, 6)
             unsigned long long* __restrict__ SB0, uint64_t nsb, uint32_t* __restrict__ B1,
             const int32_t* __restrict__ flag, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ unsigned char p2_raw[];
-  P2Smem& sm = *reinterpret_cast<P2Smem*>((reinterpret_cast<uintptr_t>(p2_raw) + 1023) & ~uintptr_t(1023));
+  // (an offset from the __shared__ array, not an integer round trip: the
+  // compiler keeps the shared address space -- LDS / STS instead of generic loads)
+  P2Smem& sm = *reinterpret_cast<P2Smem*>(p2_raw + ((1024u - (smem_u32(p2_raw) & 1023u)) & 1023u));
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < 256; i += 32 * P2_WARPS) sm.lut[i] = p2_lut_entry(i);
   if (lane == 0) {

@@ -209,7 +209,9 @@ __global__ void __launch_bounds__(32 * PN_WARPS, 6)
   using C = PnCfg<T>;
   constexpr int E = C::E, EH = C::EH, WT = C::WT, NH = C::NH;
   extern __shared__ unsigned char pn_raw[];
-  PnSmem& sm = *reinterpret_cast<PnSmem*>((reinterpret_cast<uintptr_t>(pn_raw) + 1023) & ~uintptr_t(1023));
+  // (an offset from the __shared__ array, not an integer round trip: the
+  // compiler keeps the shared address space -- LDS / STS instead of generic loads)
+  PnSmem& sm = *reinterpret_cast<PnSmem*>(pn_raw + ((1024u - (smem_u32(pn_raw) & 1023u)) & 1023u));
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < 256; i += 32 * PN_WARPS) sm.lut[i] = p2_lut_entry(i);
   if (lane == 0) {

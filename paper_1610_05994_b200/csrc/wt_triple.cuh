@@ -340,7 +340,9 @@ __global__ void __launch_bounds__(32 * PN_WARPS, WT_TR_MINB)
   using C = TrCfg<T>;
   constexpr int E = C::E, EH = E / 2, WT = C::WT, UG = C::UG, US = C::US, NU = C::NU;
   extern __shared__ unsigned char tr_raw[];
-  TrSmem& sm = *reinterpret_cast<TrSmem*>((reinterpret_cast<uintptr_t>(tr_raw) + 1023) & ~uintptr_t(1023));
+  // (an offset from the __shared__ array, not an integer round trip: the
+  // compiler keeps the shared address space -- LDS / STS instead of generic loads)
+  TrSmem& sm = *reinterpret_cast<TrSmem*>(tr_raw + ((1024u - (smem_u32(tr_raw) & 1023u)) & 1023u));
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < 256; i += 32 * PN_WARPS) {
     sm.lut[i] = p2_lut_entry(i);
