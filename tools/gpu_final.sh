@@ -2,7 +2,7 @@
 # Round-end evidence: smoke, the GPU tests, the default bench line, the reference
 # arm, the dd step at N = 1, ncu launch lists + captures summarised on the box.
 set -u
-TAG=${TAG:-r02_v10}
+TAG=${TAG:-r02_v11}
 mkdir -p gpurun_out/profiles_out
 python -c 'import __graft_entry__ as g; g.build(); g.smoke()' > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 2400 python -m pytest tests -m gpu -q -x --timeout 1200 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log

@@ -3,7 +3,7 @@
 # roofline kernel(s), summarised ON THE BOX (tools/ncu_summary.py) into gpurun_out/profiles_out/
 # (the .ncu-rep files of the multi-kernel captures are too large to bring back).
 set -u
-TAG=${TAG:-r02_v10}
+TAG=${TAG:-r02_v11}
 mkdir -p gpurun_out/profiles_out
 cap() {  # cfg kregex skip count keep_rep
   local CFG=$1 K=$2 SKIP=$3 COUNT=$4 KEEP=$5
